@@ -1,0 +1,169 @@
+/*
+ * tickjoin_b200.h — C ABI of the B200-native QUAD tick pipeline.
+ *
+ * Drop-in boundary for the reference's QUAD path (arXiv 1411.3212,
+ * `tickjoin` package).  The reference has no FFI: its boundary is the Python
+ * tick API `Engine(MethodConfig(method="quad")).process_tick(batch)`
+ * (tickjoin/engine.py:137-259).  Each entry point below names the reference
+ * interface it replaces.  Plain pointers and sizes only; no torch types.
+ *
+ * Status codes: 0 = OK, negative = error.  The error codes map 1:1 onto the
+ * reference exception classes (tickjoin/errors.py:4-45) plus device errors.
+ * A context is single-threaded (like `Engine`); distinct
+ * contexts may run concurrently on distinct devices.
+ */
+#ifndef TICKJOIN_B200_H
+#define TICKJOIN_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TJ_ABI_VERSION 1
+
+/* status codes — errors.py:4-45 */
+#define TJ_OK 0
+#define TJ_E_EMPTY_BATCH (-1)      /* EmptyBatch        errors.py:7   */
+#define TJ_E_OUT_OF_BOUNDS (-2)    /* OutOfBounds       errors.py:11  */
+#define TJ_E_TILING_GAP (-5)       /* TilingGap         errors.py:23  */
+#define TJ_E_COUNT_MISMATCH (-6)   /* CountMismatch     errors.py:27  */
+#define TJ_E_DUPLICATE_RESULT (-7) /* DuplicateResult   errors.py:31  */
+#define TJ_E_BAD_CONFIG (-8)       /* BadConfig         errors.py:35  */
+#define TJ_E_INVALID_ARG (-20)     /* ValueError (bad rect, null ptr)  */
+#define TJ_E_CUDA (-100)
+#define TJ_E_NCCL (-101)
+#define TJ_E_OOM (-102)
+#define TJ_E_NO_DEVICE (-103)
+
+/* memory spaces of caller buffers */
+#define TJ_MEM_HOST 0   /* pageable or pinned host memory                  */
+#define TJ_MEM_DEVICE 1 /* device memory on the context's CUDA device      */
+
+/* rebuild policies — MethodConfig.rebuild, engine.py:70,163-170 */
+#define TJ_REBUILD_EVERY_TICK 0
+#define TJ_REBUILD_ADAPTIVE 1
+
+typedef struct tj_ctx tj_ctx;
+
+/* MethodConfig fields read by the QUAD path (engine.py:57-96). */
+typedef struct tj_config {
+  int32_t th_quad;               /* occupancy threshold, >= 1 (default 384)  */
+  int32_t l_max;                 /* deepest level, 1..12 (default 12)        */
+  int32_t covering_optimization; /* 1: covering subqueries skip bitmaps      */
+  int32_t rebuild;               /* TJ_REBUILD_*                             */
+  int32_t device;                /* CUDA device ordinal                      */
+  int32_t reserved;
+} tj_config;
+
+/* One tick of input as structure-of-arrays (TickBatch, geometry.py:58-64,
+ * converted AoS->SoA as in geometry.py:91-110).  Pointers live in `mem`. */
+typedef struct tj_tick_in {
+  int64_t n_obj;
+  const int64_t* obj_id;
+  const double* obj_x;
+  const double* obj_y;
+  int64_t n_q;
+  const int64_t* q_issuer;
+  const double* q_xa;
+  const double* q_ya;
+  const double* q_xb;
+  const double* q_yb;
+  int32_t mem;     /* TJ_MEM_HOST / TJ_MEM_DEVICE for the inputs        */
+  int32_t out_mem; /* where tj_tick_out buffers should be delivered     */
+} tj_tick_in;
+
+/* Per-query results as CSR in input-query order; ids ascending per query
+ * (ResultSet.by_query, decode.py:23-37).  Library-owned; valid until the
+ * next tj_tick or tj_destroy on the same context. */
+typedef struct tj_tick_out {
+  int64_t n_q;
+  int64_t n_results;
+  const int64_t* offsets; /* n_q + 1 */
+  const int64_t* ids;     /* n_results */
+  int32_t mem;
+  int32_t reserved;
+} tj_tick_out;
+
+/* TickStats counters (engine.py:99-121) plus device stage times. */
+typedef struct tj_stats {
+  int64_t n_objects, n_queries;
+  int64_t containment_tests;   /* engine.py:225 */
+  int64_t decoded_bits;        /* engine.py:279 */
+  int64_t subq_intersecting;   /* engine.py:213 */
+  int64_t subq_covering;       /* engine.py:214 */
+  int64_t covering_results;    /* engine.py:245 */
+  int64_t active_cells;        /* engine.py:263 */
+  int64_t results_total;       /* engine.py:248 */
+  int64_t occ_sum, occ_sumsq;  /* occupancy moments over non-empty leaves */
+  int64_t n_leaves, l_deep, n_tasks, bitmap_words, n_subqueries, work_units;
+  int32_t rebuilt;             /* 1 if the index was (re)built this tick */
+  int32_t retries;             /* capacity-growth replays of this tick    */
+  double t_index_ms, t_filter_ms, t_decode_ms, t_merge_ms, t_total_ms; /* CUDA events */
+  double mbr[4];
+  double t_join_ms;            /* the per-leaf join kernel alone (CUDA events) */
+  int64_t task_objects;        /* P_a: objects in leaves that are join tasks   */
+  int64_t task_subqueries;     /* S_a: intersecting subqueries in join tasks   */
+  int64_t kernel_launches;     /* kernels this call launched (all attempts)    */
+} tj_stats;
+
+/* Reference-order index view (QuadIndex, quadtree.py:41-67). */
+typedef struct tj_index_info {
+  double mbr[4];
+  int32_t th_quad, l_max, l_deep, reserved;
+  int64_t n_leaves; /* len(leaves) */
+  int64_t n_cells;  /* len(zmap) = 4**l_deep */
+} tj_index_info;
+
+/* ---- lifecycle -------------------------------------------------------- */
+int tj_abi_version(void);
+int tj_device_count(int* count);
+/* Engine.__init__ + MethodConfig.validate (engine.py:73-88,140-145). */
+int tj_create(const tj_config* cfg, tj_ctx** out);
+int tj_destroy(tj_ctx* ctx);
+/* Last error message of a context (or of the last failed tj_create if ctx is NULL). */
+const char* tj_last_error(const tj_ctx* ctx);
+
+/* ---- the hot path ------------------------------------------------------ */
+/* Engine.process_tick for method "quad" (engine.py:178-259): index build,
+ * query->leaf scatter, per-leaf bitmap join, decode, canonical merge. */
+int tj_tick(tj_ctx* ctx, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats);
+
+/* ---- introspection (parity tests; host copies, reference order) ------- */
+/* build_quadtree result: leaves ascending packed (level << 2*l_max | z),
+ * zmap packed ids per deepest cell (quadtree.py:74-158).  Null buffers: info only. */
+int tj_get_index(tj_ctx* ctx, tj_index_info* info, int64_t* leaves, int64_t leaves_cap,
+                 int64_t* zmap, int64_t zmap_cap);
+/* map_objects_quad (quadtree.py:161-165): packed leaf per input object. */
+int tj_get_object_cells(tj_ctx* ctx, int64_t* cells, int64_t cap);
+/* split_queries_quad output (quadtree.py:168-240), per query in ascending
+ * packed-leaf order: input query row, packed leaf, covering flag. */
+int tj_get_subqueries(tj_ctx* ctx, int64_t* count, int64_t* q_row, int64_t* cell,
+                      uint8_t* covering, int64_t cap);
+/* sort_by_cell (directory.py:119-158): objects' input rows in directory order;
+ * indices into the subquery list for the intersecting / covering blocks. */
+int tj_get_directory(tj_ctx* ctx, int64_t* obj_rows, int64_t obj_cap, int64_t* isq, int64_t* n_isq,
+                     int64_t* cov, int64_t* n_cov, int64_t sq_cap);
+/* Per-task linear bitmaps + popcounts (bitmap.py:70-119) for tasks in
+ * ascending packed cell order; task_woff has n_tasks + 1 entries. */
+int tj_get_bitmaps(tj_ctx* ctx, int64_t* n_tasks, int64_t* n_words, int64_t* task_cell,
+                   int64_t* task_nobj, int64_t* task_nisq, int64_t* task_woff, uint32_t* words,
+                   int64_t* counts, int64_t task_cap, int64_t word_cap, int64_t count_cap);
+/* simulate_assignment over heaviest-first tasks (scheduler.py:31-54):
+ * greedy least-loaded assignment of task weights n_isq*n_obj. */
+int tj_get_imbalance(tj_ctx* ctx, int32_t sim_processors, int32_t heaviest_first, double* imbalance);
+
+/* The context's CUDA stream (cudaStream_t), for callers that time or order
+ * work against the tick with their own events. */
+int tj_get_stream(tj_ctx* ctx, void** stream);
+
+/* ---- pinned host buffers for end-to-end callers ------------------------ */
+int tj_host_alloc(int64_t bytes, void** ptr);
+int tj_host_free(void* ptr);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TICKJOIN_B200_H */

@@ -1,0 +1,250 @@
+"""ctypes binding of the native library `libtickjoin_b200.so` (include/tickjoin_b200.h).
+
+The library is built in-tree by `__graft_entry__.build()` (nvcc, sm_100a).
+There is no fallback: if the library or a CUDA device is missing, creating a
+context raises `DeviceError` loudly.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+from ctypes import POINTER, c_char_p, c_double, c_int, c_int32, c_int64, c_uint8, c_uint32, c_void_p
+from typing import Optional
+
+import numpy as np
+
+from . import errors
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libtickjoin_b200.so")
+
+TJ_MEM_HOST = 0
+TJ_MEM_DEVICE = 1
+TJ_REBUILD_EVERY_TICK = 0
+TJ_REBUILD_ADAPTIVE = 1
+
+_ERRORS = {
+    -1: errors.EmptyBatch,
+    -2: errors.OutOfBounds,
+    -5: errors.TilingGap,
+    -6: errors.CountMismatch,
+    -7: errors.DuplicateResult,
+    -8: errors.BadConfig,
+    -20: ValueError,
+    -100: errors.DeviceError,
+    -101: errors.DeviceError,
+    -102: errors.DeviceError,
+    -103: errors.DeviceError,
+}
+
+
+class TjConfig(ctypes.Structure):
+    _fields_ = [("th_quad", c_int32), ("l_max", c_int32), ("covering_optimization", c_int32),
+                ("rebuild", c_int32), ("device", c_int32), ("reserved", c_int32)]
+
+
+class TjTickIn(ctypes.Structure):
+    _fields_ = [("n_obj", c_int64), ("obj_id", c_void_p), ("obj_x", c_void_p), ("obj_y", c_void_p),
+                ("n_q", c_int64), ("q_issuer", c_void_p), ("q_xa", c_void_p), ("q_ya", c_void_p),
+                ("q_xb", c_void_p), ("q_yb", c_void_p), ("mem", c_int32), ("out_mem", c_int32)]
+
+
+class TjTickOut(ctypes.Structure):
+    _fields_ = [("n_q", c_int64), ("n_results", c_int64), ("offsets", c_void_p), ("ids", c_void_p),
+                ("mem", c_int32), ("reserved", c_int32)]
+
+
+class TjStats(ctypes.Structure):
+    _fields_ = [(k, c_int64) for k in (
+        "n_objects", "n_queries", "containment_tests", "decoded_bits", "subq_intersecting",
+        "subq_covering", "covering_results", "active_cells", "results_total", "occ_sum", "occ_sumsq",
+        "n_leaves", "l_deep", "n_tasks", "bitmap_words", "n_subqueries", "work_units")] + [
+        ("rebuilt", c_int32), ("retries", c_int32)] + [
+        (k, c_double) for k in ("t_index_ms", "t_filter_ms", "t_decode_ms", "t_merge_ms", "t_total_ms")] + [
+        ("mbr", c_double * 4), ("t_join_ms", c_double), ("task_objects", c_int64), ("task_subqueries", c_int64),
+        ("kernel_launches", c_int64)]
+
+
+class TjIndexInfo(ctypes.Structure):
+    _fields_ = [("mbr", c_double * 4), ("th_quad", c_int32), ("l_max", c_int32), ("l_deep", c_int32),
+                ("reserved", c_int32), ("n_leaves", c_int64), ("n_cells", c_int64)]
+
+
+EXPORTED = (
+    "tj_abi_version", "tj_device_count", "tj_create", "tj_destroy", "tj_last_error", "tj_tick",
+    "tj_get_index", "tj_get_object_cells", "tj_get_subqueries", "tj_get_directory", "tj_get_bitmaps",
+    "tj_get_imbalance", "tj_get_stream", "tj_host_alloc", "tj_host_free",
+)
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def load_library() -> ctypes.CDLL:
+    """Load the in-tree native library (raises DeviceError if it is not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise errors.DeviceError(
+            f"native library missing: {LIB_PATH} (run __graft_entry__.build()); there is no CPU fallback")
+    lib = ctypes.CDLL(LIB_PATH)
+    i64p = POINTER(c_int64)
+    lib.tj_abi_version.restype = c_int
+    lib.tj_device_count.argtypes = [POINTER(c_int)]
+    lib.tj_create.argtypes = [POINTER(TjConfig), POINTER(c_void_p)]
+    lib.tj_destroy.argtypes = [c_void_p]
+    lib.tj_last_error.argtypes = [c_void_p]
+    lib.tj_last_error.restype = c_char_p
+    lib.tj_tick.argtypes = [c_void_p, POINTER(TjTickIn), POINTER(TjTickOut), POINTER(TjStats)]
+    lib.tj_get_index.argtypes = [c_void_p, POINTER(TjIndexInfo), c_void_p, c_int64, c_void_p, c_int64]
+    lib.tj_get_object_cells.argtypes = [c_void_p, c_void_p, c_int64]
+    lib.tj_get_subqueries.argtypes = [c_void_p, i64p, c_void_p, c_void_p, c_void_p, c_int64]
+    lib.tj_get_directory.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, i64p, c_void_p, i64p, c_int64]
+    lib.tj_get_bitmaps.argtypes = [c_void_p, i64p, i64p] + [c_void_p] * 6 + [c_int64] * 3
+    lib.tj_get_imbalance.argtypes = [c_void_p, c_int32, c_int32, POINTER(c_double)]
+    lib.tj_get_stream.argtypes = [c_void_p, POINTER(c_void_p)]
+    lib.tj_host_alloc.argtypes = [c_int64, POINTER(c_void_p)]
+    lib.tj_host_free.argtypes = [c_void_p]
+    _lib = lib
+    return lib
+
+
+def device_count() -> int:
+    n = c_int(0)
+    load_library().tj_device_count(ctypes.byref(n))
+    return n.value
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data if a.size else 0
+
+
+class NativeContext:
+    """Owns one `tj_ctx` (one CUDA device, one stream)."""
+
+    def __init__(self, th_quad: int, l_max: int, covering: bool, rebuild: int = 0, device: int = 0):
+        self.lib = load_library()
+        cfg = TjConfig(th_quad, l_max, 1 if covering else 0, rebuild, device, 0)
+        h = c_void_p()
+        rc = self.lib.tj_create(ctypes.byref(cfg), ctypes.byref(h))
+        if rc != 0:
+            self._raise(rc, None)
+        self.h = h
+        self.device = device
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.tj_destroy(self.h)
+            self.h = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _raise(self, rc: int, h) -> None:
+        msg = self.lib.tj_last_error(h).decode(errors="replace") if self.lib else ""
+        cls = _ERRORS.get(rc, errors.DeviceError)
+        raise cls(msg or f"native error {rc}")
+
+    def _check(self, rc: int) -> None:
+        if rc != 0:
+            self._raise(rc, self.h)
+
+    # -- hot path ---------------------------------------------------------
+    def tick_host(self, ids, xs, ys, qids, qxa, qya, qxb, qyb):
+        """Host arrays in, host CSR out (copied into fresh NumPy arrays)."""
+        arrs = [np.ascontiguousarray(ids, np.int64), np.ascontiguousarray(xs, np.float64),
+                np.ascontiguousarray(ys, np.float64), np.ascontiguousarray(qids, np.int64),
+                np.ascontiguousarray(qxa, np.float64), np.ascontiguousarray(qya, np.float64),
+                np.ascontiguousarray(qxb, np.float64), np.ascontiguousarray(qyb, np.float64)]
+        tin = TjTickIn(len(arrs[0]), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[3]),
+                       _ptr(arrs[3]), _ptr(arrs[4]), _ptr(arrs[5]), _ptr(arrs[6]), _ptr(arrs[7]),
+                       TJ_MEM_HOST, TJ_MEM_HOST)
+        tout = TjTickOut()
+        st = TjStats()
+        self._check(self.lib.tj_tick(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
+        m = tout.n_q
+        offs = np.ctypeslib.as_array(ctypes.cast(tout.offsets, POINTER(c_int64)), shape=(m + 1,)).copy()
+        if tout.n_results:
+            res = np.ctypeslib.as_array(ctypes.cast(tout.ids, POINTER(c_int64)),
+                                        shape=(tout.n_results,)).copy()
+        else:
+            res = np.zeros(0, np.int64)
+        return offs, res, st
+
+    def tick_ptrs(self, n, ids, xs, ys, m, qids, qxa, qya, qxb, qyb, mem: int, out_mem: int):
+        """Raw-pointer tick (device tensors or pinned host buffers); returns (TjTickOut, TjStats)."""
+        tin = TjTickIn(n, ids, xs, ys, m, qids, qxa, qya, qxb, qyb, mem, out_mem)
+        tout = TjTickOut()
+        st = TjStats()
+        self._check(self.lib.tj_tick(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
+        return tout, st
+
+    def stream(self) -> int:
+        s = c_void_p()
+        self._check(self.lib.tj_get_stream(self.h, ctypes.byref(s)))
+        return s.value or 0
+
+    # -- introspection (reference order) ----------------------------------
+    def index(self):
+        info = TjIndexInfo()
+        self._check(self.lib.tj_get_index(self.h, ctypes.byref(info), None, 0, None, 0))
+        leaves = np.zeros(info.n_leaves, np.int64)
+        zmap = np.zeros(info.n_cells, np.int64)
+        self._check(self.lib.tj_get_index(self.h, ctypes.byref(info), _ptr(leaves), len(leaves),
+                                          _ptr(zmap), len(zmap)))
+        return dict(mbr=tuple(info.mbr), l_deep=info.l_deep, leaves=leaves, zmap=zmap)
+
+    def object_cells(self, n: int) -> np.ndarray:
+        out = np.zeros(n, np.int64)
+        self._check(self.lib.tj_get_object_cells(self.h, _ptr(out), n))
+        return out
+
+    def subqueries(self):
+        cnt = c_int64(0)
+        self._check(self.lib.tj_get_subqueries(self.h, ctypes.byref(cnt), None, None, None, 0))
+        S = cnt.value
+        q = np.zeros(S, np.int64)
+        cell = np.zeros(S, np.int64)
+        cov = np.zeros(S, np.uint8)
+        self._check(self.lib.tj_get_subqueries(self.h, ctypes.byref(cnt), _ptr(q), _ptr(cell), _ptr(cov), S))
+        return q, cell, cov.astype(bool)
+
+    def directory(self, n: int):
+        ni, nc = c_int64(0), c_int64(0)
+        self._check(self.lib.tj_get_directory(self.h, None, 0, None, ctypes.byref(ni), None,
+                                              ctypes.byref(nc), 0))
+        rows = np.zeros(n, np.int64)
+        isq = np.zeros(ni.value, np.int64)
+        cov = np.zeros(nc.value, np.int64)
+        cap = max(ni.value, nc.value)
+        self._check(self.lib.tj_get_directory(self.h, _ptr(rows), n, _ptr(isq), ctypes.byref(ni), _ptr(cov),
+                                              ctypes.byref(nc), cap))
+        return rows, isq, cov
+
+    def bitmaps(self):
+        nt, nw = c_int64(0), c_int64(0)
+        self._check(self.lib.tj_get_bitmaps(self.h, ctypes.byref(nt), ctypes.byref(nw), None, None, None, None,
+                                            None, None, 0, 0, 0))
+        T, W = nt.value, nw.value
+        cell = np.zeros(T, np.int64)
+        nobj = np.zeros(T, np.int64)
+        nisq = np.zeros(T, np.int64)
+        woff = np.zeros(T + 1, np.int64)
+        words = np.zeros(W, np.uint32)
+        # counts: one per intersecting subquery of a task; bounded by W
+        counts = np.zeros(max(W, 1), np.int64)
+        self._check(self.lib.tj_get_bitmaps(self.h, ctypes.byref(nt), ctypes.byref(nw), _ptr(cell), _ptr(nobj),
+                                            _ptr(nisq), _ptr(woff), _ptr(words), _ptr(counts), T, W,
+                                            len(counts)))
+        return dict(cell=cell, nobj=nobj, nisq=nisq, woff=woff, words=words,
+                    counts=counts[: int(nisq.sum())])
+
+    def imbalance(self, sim_processors: int, heaviest_first: bool) -> float:
+        v = c_double(0.0)
+        self._check(self.lib.tj_get_imbalance(self.h, sim_processors, 1 if heaviest_first else 0,
+                                              ctypes.byref(v)))
+        return v.value

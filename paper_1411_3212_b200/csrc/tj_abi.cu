@@ -1,0 +1,843 @@
+// C ABI of the B200 QUAD tick pipeline (include/tickjoin_b200.h).
+//
+// Host side of the native library: context + device arena management, the
+// per-tick launch sequence (one stream, no host synchronisation between
+// stages; sizes live in DevHdr), capacity-overflow replay, result delivery,
+// and the reference-order introspection used by the parity tests.
+#include "tickjoin_b200.h"
+#include "tj_kernels.cuh"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+using namespace tj;
+
+namespace {
+
+std::string g_last_error;
+
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+
+}  // namespace
+
+struct tj_ctx {
+  tj_config cfg{};
+  int device = 0;
+  int num_sms = 148;
+  cudaStream_t st = nullptr;
+  cudaEvent_t ev[6] = {};
+  DevHdr* d_hdr = nullptr;
+  DevHdr* h_hdr = nullptr;  // pinned
+  int64_t* d_consts = nullptr;
+  std::string err;
+  // inputs
+  DBuf ids, xs, ys, qxa, qya, qxb, qyb;
+  // objects
+  DBuf code, okey0, okey1, oval0, oval1, sx, sy, sid;
+  // index
+  DBuf pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
+  // queries
+  DBuf crect, qwin, nsub, qsbase;
+  // subqueries
+  DBuf sqleaf, sqq, sqcov, sqcount, slotout, skey0, skey1, sval0, sval1;
+  // join / outputs
+  DBuf bitmap, stage, outids, outoff;
+  // scan / radix scratch
+  DBuf partial, rhist, roffs;
+  // pinned host outputs
+  void* h_off = nullptr;
+  size_t h_off_bytes = 0;
+  void* h_ids = nullptr;
+  size_t h_ids_bytes = 0;
+  // capacities of the dynamically sized arenas
+  int64_t cap_S = 0, cap_W = 0, cap_R = 0, cap_L = 0, cap_heavy = 0;
+  int64_t last_L = 0;
+  // last tick, for introspection
+  bool have = false;
+  int64_t n = 0, m = 0;
+  DevHdr last{};
+  Dev dv{};
+  int obj_passes = 0, sq_passes = 0;
+};
+
+namespace {
+
+int fail(tj_ctx* c, int code, const std::string& msg) {
+  if (c) c->err = msg;
+  g_last_error = msg;
+  return code;
+}
+
+#define TJ_CUDA(call)                                                                   \
+  do {                                                                                  \
+    cudaError_t e_ = (call);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(c, e_ == cudaErrorMemoryAllocation ? TJ_E_OOM : TJ_E_CUDA,            \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));                  \
+  } while (0)
+
+// grow-only device buffer
+int ensure(tj_ctx* c, DBuf& b, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (b.bytes >= bytes) return TJ_OK;
+  if (b.p) {
+    cudaStreamSynchronize(c->st);
+    cudaFree(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
+  }
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(c, TJ_E_OOM, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  return TJ_OK;
+}
+
+int ensure_host(tj_ctx* c, void*& p, size_t& have, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  if (have >= bytes) return TJ_OK;
+  if (p) cudaFreeHost(p);
+  p = nullptr;
+  have = 0;
+  cudaError_t e = cudaMallocHost(&p, bytes);
+  if (e != cudaSuccess) return fail(c, TJ_E_OOM, std::string("cudaMallocHost: ") + cudaGetErrorString(e));
+  have = bytes;
+  return TJ_OK;
+}
+
+template <typename T>
+T* P(const DBuf& b) { return reinterpret_cast<T*>(b.p); }
+
+int bits_for(int64_t v) {  // bits needed to represent values in [0, v]
+  int b = 0;
+  while (b < 63 && (v >> b) != 0) ++b;
+  return b;
+}
+
+int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+inline int grid_for(tj_ctx* c, int64_t items, int per_sm = 8) {
+  int64_t g = ceil_div(items, 256);
+  int64_t cap = (int64_t)c->num_sms * per_sm;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+// Allocate everything whose size depends only on n, m and the config.
+int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
+  const int lmax = c->cfg.l_max;
+  const int F = std::min(lmax, kDenseTop);
+  const int D = lmax - F;
+  const int64_t th = c->cfg.th_quad;
+  int rc;
+#define ENS(buf, bytes) \
+  if ((rc = ensure(c, c->buf, (size_t)(bytes))) != TJ_OK) return rc
+  // leaves: <= 4 + 3*(#split nodes); a level holds <= n/(th+1) split nodes
+  const int64_t Zmax = int64_t(1) << (2 * lmax);
+  int64_t lcap = 4 + 3 * (int64_t)(lmax > 1 ? lmax - 1 : 0) * (n / (th + 1) + 1);
+  c->cap_L = std::min(lcap, Zmax);
+  c->cap_heavy = D > 0 ? std::min<int64_t>(n / (th + 1) + 1, int64_t(1) << (2 * F)) : 0;
+  ENS(code, n * 4);
+  ENS(okey0, n * 4);
+  ENS(okey1, n * 4);
+  ENS(oval0, n * 4);
+  ENS(oval1, n * 4);
+  ENS(sx, n * 8);
+  ENS(sy, n * 8);
+  ENS(sid, n * 8);
+  ENS(pyr, pyr_off(F + 1) * 4);
+  ENS(heavy, (int64_t(1) << (2 * F)) * 4);
+  ENS(sub, std::max<int64_t>(1, c->cap_heavy * sub_size(D)) * 4);
+  ENS(clev, Zmax);
+  ENS(zmap, Zmax * 4);
+  ENS(lcode, c->cap_L * 4);
+  ENS(lnobj, c->cap_L * 4);
+  ENS(lobase, c->cap_L * 4);
+  ENS(lnisq, c->cap_L * 4);
+  ENS(lncov, c->cap_L * 4);
+  ENS(lsbase, c->cap_L * 4);
+  ENS(lwoff, c->cap_L * 8);
+  ENS(lubase, c->cap_L * 8);
+  ENS(crect, m * sizeof(Rect4));
+  ENS(qwin, m * sizeof(int4));
+  ENS(nsub, m * 4);
+  ENS(qsbase, m * 4);
+  ENS(outoff, (m + 1) * 8);
+  ENS(partial, 1024 * 8);
+  const int Gr = 2 * c->num_sms;
+  ENS(rhist, (int64_t)256 * Gr * 4);
+  ENS(roffs, (int64_t)256 * Gr * 8);
+  if (c->cap_S == 0) c->cap_S = 4 * m + 256;
+  if (c->cap_W == 0) c->cap_W = 8 * c->cap_S + 4096;
+  if (c->cap_R == 0) c->cap_R = 16 * m + 4096;
+#undef ENS
+  return TJ_OK;
+}
+
+int prepare_dynamic(tj_ctx* c) {
+  int rc;
+#define ENS(buf, bytes) \
+  if ((rc = ensure(c, c->buf, (size_t)(bytes))) != TJ_OK) return rc
+  ENS(sqleaf, c->cap_S * 4);
+  ENS(sqq, c->cap_S * 4);
+  ENS(sqcov, c->cap_S);
+  ENS(sqcount, c->cap_S * 4);
+  ENS(slotout, c->cap_S * 8);
+  ENS(skey0, c->cap_S * 4);
+  ENS(skey1, c->cap_S * 4);
+  ENS(sval0, c->cap_S * 4);
+  ENS(sval1, c->cap_S * 4);
+  ENS(bitmap, c->cap_W * 4);
+  ENS(stage, c->cap_R * 8);
+  ENS(outids, c->cap_R * 8);
+#undef ENS
+  return TJ_OK;
+}
+
+void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys, const double* qxa,
+              const double* qya, const double* qxb, const double* qyb) {
+  Dev& d = c->dv;
+  const int lmax = c->cfg.l_max;
+  const int F = std::min(lmax, kDenseTop);
+  d.h = c->d_hdr;
+  d.ids = ids;
+  d.xs = xs;
+  d.ys = ys;
+  d.qxa = qxa;
+  d.qya = qya;
+  d.qxb = qxb;
+  d.qyb = qyb;
+  d.code = P<uint32_t>(c->code);
+  d.okey[0] = P<uint32_t>(c->okey0);
+  d.okey[1] = P<uint32_t>(c->okey1);
+  d.oval[0] = P<int32_t>(c->oval0);
+  d.oval[1] = P<int32_t>(c->oval1);
+  d.sx = P<double>(c->sx);
+  d.sy = P<double>(c->sy);
+  d.sid = P<int64_t>(c->sid);
+  d.pyr = P<uint32_t>(c->pyr);
+  d.heavy_map = P<int32_t>(c->heavy);
+  d.sub = P<uint32_t>(c->sub);
+  d.clev = P<uint8_t>(c->clev);
+  d.zmap = P<uint32_t>(c->zmap);
+  d.leaf_code = P<uint32_t>(c->lcode);
+  d.leaf_nobj = P<int32_t>(c->lnobj);
+  d.leaf_obase = P<int32_t>(c->lobase);
+  d.leaf_nisq = P<int32_t>(c->lnisq);
+  d.leaf_ncov = P<int32_t>(c->lncov);
+  d.leaf_sbase = P<int32_t>(c->lsbase);
+  d.leaf_woff = P<int64_t>(c->lwoff);
+  d.leaf_ubase = P<int64_t>(c->lubase);
+  d.crect = P<Rect4>(c->crect);
+  d.qwin = P<int4>(c->qwin);
+  d.nsub = P<int32_t>(c->nsub);
+  d.qsbase = P<int32_t>(c->qsbase);
+  d.sq_leaf = P<int32_t>(c->sqleaf);
+  d.sq_q = P<int32_t>(c->sqq);
+  d.sq_cov = P<uint8_t>(c->sqcov);
+  d.sq_count = P<int32_t>(c->sqcount);
+  d.slot_out = P<int64_t>(c->slotout);
+  d.skey[0] = P<uint32_t>(c->skey0);
+  d.skey[1] = P<uint32_t>(c->skey1);
+  d.sval[0] = P<int32_t>(c->sval0);
+  d.sval[1] = P<int32_t>(c->sval1);
+  d.bitmap = P<uint32_t>(c->bitmap);
+  d.stage = P<int64_t>(c->stage);
+  d.out_ids = P<int64_t>(c->outids);
+  d.out_off = P<int64_t>(c->outoff);
+  d.D = lmax - F;
+  d.SUB = sub_size(d.D);
+  d.sidx = d.oval[c->obj_passes & 1];
+  d.ssorted = d.sval[c->sq_passes & 1];
+}
+
+// stable LSD radix sort of (key, value) pairs over `passes` 8-bit digits
+void radix_sort(tj_ctx* c, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, int passes) {
+  const int Gr = 2 * c->num_sms;
+  ScanPlan sp{std::min(1024, 2 * c->num_sms), P<int64_t>(c->partial)};
+  for (int p = 0; p < passes; ++p) {
+    const int src = p & 1, dst = src ^ 1;
+    k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], n_ptr, c->d_hdr, 8 * p, P<uint32_t>(c->rhist));
+    scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)},
+                c->d_consts, c->d_hdr, (int64_t*)nullptr, c->st);
+    k_radix_downsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], v[src], k[dst], v[dst], n_ptr, c->d_hdr,
+                                                        8 * p, P<int64_t>(c->roffs));
+  }
+}
+
+// The per-tick launch sequence.  No host synchronisation inside.
+// Returns the number of kernels launched.
+int launch_tick(tj_ctx* c) {
+  cudaStream_t st = c->st;
+  Dev& d = c->dv;
+  DevHdr* h = c->d_hdr;
+  const int lmax = c->cfg.l_max;
+  const int F = std::min(lmax, kDenseTop);
+  const int D = lmax - F;
+  const int64_t n = c->n, m = c->m;
+  const int Gn = grid_for(c, n), Gm = grid_for(c, m);
+  const int Gbig = c->num_sms * 8;
+  ScanPlan sp{std::min(1024, 2 * c->num_sms), P<int64_t>(c->partial)};
+
+  cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
+  cudaMemsetAsync(d.leaf_nisq, 0, c->cap_L * 4, st);
+  cudaMemsetAsync(d.leaf_ncov, 0, c->cap_L * 4, st);
+
+  cudaEventRecord(c->ev[0], st);
+  // ---- K0 / K1: index build -------------------------------------------
+  k_mbr<<<Gn, 256, 0, st>>>(d);
+  k_monotone<<<Gn, 256, 0, st>>>(d);
+  k_finalize_mbr<<<1, 1, 0, st>>>(h);
+  k_codes<<<Gn, 256, 0, st>>>(d);
+  for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
+  if (D > 0) {
+    k_heavy<<<grid_for(c, int64_t(1) << (2 * F)), 256, 0, st>>>(d);
+    k_zero_sub<<<Gbig, 256, 0, st>>>(d);
+    k_sub_hist<<<Gn, 256, 0, st>>>(d);
+    for (int r = D - 1; r >= 1; --r) k_sub_level<<<Gbig, 256, 0, st>>>(d, r);
+  }
+  k_finalize_index<<<1, 1, 0, st>>>(h);
+  k_cell_level<<<Gbig, 256, 0, st>>>(d);
+  scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
+  k_check_caps<<<1, 1, 0, st>>>(h, 0, 8 * c->obj_passes, 8 * c->sq_passes);
+  k_obj_keys<<<Gn, 256, 0, st>>>(d);
+  radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
+  scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr, st);
+  k_gather<<<Gn, 256, 0, st>>>(d);
+  // ---- K2: query -> leaf scatter ----------------------------------------
+  k_query_count<<<Gm, 256, 0, st>>>(d);
+  scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
+  k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
+  k_query_fill<<<Gm, 256, 0, st>>>(d);
+  k_sq_keys<<<Gbig, 256, 0, st>>>(d);
+  radix_sort(c, d.skey, d.sval, &h->S, c->sq_passes);
+  scan_launch(sp, LeafSubIn{d.leaf_nisq, d.leaf_ncov}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
+              (int64_t*)nullptr, st);
+  k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
+  cudaEventRecord(c->ev[1], st);
+  // ---- K3: join -----------------------------------------------------------
+  scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h, &h->W, st);
+  scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h, &h->U, st);
+  k_check_caps<<<1, 1, 0, st>>>(h, 2, 0, 0);
+  k_zero_counts<<<Gbig, 256, 0, st>>>(d);
+  cudaEventRecord(c->ev[2], st);
+  k_join<<<c->num_sms * 8, kJoinThreads, 0, st>>>(d);
+  cudaEventRecord(c->ev[3], st);
+  // ---- K4: decode + canonical lists --------------------------------------
+  scan_launch(sp, SlotCntIn{d.sq_cov, d.sq_leaf, d.leaf_nobj, d.sq_count}, ExclOut<int64_t>{d.slot_out}, &h->S,
+              h, &h->R, st);
+  k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
+  k_query_offsets<<<Gm, 256, 0, st>>>(d);
+  k_decode<<<Gbig, 256, 0, st>>>(d);
+  k_cover<<<Gbig, 256, 0, st>>>(d);
+  cudaEventRecord(c->ev[4], st);
+  k_merge_runs<<<Gbig, 256, 0, st>>>(d);
+  k_sort_queries<<<c->num_sms * 4, 256, 0, st>>>(d);
+  cudaEventRecord(c->ev[5], st);
+  // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
+  const int scans = 7, singles = 23 + F + (D > 0 ? 3 + (D - 1) : 0);
+  return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles;
+}
+
+void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
+  DevHdr& H = *c->h_hdr;
+  std::memset(&H, 0, sizeof(DevHdr));
+  H.n = n;
+  H.m = m;
+  H.th = c->cfg.th_quad;
+  H.l_max = c->cfg.l_max;
+  H.F = std::min(c->cfg.l_max, kDenseTop);
+  H.covering = c->cfg.covering_optimization ? 1 : 0;
+  H.cap_S = c->cap_S;
+  H.cap_W = c->cap_W;
+  H.cap_R = c->cap_R;
+  H.cap_U = INT64_MAX;
+  H.cap_L = c->cap_L;
+  H.cap_heavy = c->cap_heavy;
+  H.kmin_x = H.kmin_y = ~0ull;
+  H.kmax_x = H.kmax_y = 0ull;
+  H.l_deep = 1;
+}
+
+int passes_for(int64_t maxkey) { return std::max(1, (bits_for(maxkey) + 7) / 8); }
+
+int check_launch(tj_ctx* c) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(c, TJ_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+  return TJ_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int tj_abi_version(void) { return TJ_ABI_VERSION; }
+
+int tj_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return TJ_OK;
+}
+
+const char* tj_last_error(const tj_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int tj_create(const tj_config* cfg, tj_ctx** out) {
+  tj_ctx* c = nullptr;
+  if (!cfg || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
+  // MethodConfig.validate for the quad method (engine.py:73-88)
+  if (cfg->th_quad < 1) return fail(c, TJ_E_BAD_CONFIG, "th_quad must be >= 1");
+  if (cfg->l_max < 1 || cfg->l_max > kMaxLevel) return fail(c, TJ_E_BAD_CONFIG, "l_max must be in [1, 12]");
+  if (cfg->rebuild != TJ_REBUILD_EVERY_TICK && cfg->rebuild != TJ_REBUILD_ADAPTIVE)
+    return fail(c, TJ_E_BAD_CONFIG, "unknown rebuild policy");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(c, TJ_E_NO_DEVICE, "no CUDA device visible");
+  }
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(c, TJ_E_NO_DEVICE, "device ordinal out of range");
+  c = new tj_ctx();
+  c->cfg = *cfg;
+  c->device = cfg->device;
+  cudaSetDevice(c->device);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&c->d_hdr, sizeof(DevHdr)) != cudaSuccess ||
+      cudaMallocHost(&c->h_hdr, sizeof(DevHdr)) != cudaSuccess ||
+      cudaMalloc(&c->d_consts, 8 * sizeof(int64_t)) != cudaSuccess) {
+    std::string msg = std::string("context setup: ") + cudaGetErrorString(cudaGetLastError());
+    tj_destroy(c);
+    return fail(nullptr, TJ_E_CUDA, msg);
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  int64_t consts[8] = {(int64_t)256 * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
+  *out = c;
+  return TJ_OK;
+}
+
+int tj_destroy(tj_ctx* c) {
+  if (!c) return TJ_OK;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
+                 &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
+                 &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->sqleaf, &c->sqq, &c->sqcov,
+                 &c->sqcount, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->bitmap,
+                 &c->stage, &c->outids, &c->outoff, &c->partial, &c->rhist, &c->roffs};
+  for (DBuf* b : all)
+    if (b->p) cudaFree(b->p);
+  if (c->h_off) cudaFreeHost(c->h_off);
+  if (c->h_ids) cudaFreeHost(c->h_ids);
+  if (c->d_hdr) cudaFree(c->d_hdr);
+  if (c->h_hdr) cudaFreeHost(c->h_hdr);
+  if (c->d_consts) cudaFree(c->d_consts);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->st) cudaStreamDestroy(c->st);
+  delete c;
+  return TJ_OK;
+}
+
+int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) {
+  if (!c || !in || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
+  const int64_t n = in->n_obj, m = in->n_q;
+  if (n < 0 || m < 0) return fail(c, TJ_E_INVALID_ARG, "negative size");
+  if (n > INT32_MAX / 2 || m > INT32_MAX / 2) return fail(c, TJ_E_INVALID_ARG, "tick too large for 32-bit rows");
+  if ((n && (!in->obj_id || !in->obj_x || !in->obj_y)) ||
+      (m && (!in->q_issuer || !in->q_xa || !in->q_ya || !in->q_xb || !in->q_yb)))
+    return fail(c, TJ_E_INVALID_ARG, "null input array");
+  TJ_CUDA(cudaSetDevice(c->device));
+  c->have = false;
+  tj_stats S{};
+  S.n_objects = n;
+  S.n_queries = m;
+  int rc;
+
+  // ---- inputs to device ---------------------------------------------------
+  const int64_t* ids = in->obj_id;
+  const double *xs = in->obj_x, *ys = in->obj_y;
+  const double *qxa = in->q_xa, *qya = in->q_ya, *qxb = in->q_xb, *qyb = in->q_yb;
+  if (in->mem == TJ_MEM_HOST) {
+    if ((rc = ensure(c, c->ids, n * 8)) || (rc = ensure(c, c->xs, n * 8)) || (rc = ensure(c, c->ys, n * 8)) ||
+        (rc = ensure(c, c->qxa, m * 8)) || (rc = ensure(c, c->qya, m * 8)) || (rc = ensure(c, c->qxb, m * 8)) ||
+        (rc = ensure(c, c->qyb, m * 8)))
+      return rc;
+    TJ_CUDA(cudaMemcpyAsync(c->ids.p, ids, n * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->xs.p, xs, n * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->ys.p, ys, n * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qxa.p, qxa, m * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qya.p, qya, m * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qxb.p, qxb, m * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qyb.p, qyb, m * 8, cudaMemcpyHostToDevice, c->st));
+    ids = P<int64_t>(c->ids);
+    xs = P<double>(c->xs);
+    ys = P<double>(c->ys);
+    qxa = P<double>(c->qxa);
+    qya = P<double>(c->qya);
+    qxb = P<double>(c->qxb);
+    qyb = P<double>(c->qyb);
+  } else if (in->mem != TJ_MEM_DEVICE) {
+    return fail(c, TJ_E_INVALID_ARG, "unknown memory space");
+  }
+
+  if ((rc = ensure(c, c->outoff, (m + 1) * 8))) return rc;
+  int64_t R = 0;
+  if (n == 0) {  // engine.py:188-190: every issued query gets []
+    TJ_CUDA(cudaMemsetAsync(c->outoff.p, 0, (m + 1) * 8, c->st));
+    TJ_CUDA(cudaStreamSynchronize(c->st));
+  } else {
+    c->n = n;
+    c->m = m;
+    if ((rc = prepare_static(c, n, m))) return rc;
+    if (c->last_L == 0) c->last_L = c->cap_L;
+    c->obj_passes = passes_for(std::max<int64_t>(c->last_L + c->last_L / 2, 1) - 1);
+    c->sq_passes = passes_for(2 * (c->last_L + c->last_L / 2) - 1);
+    bool done = false;
+    for (int attempt = 0; attempt < 8 && !done; ++attempt) {
+      if ((rc = prepare_dynamic(c))) return rc;
+      fill_dev(c, ids, xs, ys, qxa, qya, qxb, qyb);
+      init_hdr(c, n, m);
+      TJ_CUDA(cudaMemcpyAsync(c->d_hdr, c->h_hdr, sizeof(DevHdr), cudaMemcpyHostToDevice, c->st));
+      S.kernel_launches += launch_tick(c);
+      if ((rc = check_launch(c))) return rc;
+      TJ_CUDA(cudaMemcpyAsync(c->h_hdr, c->d_hdr, sizeof(DevHdr), cudaMemcpyDeviceToHost, c->st));
+      TJ_CUDA(cudaStreamSynchronize(c->st));
+      const DevHdr& H = *c->h_hdr;
+      if (!H.abort) {
+        done = true;
+        break;
+      }
+      S.retries++;
+      if (H.abort & (8 | 16)) return fail(c, TJ_E_CUDA, "internal capacity bound violated (heavy/leaves)");
+      if (H.abort & 32) {
+        c->obj_passes = passes_for(H.L - 1);
+        c->sq_passes = passes_for(2 * H.L - 1);
+      }
+      if (H.abort & 1) c->cap_S = std::max<int64_t>(2 * c->cap_S, H.S + H.S / 4 + 256);
+      if (H.abort & 2) c->cap_W = std::max<int64_t>(2 * c->cap_W, H.W + H.W / 4 + 4096);
+      if (H.abort & 4) c->cap_R = std::max<int64_t>(2 * c->cap_R, H.R + H.R / 4 + 4096);
+    }
+    if (!done) return fail(c, TJ_E_CUDA, "tick did not converge after capacity growth");
+    const DevHdr& H = *c->h_hdr;
+    c->last = H;
+    c->last_L = H.L;
+    if (H.dup) return fail(c, TJ_E_DUPLICATE_RESULT, "a (query, object) pair was produced twice");
+    R = H.R;
+    c->have = true;
+    float ms[5] = {0, 0, 0, 0, 0}, tot = 0;
+    cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]);
+    cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[3]);
+    cudaEventElapsedTime(&ms[2], c->ev[3], c->ev[4]);
+    cudaEventElapsedTime(&ms[3], c->ev[4], c->ev[5]);
+    cudaEventElapsedTime(&ms[4], c->ev[2], c->ev[3]);
+    cudaEventElapsedTime(&tot, c->ev[0], c->ev[5]);
+    S.t_index_ms = ms[0];
+    S.t_filter_ms = ms[1];
+    S.t_decode_ms = ms[2];
+    S.t_merge_ms = ms[3];
+    S.t_join_ms = ms[4];
+    S.t_total_ms = tot;
+    S.task_objects = (int64_t)H.task_obj;
+    S.task_subqueries = (int64_t)H.task_isq;
+    S.containment_tests = (int64_t)H.tests;
+    S.decoded_bits = H.W * 32;
+    S.subq_intersecting = (int64_t)H.sum_isq;
+    S.subq_covering = (int64_t)H.sum_cov;
+    S.covering_results = (int64_t)H.cov_results;
+    S.active_cells = (int64_t)H.active_cells;
+    S.results_total = H.R;
+    S.occ_sum = (int64_t)H.occ_sum;
+    S.occ_sumsq = (int64_t)H.occ_sumsq;
+    S.n_leaves = H.L;
+    S.l_deep = H.l_deep;
+    S.n_tasks = H.n_tasks;
+    S.bitmap_words = H.W;
+    S.n_subqueries = H.S;
+    S.work_units = H.U;
+    S.rebuilt = 1;
+    S.mbr[0] = H.xa;
+    S.mbr[1] = H.ya;
+    S.mbr[2] = H.xb;
+    S.mbr[3] = H.yb;
+  }
+
+  // ---- deliver results ----------------------------------------------------
+  out->n_q = m;
+  out->n_results = R;
+  if (in->out_mem == TJ_MEM_DEVICE) {
+    out->offsets = P<int64_t>(c->outoff);
+    out->ids = n ? P<int64_t>(c->outids) : nullptr;
+    out->mem = TJ_MEM_DEVICE;
+  } else {
+    if ((rc = ensure_host(c, c->h_off, c->h_off_bytes, (m + 1) * 8))) return rc;
+    if ((rc = ensure_host(c, c->h_ids, c->h_ids_bytes, R * 8))) return rc;
+    TJ_CUDA(cudaMemcpyAsync(c->h_off, c->outoff.p, (m + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+    if (R) TJ_CUDA(cudaMemcpyAsync(c->h_ids, c->outids.p, R * 8, cudaMemcpyDeviceToHost, c->st));
+    TJ_CUDA(cudaStreamSynchronize(c->st));
+    out->offsets = (const int64_t*)c->h_off;
+    out->ids = (const int64_t*)c->h_ids;
+    out->mem = TJ_MEM_HOST;
+  }
+  if (stats) *stats = S;
+  return TJ_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Introspection (host copies in the reference's order)
+// ---------------------------------------------------------------------------
+namespace {
+
+template <typename T>
+int d2h(tj_ctx* c, std::vector<T>& v, const void* src, int64_t count) {
+  v.resize((size_t)std::max<int64_t>(count, 0));
+  if (count > 0) TJ_CUDA(cudaMemcpy(v.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost));
+  return TJ_OK;
+}
+
+struct LeafView {
+  std::vector<uint32_t> code;
+  std::vector<int32_t> nobj, obase, nisq, ncov, sbase;
+  std::vector<int64_t> woff;
+  std::vector<int64_t> packed;  // reference packing per leaf rank
+  std::vector<int64_t> order;   // leaf ranks in ascending packed order
+};
+
+int load_leaves(tj_ctx* c, LeafView& lv) {
+  const int64_t L = c->last.L;
+  int rc;
+  if ((rc = d2h(c, lv.code, c->lcode.p, L)) || (rc = d2h(c, lv.nobj, c->lnobj.p, L)) ||
+      (rc = d2h(c, lv.obase, c->lobase.p, L)) || (rc = d2h(c, lv.nisq, c->lnisq.p, L)) ||
+      (rc = d2h(c, lv.ncov, c->lncov.p, L)) || (rc = d2h(c, lv.sbase, c->lsbase.p, L)) ||
+      (rc = d2h(c, lv.woff, c->lwoff.p, L)))
+    return rc;
+  lv.packed.resize(L);
+  const int sh = 2 * c->cfg.l_max;
+  for (int64_t r = 0; r < L; ++r) {
+    const int64_t lev = lv.code[r] >> kLevelShift;
+    const int64_t z = lv.code[r] & kPayloadMask;
+    lv.packed[r] = (lev << sh) | z;
+  }
+  lv.order.resize(L);
+  for (int64_t r = 0; r < L; ++r) lv.order[r] = r;
+  std::sort(lv.order.begin(), lv.order.end(), [&](int64_t a, int64_t b) { return lv.packed[a] < lv.packed[b]; });
+  return TJ_OK;
+}
+
+int need_tick(tj_ctx* c) {
+  if (!c) return TJ_E_INVALID_ARG;
+  if (!c->have) return fail(c, TJ_E_INVALID_ARG, "no completed tick with objects to introspect");
+  cudaSetDevice(c->device);
+  return TJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tj_get_index(tj_ctx* c, tj_index_info* info, int64_t* leaves, int64_t leaves_cap, int64_t* zmap,
+                 int64_t zmap_cap) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  const DevHdr& H = c->last;
+  if (info) {
+    info->mbr[0] = H.xa;
+    info->mbr[1] = H.ya;
+    info->mbr[2] = H.xb;
+    info->mbr[3] = H.yb;
+    info->th_quad = c->cfg.th_quad;
+    info->l_max = c->cfg.l_max;
+    info->l_deep = H.l_deep;
+    info->n_leaves = H.L;
+    info->n_cells = H.Z;
+  }
+  if (!leaves && !zmap) return TJ_OK;
+  LeafView lv;
+  if ((rc = load_leaves(c, lv))) return rc;
+  if (leaves) {
+    if (leaves_cap < H.L) return fail(c, TJ_E_INVALID_ARG, "leaves buffer too small");
+    for (int64_t k = 0; k < H.L; ++k) leaves[k] = lv.packed[lv.order[k]];
+  }
+  if (zmap) {
+    if (zmap_cap < H.Z) return fail(c, TJ_E_INVALID_ARG, "zmap buffer too small");
+    std::vector<uint32_t> z;
+    if ((rc = d2h(c, z, c->zmap.p, H.Z))) return rc;
+    for (int64_t k = 0; k < H.Z; ++k) zmap[k] = lv.packed[z[k] & kPayloadMask];
+  }
+  return TJ_OK;
+}
+
+int tj_get_object_cells(tj_ctx* c, int64_t* cells, int64_t cap) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  if (!cells || cap < c->n) return fail(c, TJ_E_INVALID_ARG, "cells buffer too small");
+  LeafView lv;
+  if ((rc = load_leaves(c, lv))) return rc;
+  std::vector<uint32_t> code, z;
+  if ((rc = d2h(c, code, c->code.p, c->n)) || (rc = d2h(c, z, c->zmap.p, c->last.Z))) return rc;
+  const int sh = 2 * (c->cfg.l_max - c->last.l_deep);
+  for (int64_t i = 0; i < c->n; ++i) cells[i] = lv.packed[z[code[i] >> sh] & kPayloadMask];
+  return TJ_OK;
+}
+
+int tj_get_subqueries(tj_ctx* c, int64_t* count, int64_t* q_row, int64_t* cell, uint8_t* covering,
+                      int64_t cap) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  const int64_t S = c->last.S;
+  if (count) *count = S;
+  if (!q_row && !cell && !covering) return TJ_OK;
+  if (cap < S) return fail(c, TJ_E_INVALID_ARG, "subquery buffers too small");
+  LeafView lv;
+  if ((rc = load_leaves(c, lv))) return rc;
+  std::vector<int32_t> leaf, q;
+  std::vector<uint8_t> cv;
+  if ((rc = d2h(c, leaf, c->sqleaf.p, S)) || (rc = d2h(c, q, c->sqq.p, S)) || (rc = d2h(c, cv, c->sqcov.p, S)))
+    return rc;
+  for (int64_t s = 0; s < S; ++s) {
+    if (q_row) q_row[s] = q[s];
+    if (cell) cell[s] = lv.packed[leaf[s]];
+    if (covering) covering[s] = cv[s];
+  }
+  return TJ_OK;
+}
+
+int tj_get_directory(tj_ctx* c, int64_t* obj_rows, int64_t obj_cap, int64_t* isq, int64_t* n_isq, int64_t* cov,
+                     int64_t* n_cov, int64_t sq_cap) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  const DevHdr& H = c->last;
+  if (n_isq) *n_isq = (int64_t)H.sum_isq;
+  if (n_cov) *n_cov = (int64_t)H.sum_cov;
+  if (!obj_rows && !isq && !cov) return TJ_OK;
+  LeafView lv;
+  if ((rc = load_leaves(c, lv))) return rc;
+  if (obj_rows) {
+    if (obj_cap < c->n) return fail(c, TJ_E_INVALID_ARG, "obj_rows buffer too small");
+    std::vector<int32_t> sidx;
+    if ((rc = d2h(c, sidx, c->dv.sidx, c->n))) return rc;
+    int64_t k = 0;
+    for (int64_t r : lv.order)
+      for (int32_t j = 0; j < lv.nobj[r]; ++j) obj_rows[k++] = sidx[lv.obase[r] + j];
+  }
+  if (isq || cov) {
+    if (sq_cap < (int64_t)std::max(H.sum_isq, H.sum_cov)) return fail(c, TJ_E_INVALID_ARG, "sq buffers too small");
+    std::vector<int32_t> ss;
+    if ((rc = d2h(c, ss, c->dv.ssorted, H.S))) return rc;
+    int64_t ki = 0, kc = 0;
+    for (int64_t r : lv.order) {
+      for (int32_t j = 0; j < lv.nisq[r]; ++j)
+        if (isq) isq[ki++] = ss[lv.sbase[r] + j];
+      for (int32_t j = 0; j < lv.ncov[r]; ++j)
+        if (cov) cov[kc++] = ss[lv.sbase[r] + lv.nisq[r] + j];
+    }
+  }
+  return TJ_OK;
+}
+
+int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_cell, int64_t* task_nobj,
+                   int64_t* task_nisq, int64_t* task_woff, uint32_t* words, int64_t* counts, int64_t task_cap,
+                   int64_t word_cap, int64_t count_cap) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  const DevHdr& H = c->last;
+  if (n_tasks) *n_tasks = H.n_tasks;
+  if (n_words) *n_words = H.W;
+  if (!task_cell && !words && !counts) return TJ_OK;
+  if (task_cap < H.n_tasks || word_cap < H.W) return fail(c, TJ_E_INVALID_ARG, "bitmap buffers too small");
+  LeafView lv;
+  if ((rc = load_leaves(c, lv))) return rc;
+  std::vector<uint32_t> bm;
+  std::vector<int32_t> ss, cnt;
+  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, ss, c->dv.ssorted, H.S)) ||
+      (rc = d2h(c, cnt, c->sqcount.p, H.S)))
+    return rc;
+  int64_t t = 0, w = 0, k = 0;
+  if (task_woff) task_woff[0] = 0;
+  for (int64_t r : lv.order) {
+    const int64_t no = lv.nobj[r], ni = lv.nisq[r];
+    if (!(no > 0 && ni > 0)) continue;
+    const int64_t nw = ni * ((no + 31) / 32);
+    if (task_cell) task_cell[t] = lv.packed[r];
+    if (task_nobj) task_nobj[t] = no;
+    if (task_nisq) task_nisq[t] = ni;
+    if (words) std::memcpy(words + w, bm.data() + lv.woff[r], nw * 4);
+    if (counts) {
+      if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
+      for (int64_t j = 0; j < ni; ++j) counts[k + j] = cnt[ss[lv.sbase[r] + j]];
+    }
+    w += nw;
+    k += ni;
+    ++t;
+    if (task_woff) task_woff[t] = w;
+  }
+  return TJ_OK;
+}
+
+int tj_get_imbalance(tj_ctx* c, int32_t sim_processors, int32_t heaviest_first, double* imbalance) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  if (sim_processors < 1 || !imbalance) return fail(c, TJ_E_INVALID_ARG, "bad arguments");
+  LeafView lv;
+  if ((rc = load_leaves(c, lv))) return rc;
+  std::vector<std::pair<int64_t, int64_t>> tasks;  // (weight, packed cell), directory order
+  for (int64_t r : lv.order)
+    if (lv.nobj[r] > 0 && lv.nisq[r] > 0) tasks.emplace_back((int64_t)lv.nobj[r] * lv.nisq[r], lv.packed[r]);
+  if (heaviest_first)  // scheduler.py:31-38: (-weight, cell_id)
+    std::stable_sort(tasks.begin(), tasks.end(), [](const auto& a, const auto& b) {
+      return a.first != b.first ? a.first > b.first : a.second < b.second;
+    });
+  std::vector<int64_t> tot(sim_processors, 0);  // scheduler.py:41-54
+  for (const auto& t : tasks) {
+    int best = 0;
+    for (int p = 1; p < sim_processors; ++p)
+      if (tot[p] < tot[best]) best = p;
+    tot[best] += t.first;
+  }
+  const int64_t top = *std::max_element(tot.begin(), tot.end());
+  const int64_t low = *std::min_element(tot.begin(), tot.end());
+  *imbalance = top == 0 ? 0.0 : (double)(top - low) / (double)top;
+  return TJ_OK;
+}
+
+int tj_get_stream(tj_ctx* c, void** stream) {
+  if (!c || !stream) return TJ_E_INVALID_ARG;
+  *stream = (void*)c->st;
+  return TJ_OK;
+}
+
+int tj_host_alloc(int64_t bytes, void** ptr) {
+  if (!ptr || bytes < 0) return TJ_E_INVALID_ARG;
+  cudaError_t e = cudaMallocHost(ptr, (size_t)std::max<int64_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    g_last_error = cudaGetErrorString(e);
+    return TJ_E_OOM;
+  }
+  return TJ_OK;
+}
+
+int tj_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+  return TJ_OK;
+}
+
+}  // extern "C"

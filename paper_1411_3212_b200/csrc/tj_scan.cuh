@@ -1,0 +1,210 @@
+// Device-wide exclusive scan and stable radix sort with device-resident sizes.
+//
+// Every size in the tick after the index build (leaves, subqueries, words,
+// results) is known only on the device.  These primitives read their length
+// from a device pointer so the whole tick is a fixed launch sequence (CUDA
+// graph capturable) with no host round trip between stages.
+#pragma once
+
+#include "tj_common.cuh"
+
+namespace tj {
+
+constexpr int kScanThreads = 256;
+
+// ---------------------------------------------------------------------------
+// Exclusive scan: three launches (chunk reduce, partial scan, chunk scan).
+// `In`  : int64_t operator()(int64_t i) const        — value of item i
+// `Out` : void operator()(int64_t i, int64_t excl, int64_t v) const
+// ---------------------------------------------------------------------------
+template <typename In>
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_reduce(In in, const int64_t* n_ptr, const DevHdr* h, int64_t* partial) {
+  if (h->abort) return;
+  __shared__ int64_t sh[33];
+  const int64_t n = *n_ptr, G = gridDim.x;
+  const int64_t chunk = (n + G - 1) / G;
+  const int64_t b = blockIdx.x * chunk;
+  const int64_t e = (b + chunk < n) ? b + chunk : n;
+  int64_t s = 0;
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) s += in(i);
+  s = warp_sum(s);
+  if (lane_id() == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+
+// single block of 1024 threads; G <= 1024
+__global__ void __launch_bounds__(1024)
+k_scan_partials(int64_t* partial, int G, int64_t* total_out, DevHdr* h) {
+  if (h->abort) return;
+  __shared__ int64_t sh[33];
+  int64_t v = threadIdx.x < G ? partial[threadIdx.x] : 0;
+  int64_t tot;
+  int64_t ex = block_excl_scan(v, sh, &tot);
+  if (threadIdx.x < G) partial[threadIdx.x] = ex;
+  if (threadIdx.x == 0 && total_out) *total_out = tot;
+}
+
+template <typename In, typename Out>
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_down(In in, Out out, const int64_t* n_ptr, const DevHdr* h, const int64_t* partial) {
+  if (h->abort) return;
+  __shared__ int64_t sh[33];
+  const int64_t n = *n_ptr, G = gridDim.x;
+  const int64_t chunk = (n + G - 1) / G;
+  const int64_t b = blockIdx.x * chunk;
+  const int64_t e = (b + chunk < n) ? b + chunk : n;
+  int64_t carry = partial[blockIdx.x];
+  for (int64_t base = b; base < e; base += blockDim.x) {  // uniform trip count per block
+    const int64_t i = base + threadIdx.x;
+    const int64_t v = (i < e) ? in(i) : 0;
+    int64_t tot;
+    const int64_t ex = block_excl_scan(v, sh, &tot);
+    if (i < e) out(i, carry + ex, v);
+    carry += tot;
+  }
+}
+
+struct ScanPlan {
+  int G;
+  int64_t* partial;  // G entries
+};
+
+template <typename In, typename Out>
+inline void scan_launch(const ScanPlan& p, In in, Out out, const int64_t* n_ptr, DevHdr* h,
+                        int64_t* total_out, cudaStream_t st) {
+  k_scan_reduce<In><<<p.G, kScanThreads, 0, st>>>(in, n_ptr, h, p.partial);
+  k_scan_partials<<<1, 1024, 0, st>>>(p.partial, p.G, total_out, h);
+  k_scan_down<In, Out><<<p.G, kScanThreads, 0, st>>>(in, out, n_ptr, h, p.partial);
+}
+
+// Generic functors ----------------------------------------------------------
+template <typename T>
+struct ArrIn {
+  const T* a;
+  __device__ int64_t operator()(int64_t i) const { return (int64_t)a[i]; }
+};
+template <typename T>
+struct ExclOut {
+  T* a;
+  __device__ void operator()(int64_t i, int64_t ex, int64_t) const { a[i] = (T)ex; }
+};
+
+// ---------------------------------------------------------------------------
+// Stable LSD radix sort of (u32 key, i32 value) pairs, 8-bit digits.
+// Upsweep: per-chunk digit histograms; scan over (digit, chunk); downsweep:
+// each CTA walks its chunk in input order, ranks items per digit with warp
+// match (stable: warp w / round k / lane order), stages the tile by digit in
+// shared memory and writes digit runs coalesced.
+// ---------------------------------------------------------------------------
+constexpr int kRadixThreads = 256;
+constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixIPT = 8;                        // items per thread per tile
+constexpr int kRadixTile = kRadixThreads * kRadixIPT;  // 2048
+
+__global__ void __launch_bounds__(kRadixThreads)
+k_radix_upsweep(const uint32_t* keys, const int64_t* n_ptr, const DevHdr* h, int shift,
+                uint32_t* hist /* [256][G] */) {
+  if (h->abort) return;
+  __shared__ uint32_t cnt[256];
+  const int64_t n = *n_ptr, G = gridDim.x;
+  const int64_t chunk = ((n + G - 1) / G + kRadixTile - 1) / kRadixTile * kRadixTile;
+  const int64_t b = blockIdx.x * chunk;
+  const int64_t e = (b + chunk < n) ? b + chunk : n;
+  cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t bb = b; bb < e; bb += blockDim.x) {  // uniform trip count: full warps
+    const int64_t i = bb + threadIdx.x;
+    const bool ok = i < e;
+    const uint32_t d = ok ? ((keys[i] >> shift) & 255u) : 256u;
+    const uint32_t peers = __match_any_sync(0xffffffffu, d);
+    if (ok && (int)(__ffs(peers) - 1) == lane_id()) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+  }
+  __syncthreads();
+  hist[(int64_t)threadIdx.x * G + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kRadixThreads)
+k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out,
+                  int32_t* vals_out, const int64_t* n_ptr, const DevHdr* h, int shift,
+                  const int64_t* offs /* [256][G] exclusive */) {
+  if (h->abort) return;
+  __shared__ uint32_t wcnt[kRadixWarps][256];
+  __shared__ uint32_t base[256];      // running global offset per digit for this chunk
+  __shared__ uint32_t tprefix[256];   // tile-local exclusive prefix per digit
+  __shared__ uint32_t skey[kRadixTile];
+  __shared__ int32_t sval[kRadixTile];
+  __shared__ int64_t shs[33];
+  const int64_t n = *n_ptr, G = gridDim.x;
+  const int64_t chunk = ((n + G - 1) / G + kRadixTile - 1) / kRadixTile * kRadixTile;
+  const int64_t b = blockIdx.x * chunk;
+  const int64_t e = (b + chunk < n) ? b + chunk : n;
+  const int t = threadIdx.x, w = t >> 5, lane = t & 31;
+  base[t] = (uint32_t)offs[(int64_t)t * G + blockIdx.x];
+  const uint32_t lt = (1u << lane) - 1u;
+  for (int64_t tb = b; tb < e; tb += kRadixTile) {
+    for (int k = t; k < kRadixWarps * 256; k += kRadixThreads) (&wcnt[0][0])[k] = 0;
+    __syncthreads();
+    uint32_t key[kRadixIPT], dig[kRadixIPT], rk[kRadixIPT];
+    int32_t val[kRadixIPT];
+    // warp w owns items [tb + w*32*IPT, ...), processed in rounds of 32 in order
+#pragma unroll
+    for (int r = 0; r < kRadixIPT; ++r) {
+      const int64_t i = tb + (int64_t)w * 32 * kRadixIPT + r * 32 + lane;
+      const bool ok = i < e;
+      key[r] = ok ? keys_in[i] : 0u;
+      val[r] = ok ? vals_in[i] : 0;
+      dig[r] = ok ? ((key[r] >> shift) & 255u) : 256u;
+      const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
+      const int leader = __ffs(peers) - 1;
+      uint32_t old = 0;
+      if (ok && lane == leader) {
+        old = wcnt[w][dig[r]];
+        wcnt[w][dig[r]] = old + __popc(peers);
+      }
+      old = __shfl_sync(0xffffffffu, old, leader);
+      rk[r] = old + __popc(peers & lt);
+      __syncwarp();
+    }
+    __syncthreads();
+    // per digit: prefix across warps, tile total
+    uint32_t run = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRadixWarps; ++ww) {
+      const uint32_t c = wcnt[ww][t];
+      wcnt[ww][t] = run;
+      run += c;
+    }
+    int64_t tot;
+    const int64_t ex = block_excl_scan((int64_t)run, shs, &tot);
+    tprefix[t] = (uint32_t)ex;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < kRadixIPT; ++r) {
+      if (dig[r] < 256u) {
+        const uint32_t pos = tprefix[dig[r]] + wcnt[w][dig[r]] + rk[r];
+        skey[pos] = key[r];
+        sval[pos] = val[r];
+      }
+    }
+    __syncthreads();
+    const int tile_n = (int)((e - tb) < kRadixTile ? (e - tb) : kRadixTile);
+    for (int p = t; p < tile_n; p += kRadixThreads) {
+      const uint32_t k = skey[p];
+      const uint32_t d = (k >> shift) & 255u;
+      const int64_t dst = (int64_t)base[d] + (p - tprefix[d]);
+      keys_out[dst] = k;
+      vals_out[dst] = sval[p];
+    }
+    __syncthreads();
+    base[t] += run;
+    __syncthreads();
+  }
+}
+
+}  // namespace tj

@@ -1,0 +1,326 @@
+"""GPU parity: the native tick (through the C ABI) against the reference.
+
+Every test here runs the CUDA path on a B200 and compares with
+(a) reference-generated fixtures (tests/golden/, made by running the
+reference itself), (b) the pinned CPU oracle (oracle/quad_oracle.py) on the
+same seeded inputs, and (c) size-independent properties at full scale.
+Bit-exact throughout: integers / ids compare with array_equal.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+from conftest import load_small_cases, workload_from_json
+from oracle import quad_oracle as qo
+
+pytestmark = pytest.mark.gpu
+
+CASES = load_small_cases()
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import paper_1411_3212_b200 as p
+    from paper_1411_3212_b200 import _native
+
+    assert _native.device_count() > 0, "no CUDA device: the GPU tests need a B200"
+    return p
+
+
+def _engine(pkg, th=384, l_max=12, covering=True, **kw):
+    return pkg.Engine(pkg.MethodConfig(method="quad", th_quad=th, l_max=l_max, covering_optimization=covering,
+                                       **kw))
+
+
+def _check_vs_oracle(res, ref):
+    assert np.array_equal(res.offsets, ref.offsets)
+    assert np.array_equal(res.ids, ref.result_ids)
+
+
+# ---------------------------------------------------------------- fixtures --
+
+@pytest.mark.parametrize("case", CASES, ids=[c.name for c in CASES])
+def test_small_case_all_intermediates(pkg, case):
+    eng = _engine(pkg, case.th_quad, case.l_max, case.covering)
+    ids, xs, ys, qids, qxa, qya, qxb, qyb = case.inputs()
+    res, st = eng.process_columns(ids, xs, ys, qids, qxa, qya, qxb, qyb)
+    # final per-query results (ResultSet.by_query as CSR)
+    assert np.array_equal(res.offsets, case.res_off)
+    assert np.array_equal(res.ids, case.res_ids)
+    ctx = eng.native
+    # index: quadtree.py:74-158
+    ix = ctx.index()
+    assert tuple(ix["mbr"]) == tuple(case.mbr.tolist())
+    assert ix["l_deep"] == int(case.l_deep)
+    assert np.array_equal(ix["leaves"], case.leaves)
+    assert np.array_equal(ix["zmap"], case.zmap)
+    assert np.array_equal(ctx.object_cells(len(ids)), case.obj_cell)
+    # subqueries: quadtree.py:168-240 (query rows, packed leaf, covering)
+    q, cell, cov = ctx.subqueries()
+    assert np.array_equal(q, case.sq_qrow)
+    assert np.array_equal(cell, case.sq_cell)
+    assert np.array_equal(cov.astype(np.uint8), case.sq_cov)
+    # directory: directory.py:119-158
+    rows, isq, covl = ctx.directory(len(ids))
+    assert np.array_equal(rows, case.dir_obj_order)
+    assert np.array_equal(qids[q[isq]], case.dir_isq_qid)
+    assert np.array_equal(cell[isq], case.dir_isq_cell)
+    assert np.array_equal(qids[q[covl]], case.dir_cov_qid)
+    assert np.array_equal(cell[covl], case.dir_cov_cell)
+    # bitmaps + popcounts: bitmap.py:70-119
+    bm = ctx.bitmaps()
+    assert np.array_equal(bm["cell"], case.task_cell)
+    assert np.array_equal(bm["nobj"], case.task_nobj)
+    assert np.array_equal(bm["nisq"], case.task_nisq)
+    assert np.array_equal(bm["woff"], case.task_woff)
+    assert np.array_equal(bm["words"], case.task_words)
+    assert np.array_equal(bm["counts"], case.task_counts)
+    # TickStats counters (engine.py:212-258)
+    want = case.meta["stats"]
+    for k in ("containment_tests", "decoded_bits", "subq_intersecting", "subq_covering", "covering_results",
+              "active_cells", "results_total"):
+        assert getattr(st, k) == want[k], k
+    assert st.occupancy_mean == pytest.approx(want["occupancy_mean"], rel=1e-12)
+    assert st.occupancy_var == pytest.approx(want["occupancy_var"], rel=1e-9, abs=1e-12)
+    assert st.imbalance == pytest.approx(want["imbalance"], rel=1e-12, abs=1e-15)
+    eng.close()
+
+
+def _digest_run(pkg, run, max_ticks=None):
+    cfg = workload_from_json(run["workload"])
+    meth = run["method"]
+    eng = _engine(pkg, meth["th_quad"], meth["l_max"], meth["covering"])
+    for t, tick in enumerate(pkg.iter_ticks(cfg)):
+        if max_ticks is not None and t >= max_ticks:
+            break
+        res, st = eng.process_tick_columnar(tick)
+        want = run["ticks"][t]
+        assert st.results_total == want["stats"]["results_total"]
+        assert st.containment_tests == want["stats"]["containment_tests"]
+        assert st.subq_intersecting == want["stats"]["subq_intersecting"]
+        assert st.subq_covering == want["stats"]["subq_covering"]
+        assert qo.result_digest(tick.qids, res.offsets, res.ids) == want["digest"]
+    eng.close()
+
+
+def test_config_a_all_ticks_match_reference(pkg, digests):
+    """Config A (uniform 100K, 10%, 10 ticks): sha256 of the reference's canonical lines."""
+    _digest_run(pkg, digests["A"])
+
+
+def test_skewed_100k_matches_reference(pkg, digests):
+    _digest_run(pkg, digests["B100K"])
+
+
+@pytest.mark.parametrize("k", range(20))
+def test_acceptance_c1_family(pkg, digests, k):
+    """test_acceptance.py:28-100 workloads, quad, every tick."""
+    _digest_run(pkg, digests[f"C1_{k}"])
+
+
+# ------------------------------------------------------------- edge cases --
+
+def test_zero_objects(pkg):
+    eng = _engine(pkg)
+    res, st = eng.process_columns(np.zeros(0, np.int64), np.zeros(0), np.zeros(0), np.array([1]),
+                                  np.array([0.0]), np.array([0.0]), np.array([1.0]), np.array([1.0]))
+    assert res.offsets.tolist() == [0, 0] and len(res.ids) == 0
+    assert res.to_result_set().by_query == {1: []} and st.results_total == 0
+
+
+def test_zero_queries_and_outside_mbr(pkg):
+    eng = _engine(pkg)
+    res, st = eng.process_columns(np.array([0]), np.array([1.0]), np.array([1.0]), np.zeros(0, np.int64),
+                                  np.zeros(0), np.zeros(0), np.zeros(0), np.zeros(0))
+    assert res.offsets.tolist() == [0] and st.containment_tests == 0
+    # test_engine.py:92-96 query outside the MBR still reported as []
+    res, _ = eng.process_columns(np.array([0, 1]), np.array([10.0, 20.0]), np.array([10.0, 20.0]),
+                                 np.array([0]), np.array([100.0]), np.array([100.0]), np.array([150.0]),
+                                 np.array([150.0]))
+    assert res.to_result_set().by_query == {0: []}
+
+
+def test_object_api_scenario(pkg):
+    P, R = pkg.Point, pkg.Rect
+    batch = pkg.TickBatch(0, [pkg.MovingObject(1, P(20.0, 20.0)), pkg.MovingObject(2, P(4.0, 4.0)),
+                              pkg.MovingObject(3, P(5.0, 5.0))],
+                          [pkg.Query(1, R(18, 18, 19, 19)), pkg.Query(2, R(0, 0, 1, 1)), pkg.Query(3, R(3, 3, 7, 7))])
+    rs, st = pkg.process_tick(batch, pkg.MethodConfig(method="quad", th_quad=1, l_max=3))
+    assert rs.by_query == {1: [], 2: [], 3: [2, 3]}
+    assert rs.lines() == ["1:", "2:", "3: 2,3"]
+
+
+def _rand_tick(rng, n, m, lo=0.0, hi=1000.0, side=(5.0, 80.0)):
+    xs = rng.uniform(lo, hi, n)
+    ys = rng.uniform(lo, hi, n)
+    cx = rng.uniform(lo, hi, m)
+    cy = rng.uniform(lo, hi, m)
+    h = rng.uniform(side[0], side[1], m) / 2
+    return xs, ys, cx - h, cy - h, cx + h, cy + h
+
+
+def test_non_monotone_ids_sorted_by_id(pkg):
+    rng = np.random.default_rng(3)
+    n, m = 5000, 800
+    xs, ys, a, b, c, d = _rand_tick(rng, n, m)
+    ids = rng.permutation(10 * n)[:n].astype(np.int64)  # arbitrary, non-monotone ids
+    qids = rng.permutation(m).astype(np.int64)
+    eng = _engine(pkg, th=16)
+    res, _ = eng.process_columns(ids, xs, ys, qids, a, b, c, d)
+    ref = qo.run_tick(ids, xs, ys, qids, a, b, c, d, th_quad=16)
+    _check_vs_oracle(res, ref)
+
+
+def test_duplicate_issuers_merge_like_reference(pkg):
+    xs = np.array([1.0, 2.0, 3.0, 8.0])
+    ys = np.array([1.0, 2.0, 3.0, 8.0])
+    ids = np.arange(4)
+    eng = _engine(pkg, th=1, l_max=4)
+    # two disjoint queries of issuer 7 are concatenated + sorted (decode.py:102-117)
+    res, _ = eng.process_columns(ids, xs, ys, np.array([7, 7]), np.array([7.0, 0.5]), np.array([7.0, 0.5]),
+                                 np.array([9.0, 1.5]), np.array([9.0, 1.5]))
+    assert res.to_result_set().by_query == {7: [0, 3]}
+    res, _ = eng.process_columns(ids, xs, ys, np.array([7, 7]), np.array([0.0, 0.5]), np.array([0.0, 0.5]),
+                                 np.array([2.5, 1.5]), np.array([2.5, 1.5]))
+    from paper_1411_3212_b200.errors import DuplicateResult
+
+    with pytest.raises(DuplicateResult):
+        res.to_result_set()
+
+
+def test_deep_tree_colocated_and_big_leaves(pkg):
+    """l_max leaves above th (quadtree.py:116): multi-tile join and heavy sub-pyramids."""
+    rng = np.random.default_rng(11)
+    n = 30_000
+    xs = np.concatenate([rng.uniform(0, 1000, n - 6000), np.full(3000, 500.0), 500.0 + rng.uniform(0, 1e-6, 3000)])
+    ys = np.concatenate([rng.uniform(0, 1000, n - 6000), np.full(3000, 250.0), 250.0 + rng.uniform(0, 1e-6, 3000)])
+    m = 3000
+    cx = np.concatenate([rng.uniform(0, 1000, m - 200), np.full(200, 500.0)])
+    cy = np.concatenate([rng.uniform(0, 1000, m - 200), np.full(200, 250.0)])
+    h = np.concatenate([rng.uniform(1, 30, m - 200), rng.uniform(1e-7, 2.0, 200)]) / 2
+    ids = np.arange(n, dtype=np.int64)
+    qids = np.arange(m, dtype=np.int64)
+    for th in (1, 8, 384):
+        eng = _engine(pkg, th=th)
+        res, st = eng.process_columns(ids, xs, ys, qids, cx - h, cy - h, cx + h, cy + h)
+        ref = qo.run_tick(ids, xs, ys, qids, cx - h, cy - h, cx + h, cy + h, th_quad=th)
+        _check_vs_oracle(res, ref)
+        assert st.l_deep == ref.index.l_deep and st.n_leaves == len(ref.index.leaves)
+        ix = eng.native.index()
+        assert np.array_equal(ix["leaves"], ref.index.leaves)
+        eng.close()
+
+
+def test_huge_queries_many_subqueries(pkg):
+    """Large windows: hundreds of leaves per query, covering-heavy, multi-run merges."""
+    rng = np.random.default_rng(5)
+    xs, ys, a, b, c, d = _rand_tick(rng, 40_000, 300, side=(100.0, 900.0))
+    ids = np.arange(len(xs), dtype=np.int64)
+    qids = np.arange(len(a), dtype=np.int64)
+    for cov in (True, False):
+        eng = _engine(pkg, th=16, covering=cov)
+        res, st = eng.process_columns(ids, xs, ys, qids, a, b, c, d)
+        ref = qo.run_tick(ids, xs, ys, qids, a, b, c, d, th_quad=16, covering_optimization=cov)
+        _check_vs_oracle(res, ref)
+        assert st.subq_covering == ref.counters["subq_covering"]
+        assert st.containment_tests == ref.counters["containment_tests"]
+        eng.close()
+
+
+def test_covering_toggle_preserves_results(pkg):
+    """test_engine.py:100-111 / acceptance C4 semantics."""
+    cfg = pkg.WorkloadConfig(n_objects=4000, n_ticks=1, distribution="gaussian", n_hotspots=4, seed=8,
+                             query_side=(50.0, 300.0))
+    tick = next(pkg.iter_ticks(cfg))
+    on = _engine(pkg, th=16, covering=True)
+    off = _engine(pkg, th=16, covering=False)
+    r_on, s_on = on.process_tick_columnar(tick)
+    r_off, s_off = off.process_tick_columnar(tick)
+    assert np.array_equal(r_on.ids, r_off.ids) and np.array_equal(r_on.offsets, r_off.offsets)
+    assert s_on.subq_covering > 0 and s_off.subq_covering == 0
+    assert s_on.containment_tests < s_off.containment_tests
+
+
+def test_negative_and_degenerate_coordinates(pkg):
+    rng = np.random.default_rng(17)
+    for trial in range(10):
+        n = int(rng.integers(1, 400))
+        xs = rng.uniform(-100, 100, n)
+        ys = np.full(n, 3.25) if trial % 3 == 0 else rng.uniform(-100, 100, n)
+        if trial % 4 == 1:
+            xs = np.full(n, -7.5)
+        m = int(rng.integers(0, 120))
+        cx, cy, hh = rng.uniform(-100, 100, m), rng.uniform(-100, 100, m), rng.uniform(0.5, 60, m)
+        ids = np.arange(n, dtype=np.int64)
+        qids = np.arange(m, dtype=np.int64)
+        th = int(rng.integers(1, 7))
+        eng = _engine(pkg, th=th, l_max=6)
+        res, _ = eng.process_columns(ids, xs, ys, qids, cx - hh, cy - hh, cx + hh, cy + hh)
+        ref = qo.run_tick(ids, xs, ys, qids, cx - hh, cy - hh, cx + hh, cy + hh, th_quad=th, l_max=6)
+        _check_vs_oracle(res, ref)
+        off, res_b = qo.brute_force(ids, xs, ys, cx - hh, cy - hh, cx + hh, cy + hh)
+        assert np.array_equal(res.offsets, off) and np.array_equal(res.ids, res_b)
+        eng.close()
+
+
+def test_every_lmax_level(pkg):
+    rng = np.random.default_rng(23)
+    xs, ys, a, b, c, d = _rand_tick(rng, 6000, 500, side=(1.0, 40.0))
+    xs[:1500] = 123.4 + rng.uniform(0, 0.01, 1500)
+    ys[:1500] = 567.8 + rng.uniform(0, 0.01, 1500)
+    ids = np.arange(len(xs), dtype=np.int64)
+    qids = np.arange(len(a), dtype=np.int64)
+    for l_max in range(1, 13):
+        eng = _engine(pkg, th=20, l_max=l_max)
+        res, st = eng.process_columns(ids, xs, ys, qids, a, b, c, d)
+        ref = qo.run_tick(ids, xs, ys, qids, a, b, c, d, th_quad=20, l_max=l_max)
+        _check_vs_oracle(res, ref)
+        ix = eng.native.index()
+        assert ix["l_deep"] == ref.index.l_deep
+        assert np.array_equal(ix["zmap"], ref.index.zmap)
+        eng.close()
+
+
+def test_engine_reused_across_growing_ticks(pkg):
+    """Capacity growth + replay: one Engine, ticks of increasing size."""
+    rng = np.random.default_rng(29)
+    eng = _engine(pkg, th=32)
+    for n, m, side in ((500, 50, (5.0, 20.0)), (20_000, 20_000, (5.0, 60.0)), (3000, 3000, (200.0, 600.0)),
+                       (60_000, 60_000, (20.0, 120.0))):
+        xs, ys, a, b, c, d = _rand_tick(rng, n, m, side=side)
+        ids = np.arange(n, dtype=np.int64)
+        qids = np.arange(m, dtype=np.int64)
+        res, _ = eng.process_columns(ids, xs, ys, qids, a, b, c, d)
+        ref = qo.run_tick(ids, xs, ys, qids, a, b, c, d, th_quad=32)
+        _check_vs_oracle(res, ref)
+    eng.close()
+
+
+def test_config_c_scale_properties(pkg):
+    """10M skewed objects at 5u (config C): sampled brute-force + invariants."""
+    cfg = pkg.WorkloadConfig(n_objects=10_000_000, n_ticks=1, query_rate=1.0, query_side=5.0,
+                             distribution="gaussian", n_hotspots=25, seed=3)
+    tick = next(pkg.iter_ticks(cfg))
+    eng = _engine(pkg)
+    res, st = eng.process_tick_columnar(tick, full_stats=False)
+    assert len(res.offsets) == tick.n_queries + 1 and res.offsets[-1] == st.results_total
+    # SURVEY.md §8 measured sizes for C @5u, seed 3, tick 0
+    assert st.results_total == 169_197_114
+    assert st.n_leaves == 60_820 and st.l_deep == 11
+    assert st.subq_intersecting == 16_845_566 and st.subq_covering == 0
+    lens = np.diff(res.offsets)
+    # ascending, duplicate-free per query
+    d = np.diff(res.ids)
+    bad = np.ones(len(res.ids), bool)
+    bad[res.offsets[1:-1] - 1] = False
+    assert np.all((d > 0) | ~bad[:-1])
+    rng = np.random.default_rng(99)
+    sample = rng.choice(tick.n_queries, 40, replace=False)
+    hot = np.argsort(lens)[-10:]
+    for k in np.concatenate([sample, hot]):
+        hit = ((tick.xs >= tick.qxa[k]) & (tick.xs <= tick.qxb[k]) & (tick.ys >= tick.qya[k])
+               & (tick.ys <= tick.qyb[k]))
+        assert np.array_equal(res.of(k), np.sort(tick.ids[hit]))
+    eng.close()
