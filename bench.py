@@ -1,0 +1,362 @@
+#!/usr/bin/env python
+"""bench.py — QUAD repeated-range-query tick throughput on B200.
+
+Metric (BASELINE.json): range queries/sec (and p50 tick latency) at 10M
+skewed objects.  Workload at N=1: config C of SURVEY.md §8(d) — 10,000,000
+Gaussian-hotspot objects (25 hotspots, sigma 225u, region 22500u), 100% query
+rate, square 5u queries, seed 3, every tick a full index rebuild.  Inputs are
+synthetic, produced by the RNG-identical columnar generator; each tick's
+inputs (560 MB) exceed the 126 MB L2, so no flush is needed between steps.
+
+A step = one `tj_tick` (index build -> query scatter -> per-leaf bitmap join
+-> decode -> canonical per-query lists) over one tick.
+
+  python bench.py [--gpus N --steps K --warmup W]           # our arm
+  python bench.py --impl reference [...]                    # CPU reference arm (oracle port)
+
+Under torchrun (N>1) every rank processes its own 10M-object population
+(independent seeds; no data-path collective) and rank 0 prints the whole-job
+number: weak scaling, max-over-ranks device time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "range queries/sec at 10M skewed objects (p50 tick latency alongside)"
+UNIT = "queries/s"
+
+WORKLOADS = {
+    # SURVEY.md §8(d) config C at 5u (the BASELINE metric's config)
+    "C5": dict(n_objects=10_000_000, query_rate=1.0, query_side=5.0, distribution="gaussian", n_hotspots=25,
+               seed=3),
+    # config B (1M gaussian, 50u) and A (uniform 100K, 10%) for side runs
+    "B": dict(n_objects=1_000_000, query_rate=1.0, query_side=50.0, distribution="gaussian", n_hotspots=25,
+              seed=2),
+    "A": dict(n_objects=100_000, query_rate=0.1, query_side=(200.0, 800.0), distribution="uniform", seed=1),
+}
+DESCR = {
+    "C5": "skewed 10M objects (gaussian, 25 hotspots, sigma 225u), 100% query rate, 5u squares, seed 3",
+    "B": "gaussian 1M objects, 100% query rate, 50u squares, seed 2",
+    "A": "uniform 100K objects, 10% query rate, sides U[200,800]u, seed 1",
+}
+
+
+def measured_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as fp:
+            return float(json.load(fp)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(kernel: str):
+    """Per-launch dram bytes of `kernel` from the committed ncu summary (profiles/)."""
+    import glob
+
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json")), reverse=True):
+        try:
+            with open(p) as fp:
+                d = json.load(fp)
+            k = d.get("kernels", {}).get(kernel)
+            if k and k.get("dram_bytes_per_launch"):
+                return float(k["dram_bytes_per_launch"]), os.path.relpath(p, ROOT)
+        except Exception:
+            continue
+    return None, None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def gen_ticks(name: str, count: int, seed_offset: int = 0):
+    from paper_1411_3212_b200.workload import WorkloadConfig, iter_ticks
+
+    kw = dict(WORKLOADS[name])
+    kw["seed"] = kw["seed"] + seed_offset
+    cfg = WorkloadConfig(n_ticks=count, **kw)
+    return list(iter_ticks(cfg))
+
+
+def cpu_reference_sample(n_objects: int, seed: int = 3):
+    """The CPU reference (oracle port, oracle/quad_oracle.py) on one tick of the same
+    generator configuration with `n_objects` objects; returns (queries/s, seconds, m)."""
+    from oracle import quad_oracle as qo
+    from paper_1411_3212_b200.workload import WorkloadConfig, iter_ticks
+
+    kw = dict(WORKLOADS["C5"])
+    kw["n_objects"] = n_objects
+    kw["seed"] = seed
+    tick = next(iter_ticks(WorkloadConfig(n_ticks=1, **kw)))
+    t0 = time.perf_counter()
+    qo.run_tick(tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb)
+    dt = time.perf_counter() - t0
+    return tick.n_queries / dt, dt, tick.n_queries
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    n_sample = args.ref_sample
+    times, qs = [], []
+    for s in range(args.warmup + args.steps):
+        qps, dt, m = cpu_reference_sample(n_sample, seed=3 + s)
+        if s >= args.warmup:
+            times.append(dt)
+            qs.append(m)
+    value = sum(qs) / sum(times)
+    sample = (f"oracle/quad_oracle.run_tick (NumPy port of the reference QUAD tick), one tick per step of "
+              f"{n_sample:,} objects with the workload's generator config (gaussian, 25 hotspots, 100% rate, "
+              f"5u), seeds 3..{3 + args.warmup + args.steps - 1}")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
+        "p50_tick_ms": 1e3 * statistics.median(times), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
+        "config": {"workload": args.workload, "description": DESCR[args.workload], "parallelism": "cpu"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    from paper_1411_3212_b200 import Engine, MethodConfig, _native
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    pool = max(1, min(args.pool, args.steps + args.warmup))
+    ticks = gen_ticks(args.workload, pool, seed_offset=1000 * rank)
+    dev = torch.device("cuda", local)
+
+    def to_dev(t):
+        return [torch.from_numpy(a).to(dev) for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb, t.qyb)]
+
+    dticks = [to_dev(t) for t in ticks]
+    eng = Engine(MethodConfig(method="quad", device=local))
+    ctx = eng.native
+    stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+
+    def tick_dev(k):
+        a = dticks[k % pool]
+        return ctx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
+                             *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
+
+    for k in range(args.warmup):
+        tick_dev(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record(stream)
+    stats = []
+    queries = 0
+    for k in range(args.steps):
+        _, st = tick_dev(args.warmup + k)
+        ev[k + 1].record(stream)
+        stats.append(st)
+        queries += int(st.n_queries)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = ev[0].elapsed_time(ev[-1])
+    per_tick = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+        qt = torch.tensor([queries], device=dev, dtype=torch.int64)
+        torch.distributed.all_reduce(qt)
+        queries = int(qt.item())
+    value = queries / (total_ms / 1e3)
+
+    # roofline of the dominant kernel (the per-leaf join): algorithmic bytes per launch
+    # = 16*P_a (x, y of task objects) + 44*S_a (slot 4 + query row 4 + clipped rect 32 + count 4)
+    # + 4*W (bitmap words written); SURVEY.md §8(d) K3 row.
+    join_ms = statistics.mean(s.t_join_ms for s in stats)
+    st0 = stats[-1]
+    join_bytes = 16 * st0.task_objects + 44 * st0.task_subqueries + 4 * st0.bitmap_words
+    peak, peak_src = measured_peak()
+    achieved = join_bytes / (join_ms / 1e3) / 1e9
+    traffic, traffic_src = ncu_traffic("k_join")
+    # index build (K1) roofline for the record: compulsory 44n + 4Z + 12L
+    idx_ms = statistics.mean(s.t_index_ms for s in stats)
+    n = int(st0.n_objects)
+
+    # end to end through the C ABI with pinned host buffers: H2D inputs + D2H CSR per step
+    e2e = None
+    if not args.no_e2e:
+        hticks = [[torch.from_numpy(a).pin_memory() for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb,
+                                                                t.qyb)] for t in ticks]
+
+        def tick_host(k):
+            a = hticks[k % pool]
+            return ctx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
+                                 *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST)
+
+        tick_host(0)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        e0.record(stream)
+        h2d = d2h = eq = 0
+        for k in range(e_steps):
+            out, st = tick_host(k)
+            a = hticks[k % pool]
+            h2d += sum(x.numel() * x.element_size() for x in a)
+            d2h += 8 * (out.n_q + 1) + 8 * out.n_results
+            eq += int(st.n_queries)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = e0.elapsed_time(e1)
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e_ms = float(t.item())
+            eq *= world
+        e2e = {"value": eq / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // e_steps,
+               "d2h_bytes_per_step": d2h // e_steps, "steps": e_steps,
+               "api": "tj_tick (C ABI) with pinned host input/output buffers"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        qps, dt, m = cpu_reference_sample(args.cpu_sample)
+        cpu = {"value": qps, "unit": UNIT, "cores": 1, "kind": "port",
+               "sample": (f"oracle/quad_oracle.run_tick (NumPy port of the reference QUAD tick) on one tick of "
+                          f"{args.cpu_sample:,} objects / {m:,} queries with the workload's generator config "
+                          f"(gaussian, 25 hotspots, 5u); {dt:.1f} s single-threaded")}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "p50_tick_ms": statistics.median(per_tick), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
+            "config": {"workload": args.workload, "description": DESCR[args.workload],
+                       "n_objects": n, "queries_per_tick": int(st0.n_queries),
+                       "results_per_tick": int(st0.results_total), "th_quad": 384, "l_max": 12,
+                       "rebuild": "every_tick", "distinct_ticks_cycled": pool,
+                       "l2": "inputs (>=560 MB/tick at 10M) exceed the 126 MB L2; no flush",
+                       "parallelism": f"{world} independent shard(s), one per GPU" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "kernel": "tj::k_join",
+                         "bytes_per_launch": join_bytes, "ms_per_launch": join_ms, "peak_source": peak_src,
+                         "traffic_source": traffic_src,
+                         "tests_per_s": st0.containment_tests / (join_ms / 1e3)},
+            "roofline_index": {"kernel": "K1 index build (all kernels up to the leaf directory)",
+                               "ms": idx_ms, "compulsory_bytes": 44 * n + 4 * (4 ** int(st0.l_deep)) +
+                               12 * int(st0.n_leaves)},
+            "stage_ms": {k: statistics.mean(getattr(s, f"t_{k}_ms") for s in stats)
+                         for k in ("index", "filter", "join", "decode", "merge", "total")},
+            "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": int(sum(int(s.kernel_launches) for s in stats)),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
+    ap.add_argument("--pool", type=int, default=3, help="distinct ticks generated and cycled")
+    ap.add_argument("--cpu-sample", type=int, default=1_000_000)
+    ap.add_argument("--ref-sample", type=int, default=500_000)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    return run_reference(args) if args.impl == "reference" else run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -43,9 +43,9 @@ struct tj_ctx {
   // index
   DBuf pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf crect, qwin, nsub, qsbase;
+  DBuf crect, qwin, nsub, qsbase, biglist;
   // subqueries
-  DBuf sqleaf, sqq, sqcov, sqcount, slotout, skey0, skey1, sval0, sval1;
+  DBuf sqleaf, sqq, sqcov, sqcount, slotout, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
   // join / outputs
   DBuf bitmap, stage, outids, outoff;
   // scan / radix scratch
@@ -56,7 +56,7 @@ struct tj_ctx {
   void* h_ids = nullptr;
   size_t h_ids_bytes = 0;
   // capacities of the dynamically sized arenas
-  int64_t cap_S = 0, cap_W = 0, cap_R = 0, cap_L = 0, cap_heavy = 0;
+  int64_t cap_S = 0, cap_W = 0, cap_R = 0, cap_L = 0, cap_heavy = 0, cap_U = 0;
   int64_t last_L = 0;
   // last tick, for introspection
   bool have = false;
@@ -167,18 +167,22 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(lsbase, c->cap_L * 4);
   ENS(lwoff, c->cap_L * 8);
   ENS(lubase, c->cap_L * 8);
+  ENS(runs0, c->cap_L * 2 * 4);
+  ENS(runs1, c->cap_L * 2 * 4);
   ENS(crect, m * sizeof(Rect4));
   ENS(qwin, m * sizeof(int4));
   ENS(nsub, m * 4);
   ENS(qsbase, m * 4);
+  ENS(biglist, m * 4);
   ENS(outoff, (m + 1) * 8);
   ENS(partial, 1024 * 8);
   const int Gr = 2 * c->num_sms;
-  ENS(rhist, (int64_t)256 * Gr * 4);
-  ENS(roffs, (int64_t)256 * Gr * 8);
+  ENS(rhist, (int64_t)kRadixDigits * Gr * 4);
+  ENS(roffs, (int64_t)kRadixDigits * Gr * 8);
   if (c->cap_S == 0) c->cap_S = 4 * m + 256;
   if (c->cap_W == 0) c->cap_W = 8 * c->cap_S + 4096;
   if (c->cap_R == 0) c->cap_R = 16 * m + 4096;
+  if (c->cap_U == 0) c->cap_U = c->cap_S + c->cap_L;
 #undef ENS
   return TJ_OK;
 }
@@ -197,6 +201,7 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sval0, c->cap_S * 4);
   ENS(sval1, c->cap_S * 4);
   ENS(bitmap, c->cap_W * 4);
+  ENS(unitleaf, c->cap_U * 4);
   ENS(stage, c->cap_R * 8);
   ENS(outids, c->cap_R * 8);
 #undef ENS
@@ -258,6 +263,11 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.SUB = sub_size(d.D);
   d.sidx = d.oval[c->obj_passes & 1];
   d.ssorted = d.sval[c->sq_passes & 1];
+  d.skey_sorted = d.skey[c->sq_passes & 1];
+  d.run_start = P<int32_t>(c->runs0);
+  d.run_end = P<int32_t>(c->runs1);
+  d.unit_leaf = P<int32_t>(c->unitleaf);
+  d.big_list = P<int32_t>(c->biglist);
 }
 
 // stable LSD radix sort of (key, value) pairs over `passes` 8-bit digits
@@ -266,11 +276,12 @@ void radix_sort(tj_ctx* c, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, 
   ScanPlan sp{std::min(1024, 2 * c->num_sms), P<int64_t>(c->partial)};
   for (int p = 0; p < passes; ++p) {
     const int src = p & 1, dst = src ^ 1;
-    k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], n_ptr, c->d_hdr, 8 * p, P<uint32_t>(c->rhist));
+    k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], n_ptr, c->d_hdr, kRadixBits * p,
+                                                      P<uint32_t>(c->rhist));
     scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)},
                 c->d_consts, c->d_hdr, (int64_t*)nullptr, c->st);
     k_radix_downsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], v[src], k[dst], v[dst], n_ptr, c->d_hdr,
-                                                        8 * p, P<int64_t>(c->roffs));
+                                                        kRadixBits * p, P<int64_t>(c->roffs));
   }
 }
 
@@ -289,8 +300,8 @@ int launch_tick(tj_ctx* c) {
   ScanPlan sp{std::min(1024, 2 * c->num_sms), P<int64_t>(c->partial)};
 
   cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
-  cudaMemsetAsync(d.leaf_nisq, 0, c->cap_L * 4, st);
-  cudaMemsetAsync(d.leaf_ncov, 0, c->cap_L * 4, st);
+  cudaMemsetAsync(d.run_start, 0, c->cap_L * 2 * 4, st);
+  cudaMemsetAsync(d.run_end, 0, c->cap_L * 2 * 4, st);
 
   cudaEventRecord(c->ev[0], st);
   // ---- K0 / K1: index build -------------------------------------------
@@ -308,7 +319,7 @@ int launch_tick(tj_ctx* c) {
   k_finalize_index<<<1, 1, 0, st>>>(h);
   k_cell_level<<<Gbig, 256, 0, st>>>(d);
   scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
-  k_check_caps<<<1, 1, 0, st>>>(h, 0, 8 * c->obj_passes, 8 * c->sq_passes);
+  k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, kRadixBits * c->sq_passes);
   k_obj_keys<<<Gn, 256, 0, st>>>(d);
   radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
   scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr, st);
@@ -318,16 +329,15 @@ int launch_tick(tj_ctx* c) {
   scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
   k_query_fill<<<Gm, 256, 0, st>>>(d);
-  k_sq_keys<<<Gbig, 256, 0, st>>>(d);
   radix_sort(c, d.skey, d.sval, &h->S, c->sq_passes);
-  scan_launch(sp, LeafSubIn{d.leaf_nisq, d.leaf_ncov}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
-              (int64_t*)nullptr, st);
+  k_sq_runs<<<Gbig, 256, 0, st>>>(d);
   k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[1], st);
   // ---- K3: join -----------------------------------------------------------
   scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h, &h->W, st);
   scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h, &h->U, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 2, 0, 0);
+  k_unit_map<<<Gbig, 256, 0, st>>>(d);
   k_zero_counts<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[2], st);
   k_join<<<c->num_sms * 8, kJoinThreads, 0, st>>>(d);
@@ -337,14 +347,13 @@ int launch_tick(tj_ctx* c) {
               h, &h->R, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
   k_query_offsets<<<Gm, 256, 0, st>>>(d);
-  k_decode<<<Gbig, 256, 0, st>>>(d);
-  k_cover<<<Gbig, 256, 0, st>>>(d);
+  k_decode_leaf<<<Gbig, kDecodeThreads, 0, st>>>(d);
   cudaEventRecord(c->ev[4], st);
   k_merge_runs<<<Gbig, 256, 0, st>>>(d);
-  k_sort_queries<<<c->num_sms * 4, 256, 0, st>>>(d);
+  k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[5], st);
   // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-  const int scans = 7, singles = 23 + F + (D > 0 ? 3 + (D - 1) : 0);
+  const int scans = 6, singles = 23 + F + (D > 0 ? 3 + (D - 1) : 0);
   return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles;
 }
 
@@ -360,7 +369,7 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.cap_S = c->cap_S;
   H.cap_W = c->cap_W;
   H.cap_R = c->cap_R;
-  H.cap_U = INT64_MAX;
+  H.cap_U = c->cap_U;
   H.cap_L = c->cap_L;
   H.cap_heavy = c->cap_heavy;
   H.kmin_x = H.kmin_y = ~0ull;
@@ -368,7 +377,7 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.l_deep = 1;
 }
 
-int passes_for(int64_t maxkey) { return std::max(1, (bits_for(maxkey) + 7) / 8); }
+int passes_for(int64_t maxkey) { return std::max(1, (bits_for(maxkey) + kRadixBits - 1) / kRadixBits); }
 
 int check_launch(tj_ctx* c) {
   cudaError_t e = cudaGetLastError();
@@ -426,7 +435,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
     return fail(nullptr, TJ_E_CUDA, msg);
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
-  int64_t consts[8] = {(int64_t)256 * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
+  int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
   *out = c;
   return TJ_OK;
@@ -439,8 +448,9 @@ int tj_destroy(tj_ctx* c) {
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->sqleaf, &c->sqq, &c->sqcov,
-                 &c->sqcount, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->bitmap,
+                 &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
+                 &c->sqcount, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
+                 &c->runs1, &c->unitleaf, &c->bitmap,
                  &c->stage, &c->outids, &c->outoff, &c->partial, &c->rhist, &c->roffs};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
@@ -532,7 +542,10 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
         c->sq_passes = passes_for(2 * H.L - 1);
       }
       if (H.abort & 1) c->cap_S = std::max<int64_t>(2 * c->cap_S, H.S + H.S / 4 + 256);
-      if (H.abort & 2) c->cap_W = std::max<int64_t>(2 * c->cap_W, H.W + H.W / 4 + 4096);
+      if (H.abort & 2) {
+        c->cap_W = std::max<int64_t>(c->cap_W, H.W + H.W / 4 + 4096);
+        c->cap_U = std::max<int64_t>(c->cap_U, H.U + H.U / 4 + 1024);
+      }
       if (H.abort & 4) c->cap_R = std::max<int64_t>(2 * c->cap_R, H.R + H.R / 4 + 4096);
     }
     if (!done) return fail(c, TJ_E_CUDA, "tick did not converge after capacity growth");
@@ -716,7 +729,7 @@ int tj_get_subqueries(tj_ctx* c, int64_t* count, int64_t* q_row, int64_t* cell, 
   for (int64_t s = 0; s < S; ++s) {
     if (q_row) q_row[s] = q[s];
     if (cell) cell[s] = lv.packed[leaf[s]];
-    if (covering) covering[s] = cv[s];
+    if (covering) covering[s] = cv[s] & 1;
   }
   return TJ_OK;
 }

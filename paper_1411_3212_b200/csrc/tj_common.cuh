@@ -47,7 +47,7 @@ struct DevHdr {
   int32_t dup;              // DuplicateResult detected
   int32_t oob;              // OutOfBounds (adaptive reuse: object outside old MBR)
   int32_t count_mismatch;   // CountMismatch
-  int32_t pad0;
+  int32_t n_big;            // queries queued for k_merge_big
   unsigned long long overfull2, overfull8;  // needs_rebuild counters
 };
 

@@ -96,59 +96,71 @@ struct ExclOut {
 };
 
 // ---------------------------------------------------------------------------
-// Stable LSD radix sort of (u32 key, i32 value) pairs, 8-bit digits.
+// Stable LSD radix sort of (u32 key, i32 value) pairs, kRadixBits-bit digits.
 // Upsweep: per-chunk digit histograms; scan over (digit, chunk); downsweep:
 // each CTA walks its chunk in input order, ranks items per digit with warp
-// match (stable: warp w / round k / lane order), stages the tile by digit in
+// ballots (stable: warp w / round k / lane order), stages the tile by digit in
 // shared memory and writes digit runs coalesced.
 // ---------------------------------------------------------------------------
+constexpr int kRadixBits = 9;                       // 2 passes cover 18-bit keys
+constexpr int kRadixDigits = 1 << kRadixBits;       // 512
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
+constexpr int kRadixDPT = kRadixDigits / kRadixThreads;  // digits per thread (2)
 constexpr int kRadixIPT = 8;                        // items per thread per tile
 constexpr int kRadixTile = kRadixThreads * kRadixIPT;  // 2048
 
+__device__ __forceinline__ int64_t radix_chunk(int64_t n, int64_t G) {
+  return ((n + G - 1) / G + kRadixTile - 1) / kRadixTile * kRadixTile;
+}
+
 __global__ void __launch_bounds__(kRadixThreads)
 k_radix_upsweep(const uint32_t* keys, const int64_t* n_ptr, const DevHdr* h, int shift,
-                uint32_t* hist /* [256][G] */) {
+                uint32_t* hist /* [digits][G] */) {
   if (h->abort) return;
-  __shared__ uint32_t cnt[256];
+  __shared__ uint32_t cnt[kRadixWarps][kRadixDigits];
   const int64_t n = *n_ptr, G = gridDim.x;
-  const int64_t chunk = ((n + G - 1) / G + kRadixTile - 1) / kRadixTile * kRadixTile;
+  const int64_t chunk = radix_chunk(n, G);
   const int64_t b = blockIdx.x * chunk;
   const int64_t e = (b + chunk < n) ? b + chunk : n;
-  cnt[threadIdx.x] = 0;
+  const int w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&cnt[0][0])[k] = 0;
   __syncthreads();
-  for (int64_t bb = b; bb < e; bb += blockDim.x) {  // uniform trip count: full warps
-    const int64_t i = bb + threadIdx.x;
-    const bool ok = i < e;
-    const uint32_t d = ok ? ((keys[i] >> shift) & 255u) : 256u;
-    const uint32_t peers = __match_any_sync(0xffffffffu, d);
-    if (ok && (int)(__ffs(peers) - 1) == lane_id()) atomicAdd(&cnt[d], (uint32_t)__popc(peers));
+  for (int64_t i = b + threadIdx.x; i < e; i += kRadixThreads)
+    atomicAdd(&cnt[w][(keys[i] >> shift) & (kRadixDigits - 1)], 1u);
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < kRadixDPT; ++j) {
+    const int dgt = threadIdx.x + j * kRadixThreads;
+    uint32_t s = 0;
+#pragma unroll
+    for (int ww = 0; ww < kRadixWarps; ++ww) s += cnt[ww][dgt];
+    hist[(int64_t)dgt * G + blockIdx.x] = s;
   }
-  __syncthreads();
-  hist[(int64_t)threadIdx.x * G + blockIdx.x] = cnt[threadIdx.x];
 }
 
 __global__ void __launch_bounds__(kRadixThreads)
 k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out,
                   int32_t* vals_out, const int64_t* n_ptr, const DevHdr* h, int shift,
-                  const int64_t* offs /* [256][G] exclusive */) {
+                  const int64_t* offs /* [digits][G] exclusive */) {
   if (h->abort) return;
-  __shared__ uint32_t wcnt[kRadixWarps][256];
-  __shared__ uint32_t base[256];      // running global offset per digit for this chunk
-  __shared__ uint32_t tprefix[256];   // tile-local exclusive prefix per digit
+  __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];
+  __shared__ uint32_t base[kRadixDigits];     // running global offset per digit (this chunk)
+  __shared__ uint32_t tprefix[kRadixDigits];  // tile-local exclusive prefix per digit
   __shared__ uint32_t skey[kRadixTile];
   __shared__ int32_t sval[kRadixTile];
   __shared__ int64_t shs[33];
   const int64_t n = *n_ptr, G = gridDim.x;
-  const int64_t chunk = ((n + G - 1) / G + kRadixTile - 1) / kRadixTile * kRadixTile;
+  const int64_t chunk = radix_chunk(n, G);
   const int64_t b = blockIdx.x * chunk;
   const int64_t e = (b + chunk < n) ? b + chunk : n;
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
-  base[t] = (uint32_t)offs[(int64_t)t * G + blockIdx.x];
+#pragma unroll
+  for (int j = 0; j < kRadixDPT; ++j)
+    base[t + j * kRadixThreads] = (uint32_t)offs[(int64_t)(t + j * kRadixThreads) * G + blockIdx.x];
   const uint32_t lt = (1u << lane) - 1u;
   for (int64_t tb = b; tb < e; tb += kRadixTile) {
-    for (int k = t; k < kRadixWarps * 256; k += kRadixThreads) (&wcnt[0][0])[k] = 0;
+    for (int k = t; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&wcnt[0][0])[k] = 0;
     __syncthreads();
     uint32_t key[kRadixIPT], dig[kRadixIPT], rk[kRadixIPT];
     int32_t val[kRadixIPT];
@@ -159,8 +171,15 @@ k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* key
       const bool ok = i < e;
       key[r] = ok ? keys_in[i] : 0u;
       val[r] = ok ? vals_in[i] : 0;
-      dig[r] = ok ? ((key[r] >> shift) & 255u) : 256u;
-      const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
+      // invalid lanes get digit kRadixDigits (the extra bit below)
+      dig[r] = ok ? ((key[r] >> shift) & (kRadixDigits - 1)) : (uint32_t)kRadixDigits;
+      uint32_t peers = 0xffffffffu;
+#pragma unroll
+      for (int bit = 0; bit <= kRadixBits; ++bit) {
+        const bool on = (dig[r] >> bit) & 1u;
+        const uint32_t bal = __ballot_sync(0xffffffffu, on);
+        peers &= on ? bal : ~bal;
+      }
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (ok && lane == leader) {
@@ -172,21 +191,29 @@ k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* key
       __syncwarp();
     }
     __syncthreads();
-    // per digit: prefix across warps, tile total
-    uint32_t run = 0;
+    // per digit: exclusive prefix across warps, tile total, tile-local digit offsets
+    uint32_t run[kRadixDPT];
+    int64_t carry = 0;
 #pragma unroll
-    for (int ww = 0; ww < kRadixWarps; ++ww) {
-      const uint32_t c = wcnt[ww][t];
-      wcnt[ww][t] = run;
-      run += c;
+    for (int j = 0; j < kRadixDPT; ++j) {
+      const int dgt = t + j * kRadixThreads;
+      uint32_t acc = 0;
+#pragma unroll
+      for (int ww = 0; ww < kRadixWarps; ++ww) {
+        const uint32_t c = wcnt[ww][dgt];
+        wcnt[ww][dgt] = acc;
+        acc += c;
+      }
+      run[j] = acc;
+      int64_t tot;
+      const int64_t ex = block_excl_scan((int64_t)acc, shs, &tot);
+      tprefix[dgt] = (uint32_t)(ex + carry);
+      carry += tot;
     }
-    int64_t tot;
-    const int64_t ex = block_excl_scan((int64_t)run, shs, &tot);
-    tprefix[t] = (uint32_t)ex;
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kRadixIPT; ++r) {
-      if (dig[r] < 256u) {
+      if (dig[r] < (uint32_t)kRadixDigits) {
         const uint32_t pos = tprefix[dig[r]] + wcnt[w][dig[r]] + rk[r];
         skey[pos] = key[r];
         sval[pos] = val[r];
@@ -196,13 +223,14 @@ k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* key
     const int tile_n = (int)((e - tb) < kRadixTile ? (e - tb) : kRadixTile);
     for (int p = t; p < tile_n; p += kRadixThreads) {
       const uint32_t k = skey[p];
-      const uint32_t d = (k >> shift) & 255u;
+      const uint32_t d = (k >> shift) & (kRadixDigits - 1);
       const int64_t dst = (int64_t)base[d] + (p - tprefix[d]);
       keys_out[dst] = k;
       vals_out[dst] = sval[p];
     }
     __syncthreads();
-    base[t] += run;
+#pragma unroll
+    for (int j = 0; j < kRadixDPT; ++j) base[t + j * kRadixThreads] += run[j];
     __syncthreads();
   }
 }
