@@ -45,9 +45,9 @@ struct tj_ctx {
   // queries
   DBuf crect, qwin, nsub, qsbase, biglist;
   // subqueries
-  DBuf sqleaf, sqq, sqcov, sqcount, slotout, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
+  DBuf sqleaf, sqq, sqcov, sqcount, ecount, slotout, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
   // join / outputs
-  DBuf bitmap, stage, outids, outoff;
+  DBuf bitmap, stage, outids, outoff, runoff, scratch;
   // scan / radix scratch
   DBuf partial, rhist, roffs;
   // pinned host outputs
@@ -195,6 +195,7 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sqq, c->cap_S * 4);
   ENS(sqcov, c->cap_S);
   ENS(sqcount, c->cap_S * 4);
+  ENS(ecount, c->cap_S * 4);
   ENS(slotout, c->cap_S * 8);
   ENS(skey0, c->cap_S * 4);
   ENS(skey1, c->cap_S * 4);
@@ -202,7 +203,9 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sval1, c->cap_S * 4);
   ENS(bitmap, c->cap_W * 4);
   ENS(unitleaf, c->cap_U * 4);
-  ENS(stage, c->cap_R * 8);
+  ENS(stage, c->cap_R * 4);
+  ENS(scratch, c->cap_R * 8);
+  ENS(runoff, c->cap_S * 8);
   ENS(outids, c->cap_R * 8);
 #undef ENS
   return TJ_OK;
@@ -250,13 +253,14 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.sq_q = P<int32_t>(c->sqq);
   d.sq_cov = P<uint8_t>(c->sqcov);
   d.sq_count = P<int32_t>(c->sqcount);
+  d.ecount = P<int32_t>(c->ecount);
   d.slot_out = P<int64_t>(c->slotout);
   d.skey[0] = P<uint32_t>(c->skey0);
   d.skey[1] = P<uint32_t>(c->skey1);
   d.sval[0] = P<int32_t>(c->sval0);
   d.sval[1] = P<int32_t>(c->sval1);
   d.bitmap = P<uint32_t>(c->bitmap);
-  d.stage = P<int64_t>(c->stage);
+  d.stage = P<int32_t>(c->stage);
   d.out_ids = P<int64_t>(c->outids);
   d.out_off = P<int64_t>(c->outoff);
   d.D = lmax - F;
@@ -268,12 +272,14 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.run_end = P<int32_t>(c->runs1);
   d.unit_leaf = P<int32_t>(c->unitleaf);
   d.big_list = P<int32_t>(c->biglist);
+  d.run_off = P<int64_t>(c->runoff);
+  d.scratch = P<int64_t>(c->scratch);
 }
 
 // stable LSD radix sort of (key, value) pairs over `passes` 8-bit digits
 void radix_sort(tj_ctx* c, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, int passes) {
   const int Gr = 2 * c->num_sms;
-  ScanPlan sp{std::min(1024, 2 * c->num_sms), P<int64_t>(c->partial)};
+  ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
   for (int p = 0; p < passes; ++p) {
     const int src = p & 1, dst = src ^ 1;
     k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], n_ptr, c->d_hdr, kRadixBits * p,
@@ -297,7 +303,7 @@ int launch_tick(tj_ctx* c) {
   const int64_t n = c->n, m = c->m;
   const int Gn = grid_for(c, n), Gm = grid_for(c, m);
   const int Gbig = c->num_sms * 8;
-  ScanPlan sp{std::min(1024, 2 * c->num_sms), P<int64_t>(c->partial)};
+  ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
 
   cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
   cudaMemsetAsync(d.run_start, 0, c->cap_L * 2 * 4, st);
@@ -323,7 +329,9 @@ int launch_tick(tj_ctx* c) {
   k_obj_keys<<<Gn, 256, 0, st>>>(d);
   radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
   scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr, st);
-  k_gather<<<Gn, 256, 0, st>>>(d);
+  k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
+  k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
+  k_gather<int64_t><<<Gn, 256, 0, st>>>(d, d.ids, d.sid);
   // ---- K2: query -> leaf scatter ----------------------------------------
   k_query_count<<<Gm, 256, 0, st>>>(d);
   scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
@@ -343,17 +351,18 @@ int launch_tick(tj_ctx* c) {
   k_join<<<c->num_sms * 8, kJoinThreads, 0, st>>>(d);
   cudaEventRecord(c->ev[3], st);
   // ---- K4: decode + canonical lists --------------------------------------
-  scan_launch(sp, SlotCntIn{d.sq_cov, d.sq_leaf, d.leaf_nobj, d.sq_count}, ExclOut<int64_t>{d.slot_out}, &h->S,
-              h, &h->R, st);
+  k_cov_counts<<<Gbig, 256, 0, st>>>(d);
+  scan_launch(sp, RowCntIn{d}, RowOut{d}, &h->S, h, &h->R, st);
+  scan_launch(sp, QueryCntIn{d}, ExclOut<int64_t>{d.out_off}, &h->m, h, &h->R_check, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
-  k_query_offsets<<<Gm, 256, 0, st>>>(d);
+  k_close_offsets<<<1, 1, 0, st>>>(d);
   k_decode_leaf<<<Gbig, kDecodeThreads, 0, st>>>(d);
   cudaEventRecord(c->ev[4], st);
-  k_merge_runs<<<Gbig, 256, 0, st>>>(d);
+  k_assemble<<<Gbig, 256, 0, st>>>(d);
   k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[5], st);
   // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-  const int scans = 6, singles = 23 + F + (D > 0 ? 3 + (D - 1) : 0);
+  const int scans = 7, singles = 26 + F + (D > 0 ? 3 + (D - 1) : 0);
   return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles;
 }
 
@@ -449,9 +458,9 @@ int tj_destroy(tj_ctx* c) {
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
-                 &c->sqcount, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
+                 &c->sqcount, &c->ecount, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
                  &c->runs1, &c->unitleaf, &c->bitmap,
-                 &c->stage, &c->outids, &c->outoff, &c->partial, &c->rhist, &c->roffs};
+                 &c->stage, &c->outids, &c->outoff, &c->runoff, &c->scratch, &c->partial, &c->rhist, &c->roffs};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->h_off) cudaFreeHost(c->h_off);
@@ -553,6 +562,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     c->last = H;
     c->last_L = H.L;
     if (H.dup) return fail(c, TJ_E_DUPLICATE_RESULT, "a (query, object) pair was produced twice");
+    if (H.count_mismatch) return fail(c, TJ_E_COUNT_MISMATCH, "decoded counts disagree with popcounts");
     R = H.R;
     c->have = true;
     float ms[5] = {0, 0, 0, 0, 0}, tot = 0;

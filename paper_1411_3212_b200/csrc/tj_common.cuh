@@ -38,12 +38,15 @@ struct DevHdr {
   int64_t S, S_i, S_c;      // subqueries: all / intersecting / covering
   int64_t n_tasks, W, U;    // join tasks, bitmap words, work units
   int64_t R;                // results
+  int64_t R_check;          // results counted in query order (must equal R)
   // statistics (engine.py:212-258)
   unsigned long long tests, cov_results, active_cells, occ_sum, occ_sumsq, sum_isq, sum_cov;
   unsigned long long task_obj, task_isq;  // P_a, S_a: objects / subqueries inside join tasks
   // flags
   int32_t abort;            // bit0 S, bit1 W/U, bit2 R, bit3 heavy, bit4 L
   int32_t not_monotone;     // object ids not strictly increasing in input order
+  int32_t not_identity;     // some object id differs from its input row
+  int32_t pad1;
   int32_t dup;              // DuplicateResult detected
   int32_t oob;              // OutOfBounds (adaptive reuse: object outside old MBR)
   int32_t count_mismatch;   // CountMismatch

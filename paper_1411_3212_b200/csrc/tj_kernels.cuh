@@ -66,7 +66,8 @@ struct Dev {
   int32_t* sq_q;
   uint8_t* sq_cov;
   int32_t* sq_count;
-  int64_t* slot_out;
+  int32_t* ecount;          // result count per decode entry e (entry order of ssorted)
+  int64_t* slot_out;       // per decode row e: start of its list in `stage`
   uint32_t* skey[2];
   int32_t* sval[2];
   const int32_t* ssorted;  // per leaf [isq slots asc][cov slots asc]
@@ -75,9 +76,11 @@ struct Dev {
   int32_t* run_end;        // one past the last
   int32_t* unit_leaf;      // join work unit -> leaf
   int32_t* big_list;       // queries whose lists need the CTA-wide merge
+  int64_t* run_off;        // per subquery slot: start of its decoded run in `stage`
+  int64_t* scratch;        // R entries: merge-pass scratch for k_merge_big
   // join + outputs
   uint32_t* bitmap;
-  int64_t* stage;
+  int32_t* stage;          // decoded runs (input rows), decode order
   int64_t* out_ids;
   int64_t* out_off;
   // config
@@ -134,12 +137,19 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
 // Also detects whether object ids strictly increase in input order: then
 // per-leaf blocks (input order) are id-sorted and per-query merges are merges
 // of sorted runs.
+// (and whether id == input row, the generator's arange ids: then the final
+// lists need no id lookup at all)
 __global__ void __launch_bounds__(256) k_monotone(const Dev d) {
   DevHdr* h = d.h;
   const int64_t n = h->n;
-  int bad = 0;
-  TJ_GRID_STRIDE(i, n - 1) { bad |= (d.ids[i] >= d.ids[i + 1]); }
+  int bad = 0, notid = 0;
+  TJ_GRID_STRIDE(i, n) {
+    const int64_t v = d.ids[i];
+    notid |= (v != i);
+    if (i + 1 < n) bad |= (v >= d.ids[i + 1]);
+  }
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(&h->not_monotone, 1);
+  if (__any_sync(0xffffffffu, notid) && lane_id() == 0) atomicOr(&h->not_identity, 1);
 }
 
 __global__ void k_finalize_mbr(DevHdr* h) {
@@ -370,16 +380,15 @@ __global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
   }
 }
 
-__global__ void __launch_bounds__(256) k_gather(const Dev d) {
+// Payload gather into leaf order, one array per launch: each launch's random
+// reads hit one 80 MB array (at 10M objects) that stays L2-resident, instead
+// of three arrays (240 MB) thrashing the 126 MB L2 together.
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather(const Dev d, const T* __restrict__ src, T* __restrict__ dst) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const int64_t n = h->n;
-  TJ_GRID_STRIDE(p, n) {
-    const int32_t i = d.sidx[p];
-    d.sx[p] = d.xs[i];
-    d.sy[p] = d.ys[i];
-    d.sid[p] = d.ids[i];
-  }
+  TJ_GRID_STRIDE(p, n) dst[p] = src[d.sidx[p]];
 }
 
 // checks after a size became known: abort bits make the rest of the tick a no-op
@@ -661,7 +670,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
 // ===========================================================================
 constexpr int kJoinThreads = 256;
 constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr int kST = 128;  // subqueries per work unit
+constexpr int kST = 32;   // subqueries per work unit (one warp, lane = subquery)
 constexpr int kOTB = 32;  // 32-object blocks per work unit (1024 objects)
 
 struct WordsIn {
@@ -697,35 +706,49 @@ __global__ void __launch_bounds__(256) k_unit_map(const Dev d) {
 __global__ void __launch_bounds__(256) k_zero_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  TJ_GRID_STRIDE(s, h->S) d.sq_count[s] = 0;
+  TJ_GRID_STRIDE(s, h->S) {
+    d.sq_count[s] = 0;
+    d.ecount[s] = 0;
+  }
 }
 
-// One CTA per work unit (leaf, 128-subquery tile, 1024-object tile).  The
-// unit's objects are staged in shared memory as (x, y) pairs and its clipped
-// subquery rects as Rect4.  Work is split into (32-subquery chunk, 32-object
-// block) pairs; a warp takes a pair with lane = subquery: the lane keeps its
-// rect in registers, walks the block's 32 objects (shared-memory broadcast)
-// and sets bit k of its word when object k passes the four closed fp64
-// comparisons (bitmap.py:89-94) — so bit k of word (s, b) is object 32b+k of
-// the leaf's block (bitmap.py:95-97) and the word lands directly in lane s.
-// Words are staged per tile and stored in the linear layout
+// Warp-level work units: (leaf, 32 intersecting subqueries, up to 1024
+// objects), lane = subquery.  The lane keeps its clipped rect in registers;
+// for each 32-object block of the leaf, the warp stages the block's (x, y)
+// pairs in its shared-memory slice (prefetching the next block), and every
+// lane walks the 32 objects (broadcast loads) with four chained closed fp64
+// comparisons + one predicated OR per object (bitmap.py:89-94) — bit k of the
+// lane's word is object 32b+k of the leaf's block (bitmap.py:95-97), i.e. the
+// paper's bitmap word lands directly in the subquery's lane, no ballot or
+// transpose.  Words are staged per warp and stored in the linear layout
 // linear[s*blocks + b] (bitmap.py:105-111) with coalesced rows; popcounts
-// (bitmap.py:114-119) accumulate in shared memory.
+// (bitmap.py:114-119) stay in registers.  Warps never wait on each other.
 struct __align__(16) XY {
   double x, y;
 };
 
-__global__ void __launch_bounds__(kJoinThreads) k_join(const Dev d) {
+__device__ __forceinline__ XY load_obj(const Dev& d, int32_t ob, int k, int nobj) {
+  XY o;
+  if (k < nobj) {
+    o.x = d.sx[ob + k];
+    o.y = d.sy[ob + k];
+  } else {  // padding objects never match (NaN compares false): padding bits stay zero
+    o.x = __longlong_as_double(0x7ff8000000000000ll);
+    o.y = o.x;
+  }
+  return o;
+}
+
+__global__ void __launch_bounds__(kJoinThreads, 4) k_join(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  __shared__ Rect4 rect[kST];
-  __shared__ XY obj[kOTB * 32];
-  __shared__ uint32_t tile[kST][kOTB + 1];
-  __shared__ uint32_t cnt[kST];
-  __shared__ int32_t slots[kST];
+  __shared__ XY sobj[kJoinWarps][32];
+  __shared__ uint32_t stile[kJoinWarps][32][kOTB + 1];
   const int64_t U = h->U;
-  const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
-  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+  const int lane = lane_id(), wp = threadIdx.x >> 5;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  XY* so = sobj[wp];
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarp) {
     const int64_t r = d.unit_leaf[u];
     const int nobj = d.leaf_nobj[r], nisq = d.leaf_nisq[r];
     const int nb = (nobj + 31) >> 5;
@@ -734,39 +757,26 @@ __global__ void __launch_bounds__(kJoinThreads) k_join(const Dev d) {
     const int st = lu / n_ot, ot = lu - st * n_ot;
     const int s0 = st * kST, ns = min(kST, nisq - s0);
     const int b0 = ot * kOTB, nbt = min(kOTB, nb - b0);
-    const int32_t sb = d.leaf_sbase[r];
-    const int32_t ob = d.leaf_obase[r] + b0 * 32;
-    const int no = min(nbt * 32, nobj - b0 * 32);  // objects in this tile
-    if (t < ns) {
-      const int32_t slot = d.ssorted[sb + s0 + t];
-      slots[t] = slot;
-      rect[t] = d.crect[d.sq_q[slot]];
-      cnt[t] = 0;
+    const int32_t ob = d.leaf_obase[r];
+    const bool live = lane < ns;
+    int32_t slot = 0;
+    Rect4 R;
+    R.xa = R.ya = __longlong_as_double(0x7ff0000000000000ll);   // +inf: empty rect
+    R.xb = R.yb = __longlong_as_double((long long)0xfff0000000000000ull);  // -inf
+    if (live) {
+      slot = d.ssorted[d.leaf_sbase[r] + s0 + lane];
+      R = d.crect[d.sq_q[slot]];
     }
-    for (int k = t; k < nbt * 32; k += kJoinThreads) {
-      XY o;
-      if (k < no) {
-        o.x = d.sx[ob + k];
-        o.y = d.sy[ob + k];
-      } else {  // padding objects never match (NaN compares false): padding bits stay zero
-        o.x = __longlong_as_double(0x7ff8000000000000ll);
-        o.y = o.x;
-      }
-      obj[k] = o;
-    }
-    __syncthreads();
-    const int nchunk = (ns + 31) >> 5;
-    const int npairs = nchunk * nbt;
-    for (int p = wp; p < npairs; p += kJoinWarps) {
-      const int sc = p / nbt, bl = p - sc * nbt;
-      const int sl = sc * 32 + lane;
-      const bool live = sl < ns;
-      const Rect4 R = rect[live ? sl : 0];
-      const XY* ob32 = obj + bl * 32;
+    uint32_t cnt = 0;
+    XY nxt = load_obj(d, ob, b0 * 32 + lane, nobj);
+    for (int bl = 0; bl < nbt; ++bl) {
+      so[lane] = nxt;
+      __syncwarp();
+      if (bl + 1 < nbt) nxt = load_obj(d, ob, (b0 + bl + 1) * 32 + lane, nobj);
       uint32_t w = 0;
 #pragma unroll
       for (int k = 0; k < 32; ++k) {
-        const XY o = ob32[k];
+        const XY o = so[k];
         // closed test, chained predicates: 4 DSETP + 1 predicated OR per object
         asm("{\n\t.reg .pred p;\n\t"
             "setp.ge.f64 p, %1, %2;\n\t"
@@ -777,77 +787,164 @@ __global__ void __launch_bounds__(kJoinThreads) k_join(const Dev d) {
             : "+r"(w)
             : "d"(o.x), "d"(R.xa), "d"(R.xb), "d"(o.y), "d"(R.ya), "d"(R.yb), "r"(1u << k));
       }
-      if (live) {
-        tile[sl][bl] = w;
-        atomicAdd(&cnt[sl], (uint32_t)__popc(w));
-      }
+      stile[wp][lane][bl] = w;
+      cnt += __popc(w);
+      __syncwarp();
     }
-    __syncthreads();
     uint32_t* out = d.bitmap + d.leaf_woff[r] + (int64_t)s0 * nb + b0;
     if (nbt == nb) {
       const int tot = ns * nb;
-      for (int e = t; e < tot; e += kJoinThreads) {
+      for (int e = lane; e < tot; e += 32) {
         const int s = e / nb;
-        out[e] = tile[s][e - s * nb];
+        out[e] = stile[wp][s][e - s * nb];
       }
     } else {
       const int tot = ns * nbt;
-      for (int e = t; e < tot; e += kJoinThreads) {
+      for (int e = lane; e < tot; e += 32) {
         const int s = e / nbt, c = e - s * nbt;
-        out[(int64_t)s * nb + c] = tile[s][c];
+        out[(int64_t)s * nb + c] = stile[wp][s][c];
       }
     }
-    if (t < ns) {
-      if (n_ot == 1) d.sq_count[slots[t]] = (int32_t)cnt[t];
-      else atomicAdd(&d.sq_count[slots[t]], (int32_t)cnt[t]);
+    if (live) {
+      const int64_t e = (int64_t)d.leaf_sbase[r] + s0 + lane;
+      if (n_ot == 1) {
+        d.sq_count[slot] = (int32_t)cnt;
+        d.ecount[e] = (int32_t)cnt;
+      } else {
+        atomicAdd(&d.sq_count[slot], (int32_t)cnt);
+        atomicAdd(&d.ecount[e], (int32_t)cnt);
+      }
     }
-    __syncthreads();
+    __syncwarp();
+  }
+}
+
+// covering subqueries' counts = their leaf's whole block
+__global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const int lane = lane_id();
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < h->L; r += nwarp) {
+    const int nc = d.leaf_ncov[r];
+    if (nc == 0) continue;
+    const int32_t base = d.leaf_sbase[r] + d.leaf_nisq[r];
+    const int32_t nobj = d.leaf_nobj[r];
+    for (int c = lane; c < nc; c += 32) {
+      d.sq_count[d.ssorted[base + c]] = nobj;
+      d.ecount[base + c] = nobj;
+    }
   }
 }
 
 // ===========================================================================
 // K4: decode, covering expansion, canonical per-query lists
 // ===========================================================================
-struct SlotCntIn {
-  const uint8_t* cov;
-  const int32_t* leaf;
-  const int32_t* nobj;
-  const int32_t* count;
-  __device__ int64_t operator()(int64_t s) const {
-    return (cov[s] & 1) ? (int64_t)nobj[leaf[s]] : (int64_t)count[s];
+// Result counts: an intersecting subquery contributes its popcount, a
+// covering one its leaf's whole block (decode.py:83-99).
+// (sq_count holds both after the join: covering entries are filled by k_cov_counts)
+__device__ __forceinline__ int64_t slot_count(const Dev& d, int32_t slot) { return (int64_t)d.sq_count[slot]; }
+
+// decode order: entries e of `ssorted` (leaf by leaf, intersecting then
+// covering) — every leaf's decoded lists form one contiguous chunk of `stage`
+struct RowCntIn {
+  Dev d;
+  __device__ int64_t operator()(int64_t e) const { return (int64_t)d.ecount[e]; }
+};
+struct RowOut {
+  Dev d;
+  __device__ void operator()(int64_t e, int64_t ex, int64_t) const {
+    d.slot_out[e] = ex;            // row e's list starts at stage[ex]
+    d.run_off[d.ssorted[e]] = ex;  // ... which is subquery slot's run
+  }
+};
+// output order: queries in input order, lists concatenated (ResultSet CSR)
+struct QueryCntIn {
+  Dev d;
+  __device__ int64_t operator()(int64_t q) const {
+    const int k = d.nsub[q];
+    const int32_t s0 = d.qsbase[q];
+    int64_t c = 0;
+    for (int j = 0; j < k; ++j) c += slot_count(d, s0 + j);
+    return c;
   }
 };
 
-__global__ void __launch_bounds__(256) k_query_offsets(const Dev d) {
+__global__ void k_close_offsets(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  const int64_t m = h->m, S = h->S;
-  TJ_GRID_STRIDE(q, m + 1) {
-    const int64_t sb = q < m ? d.qsbase[q] : S;
-    d.out_off[q] = sb < S ? d.slot_out[sb] : h->R;
-  }
+  d.out_off[h->m] = h->R;
+  if (h->R != h->R_check) h->count_mismatch = 1;  // CountMismatch (bitmap.py:131-132)
 }
 
 constexpr int kDecodeThreads = 256;
 constexpr int kDecodeIds = 1024;     // leaf id blocks up to this size are staged in shared memory
-constexpr int kDecodeWords = 6144;   // leaf bitmaps up to this many words are staged too
+constexpr int kDecodeWords = 4096;   // leaf bitmaps up to this many words are staged too
+
+constexpr int kDecodeBatch = 512;  // per-warp staging of 32 rows' decoded rows
 
 // Alg. 4 per leaf (decode.py:40-99, bitmap.py:122-133, engine.py:306-326):
 // one CTA per leaf stages the leaf's object ids and bitmap rows in shared
-// memory and fetches the destination of 256 rows at a time in parallel; then
-// a warp per intersecting subquery row takes the row's words (lanes = words),
-// popcounts, warp-scans and writes the ids of set bits (block order) at the
-// row's prefix offset; a warp per covering subquery copies the whole block.
-// Lists of single-run queries go straight to the output, the rest to the
-// merge stage.
+// memory.  Intersecting rows are decoded lane-per-row, 32 rows per warp step:
+// a lane walks its row's words and, for every set bit (ascending = block
+// order), puts the object's id at the row's next position.  The 32 rows'
+// lists are adjacent in `stage` (decode order), so they are assembled in a
+// per-warp shared-memory buffer and stored with full-width coalesced writes.
+// Covering subqueries copy the whole block.
+template <bool kStaged>
+__device__ __forceinline__ void decode_rows(const Dev& d, const int32_t* ids, const uint32_t* rows, int ni,
+                                            int nb, int32_t sb, int32_t* wbuf) {
+  const int lane = lane_id(), wp = threadIdx.x >> 5;
+  constexpr int nw = kDecodeThreads / 32;
+  const int64_t S = d.h->S, R = d.h->R;
+  for (int r0 = wp * 32; r0 < ni; r0 += nw * 32) {
+    const int row = r0 + lane;
+    const bool live = row < ni;
+    const int64_t off = live ? d.slot_out[sb + row] : 0;
+    const int nrow = min(32, ni - r0);
+    const int64_t e_end = (int64_t)sb + r0 + nrow;
+    const int64_t base = __shfl_sync(0xffffffffu, off, 0);
+    const int64_t end = e_end < S ? d.slot_out[e_end] : R;
+    const int64_t total = end - base;
+    const bool buffered = total <= kDecodeBatch;
+    if (live) {
+      const uint32_t* words = rows + (int64_t)row * nb;
+      if (buffered) {
+        int32_t* dst = wbuf + (off - base);  // shared memory
+        for (int b = 0; b < nb; ++b) {
+          uint32_t w = words[b];
+          while (w) {
+            const int bit = __ffs(w) - 1;
+            w &= w - 1;
+            *dst++ = ids[b * 32 + bit];
+          }
+        }
+      } else {
+        int32_t* dst = d.stage + off;  // global
+        for (int b = 0; b < nb; ++b) {
+          uint32_t w = words[b];
+          while (w) {
+            const int bit = __ffs(w) - 1;
+            w &= w - 1;
+            *dst++ = ids[b * 32 + bit];
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (buffered)
+      for (int k = lane; k < (int)total; k += 32) d.stage[base + k] = wbuf[k];
+    __syncwarp();
+  }
+}
+
 __global__ void __launch_bounds__(kDecodeThreads) k_decode_leaf(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  __shared__ int64_t sids[kDecodeIds];
+  __shared__ int32_t sids[kDecodeIds];
   __shared__ uint32_t swords[kDecodeWords];
-  __shared__ int64_t* sdst[kDecodeThreads];
+  __shared__ int32_t sbatch[kDecodeThreads / 32][kDecodeBatch];
   const int64_t L = h->L;
-  const int mono = !h->not_monotone;
   const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
   constexpr int nw = kDecodeThreads / 32;
   unsigned long long covres = 0;
@@ -857,170 +954,263 @@ __global__ void __launch_bounds__(kDecodeThreads) k_decode_leaf(const Dev d) {
     if (nobj == 0 || (ni == 0 && nc == 0)) continue;
     const int32_t ob = d.leaf_obase[r], sb = d.leaf_sbase[r];
     const int nb = (nobj + 31) >> 5;
-    const bool ids_staged = nobj <= kDecodeIds;
-    const int64_t* gids = d.sid + ob;
-    if (ids_staged)
-      for (int k = t; k < nobj; k += kDecodeThreads) sids[k] = gids[k];
-    const int64_t* ids = ids_staged ? sids : gids;
+    const int32_t* gids = d.sidx + ob;  // input rows of the leaf's objects (block order)
     const uint32_t* grows = d.bitmap + d.leaf_woff[r];
     const int64_t nwords = (int64_t)ni * nb;
-    const bool words_staged = nwords <= kDecodeWords;
-    if (words_staged)
+    const bool staged = nobj <= kDecodeIds && nwords <= kDecodeWords;
+    if (staged) {
+      for (int k = t; k < nobj; k += kDecodeThreads) sids[k] = gids[k];
       for (int k = t; k < nwords; k += kDecodeThreads) swords[k] = grows[k];
-    const uint32_t* rows = words_staged ? swords : grows;
-    const int nall = ni + nc;
-    for (int c0 = 0; c0 < nall; c0 += kDecodeThreads) {
-      const int e = c0 + t;
-      if (e < nall) {  // destinations of 256 rows at once: latency in parallel
-        const int32_t slot = d.ssorted[sb + e];
-        const bool direct = mono && (d.sq_cov[slot] & kFlagSingle);
-        sdst[t] = (direct ? d.out_ids : d.stage) + d.slot_out[slot];
-      }
       __syncthreads();
-      const int cend = min(nall - c0, kDecodeThreads);
-      for (int k = wp; k < cend; k += nw) {
-        const int row = c0 + k;
-        int64_t* dst = sdst[k];
-        if (row < ni) {
-          const uint32_t* words = rows + (int64_t)row * nb;
-          int64_t base = 0;
-          for (int w0 = 0; w0 < nb; w0 += 32) {
-            const int b = w0 + lane;
-            uint32_t w = b < nb ? words[b] : 0u;
-            const int pc = __popc(w);
-            const int inc = warp_incl_scan(pc);
-            int64_t pos = base + inc - pc;
-            while (w) {
-              const int bit = __ffs(w) - 1;
-              w &= w - 1;
-              dst[pos++] = ids[b * 32 + bit];
-            }
-            base += __shfl_sync(0xffffffffu, inc, 31);
-          }
-        } else {
-          for (int k2 = lane; k2 < nobj; k2 += 32) dst[k2] = ids[k2];
-          if (lane == 0) covres += (unsigned long long)nobj;
-        }
-      }
-      __syncthreads();
+      decode_rows<true>(d, sids, swords, ni, nb, sb, sbatch[wp]);
+    } else {
+      decode_rows<false>(d, gids, grows, ni, nb, sb, sbatch[wp]);
     }
+    for (int c = wp; c < nc; c += nw) {
+      int32_t* dst = d.stage + d.slot_out[sb + ni + c];
+      for (int k = lane; k < nobj; k += 32) dst[k] = gids[k];
+      if (lane == 0) covres += (unsigned long long)nobj;
+    }
+    __syncthreads();
   }
   if (lane == 0 && covres) atomicAdd(&h->cov_results, covres);
 }
 
-constexpr int kMergeSmem = 512;  // per-warp staging of one query's runs
 
 // Per-query canonical lists (decode.py:102-123: concatenate, sort, reject
-// duplicates).  Monotone ids (ids increase with input row — every generated
-// workload): each subquery's run is already sorted, so a query with k > 1
-// runs is merged by rank — an element's output index is its index in its own
-// run plus the number of smaller elements in every other run.  Otherwise the
-// list is sorted (warp bitonic in shared memory) and checked for duplicates.
-// A warp takes 32 queries, fetches their metadata in parallel and handles
-// them one by one; lists longer than kMergeSmem (or > 32 runs) are queued for
-// the CTA-wide k_merge_big.
-__device__ __forceinline__ void warp_bitonic(int64_t* a, int n) {
-  int P = 32;
-  while (P < n) P <<= 1;
+// duplicates), assembled from the decoded runs (input rows, int32) into the
+// output CSR (object ids, int64), written in query order.  Monotone ids (ids
+// increase with input row — every generated workload): each run is sorted by
+// row, so sorting by row sorts by id; one run is a copy, two runs a merge-path
+// merge in registers, more runs a register bitonic sort; ids are looked up
+// (ids[row]) at the final store.  Otherwise rows are turned into ids first and
+// sorted by id, with a duplicate check.  Lists longer than 64 (or > 32 runs)
+// are concatenated into the output and queued for the CTA-wide k_merge_big.
+template <typename T>
+__device__ __forceinline__ T bitonic_step(T v, int i, int j, int k) {
+  const T o = __shfl_xor_sync(0xffffffffu, v, j);
+  const bool up = (i & k) == 0, low = (i & j) == 0;
+  return (low == up) ? (o < v ? o : v) : (o > v ? o : v);
+}
+// ascending bitonic sort of 32 (r = 1) or 64 (r = 2, index = reg*32 + lane) keys in registers
+template <typename T, int NR>
+__device__ __forceinline__ void warp_sort(T (&v)[2]) {
   const int lane = lane_id();
-  for (int i = n + lane; i < P; i += 32) a[i] = (int64_t)0x7fffffffffffffffll;
-  __syncwarp();
-  for (int k = 2; k <= P; k <<= 1) {
+#pragma unroll
+  for (int k = 2; k <= 32 * NR; k <<= 1)
+#pragma unroll
     for (int j = k >> 1; j > 0; j >>= 1) {
-      for (int i = lane; i < P; i += 32) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const bool up = (i & k) == 0;
-          const int64_t x = a[i], y = a[ixj];
-          if ((x > y) == up) {
-            a[i] = y;
-            a[ixj] = x;
-          }
-        }
+      if (j == 32) {  // partner is the other register of the same lane (k == 64: ascending)
+        const T lo = v[0] < v[1] ? v[0] : v[1], hi = v[0] < v[1] ? v[1] : v[0];
+        v[0] = lo;
+        v[1] = hi;
+      } else {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) v[r] = bitonic_step(v[r], r * 32 + lane, j, k);
       }
-      __syncwarp();
     }
+}
+
+// value at concatenated index t (reg t/32, lane t%32)
+template <int NR>
+__device__ __forceinline__ int32_t vget(const int32_t (&v)[2], int t) {
+  const int32_t a = __shfl_sync(0xffffffffu, v[0], t & 31);
+  if (NR == 1) return a;
+  const int32_t b = __shfl_sync(0xffffffffu, v[1], t & 31);
+  return t < 32 ? a : b;
+}
+
+// merge path of two sorted runs A = [0, na), B = [na, cnt) held in registers:
+// output position p takes min(A[i], B[p-i]) at the split i found by binary search
+template <int NR>
+__device__ __forceinline__ void warp_merge2(const int32_t (&v)[2], int na, int cnt, int32_t (&o)[2]) {
+  const int lane = lane_id();
+  const int nb = cnt - na;
+#pragma unroll
+  for (int r = 0; r < NR; ++r) {
+    const int p = r * 32 + lane;
+    int lo = p - nb > 0 ? p - nb : 0, hi = p < na ? p : na;
+    if (p >= cnt) lo = hi = 0;
+    while (__any_sync(0xffffffffu, lo < hi)) {
+      const int mid = (lo + hi) >> 1;
+      const int ia = mid, ib = na + p - mid - 1;
+      const int32_t va = vget<NR>(v, ia < 63 ? ia : 63);
+      const int32_t vb = vget<NR>(v, ib > 0 ? (ib < 63 ? ib : 63) : 0);
+      if (lo < hi) {
+        if (va < vb) lo = mid + 1; else hi = mid;
+      }
+    }
+    const int i = lo, j = p - lo;
+    const int32_t ai = vget<NR>(v, i < na ? i : 0);
+    const int32_t bj = vget<NR>(v, j < nb ? na + j : 0);
+    o[r] = (j >= nb || (i < na && ai < bj)) ? ai : bj;
   }
 }
 
-__global__ void __launch_bounds__(256) k_merge_runs(const Dev d) {
+__global__ void __launch_bounds__(256) k_assemble(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const bool mono = !h->not_monotone;
-  __shared__ int64_t sm[8][kMergeSmem];
   const int64_t m = h->m;
-  const int lane = lane_id(), wp = threadIdx.x >> 5;
+  const int lane = lane_id();
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  int64_t* buf = sm[wp];
+  const int64_t* __restrict__ ids = d.ids;
+  const int32_t* __restrict__ stage = d.stage;
+  const bool ident = !h->not_identity;
+  auto idof = [&](int32_t row) -> int64_t { return ident ? (int64_t)row : ids[row]; };
   for (int64_t q0 = gw * 32; q0 < m; q0 += nwarp * 32) {
     const int64_t ql = q0 + lane;
-    const int kl = ql < m ? d.nsub[ql] : 0;
-    unsigned todo = __ballot_sync(0xffffffffu, mono ? kl > 1 : kl > 0);
-    if (!todo) continue;
+    int kl = 0;
     int32_t s0l = 0;
-    int64_t qol = 0, qel = 0;
-    if (mono ? kl > 1 : kl > 0) {
+    int64_t qol = 0, cntl = 0;
+    if (ql < m) {
+      kl = d.nsub[ql];
       s0l = d.qsbase[ql];
       qol = d.out_off[ql];
-      qel = d.out_off[ql + 1];
+      cntl = d.out_off[ql + 1] - qol;
     }
+    // single-run lists (sorted already when ids are monotone; length <= 1
+    // otherwise): flattened copy of the warp's output range — independent
+    // loads, coalesced stores
+    const bool single = kl == 1 && (mono || cntl <= 1);
+    const int64_t srcl = (single && cntl > 0) ? d.run_off[s0l] : -1;
+    const bool done = kl == 0 || cntl == 0 || single;
+    {
+      const int64_t lo = __shfl_sync(0xffffffffu, qol, 0);
+      const int64_t hi = __shfl_sync(0xffffffffu, qol + cntl, 31);
+      const int64_t hi2 = q0 + 32 <= m ? hi : d.out_off[m];
+      const int nvalid = (int)min((int64_t)32, m - q0);
+      const uint32_t rel = lane < nvalid ? (uint32_t)(qol - lo) : 0xffffffffu;
+      for (int64_t p0 = lo; p0 < hi2; p0 += 32) {
+        const uint32_t pr = (uint32_t)(p0 - lo) + lane;
+        int j = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint32_t v = __shfl_sync(0xffffffffu, rel, j + step);
+          if (v <= pr) j += step;
+        }
+        const uint32_t relj = __shfl_sync(0xffffffffu, rel, j);
+        const int64_t srcj = __shfl_sync(0xffffffffu, srcl, j);
+        if (p0 + lane < hi2 && srcj >= 0) d.out_ids[p0 + lane] = idof(stage[srcj + (pr - relj)]);
+      }
+    }
+    // short multi-run lists (<= 64 entries, <= 32 runs): one query at a
+    // time, the next query's run metadata in flight meanwhile
+    const bool smallq = !done && cntl <= 64 && kl <= 32;
+    unsigned pend = __ballot_sync(0xffffffffu, smallq);
+    {
+      auto meta = [&](int src, int64_t& c, int64_t& o) {
+        const int kk = __shfl_sync(0xffffffffu, kl, src);
+        const int32_t ss = __shfl_sync(0xffffffffu, s0l, src);
+        c = 0;
+        o = 0;
+        if (lane < kk) {
+          c = slot_count(d, ss + lane);
+          o = d.run_off[ss + lane];
+        }
+      };
+      int cur = pend ? __ffs(pend) - 1 : -1;
+      pend &= pend - 1;
+      int64_t c_cur = 0, o_cur = 0;
+      if (cur >= 0) meta(cur, c_cur, o_cur);
+      while (cur >= 0) {
+        const int nxt = pend ? __ffs(pend) - 1 : -1;
+        pend &= pend - 1;
+        int64_t c_nxt = 0, o_nxt = 0;
+        if (nxt >= 0) meta(nxt, c_nxt, o_nxt);
+        const int k = __shfl_sync(0xffffffffu, kl, cur);
+        const int64_t qo = __shfl_sync(0xffffffffu, qol, cur);
+        const int cnt = (int)__shfl_sync(0xffffffffu, cntl, cur);
+        const int cinc = warp_incl_scan((int)c_cur);
+        const int cexc = cinc - (int)c_cur;
+        int32_t v[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          const int x = r * 32 + lane;
+          int jj = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int st = __shfl_sync(0xffffffffu, cexc, jj + step);
+            if (jj + step < k && st <= x) jj += step;
+          }
+          const int stj = __shfl_sync(0xffffffffu, cexc, jj);
+          const int64_t ofj = __shfl_sync(0xffffffffu, o_cur, jj);
+          v[r] = x < cnt ? stage[ofj + (x - stj)] : 0x7fffffff;
+        }
+        if (mono) {
+          int32_t o[2];
+          if (k == 2) {
+            const int na = __shfl_sync(0xffffffffu, (int)c_cur, 0);
+            if (cnt <= 32) warp_merge2<1>(v, na, cnt, o); else warp_merge2<2>(v, na, cnt, o);
+          } else {
+            if (cnt <= 32) warp_sort<int32_t, 1>(v); else warp_sort<int32_t, 2>(v);
+            o[0] = v[0];
+            o[1] = v[1];
+          }
+#pragma unroll
+          for (int r = 0; r < 2; ++r)
+            if (r * 32 + lane < cnt) d.out_ids[qo + r * 32 + lane] = idof(o[r]);
+        } else {
+          int64_t w[2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) w[r] = r * 32 + lane < cnt ? idof(v[r]) : (int64_t)0x7fffffffffffffffll;
+          if (cnt <= 32) warp_sort<int64_t, 1>(w); else warp_sort<int64_t, 2>(w);
+          int dup = 0;
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int x = r * 32 + lane;
+            if (x < cnt) d.out_ids[qo + x] = w[r];
+            // neighbour of x is x+1: next lane, or register 1 lane 0
+            const int64_t nb0 = __shfl_down_sync(0xffffffffu, w[r], 1);
+            const int64_t wrap = __shfl_sync(0xffffffffu, w[1], 0);
+            const int64_t nbv = lane < 31 ? nb0 : (r == 0 ? wrap : (int64_t)0x7fffffffffffffffll);
+            dup |= (x + 1 < cnt) && nbv == w[r];
+          }
+          if (__any_sync(0xffffffffu, dup) && lane == 0) h->dup = 1;
+        }
+        cur = nxt;
+        c_cur = c_nxt;
+        o_cur = o_nxt;
+      }
+    }
+    // long lists / many runs: concatenate the runs (as ids) into the output
+    // and queue the query for the CTA-wide sort
+    unsigned todo = __ballot_sync(0xffffffffu, !done && !smallq);
     while (todo) {
       const int src_lane = __ffs(todo) - 1;
       todo &= todo - 1;
       const int k = __shfl_sync(0xffffffffu, kl, src_lane);
       const int32_t s0 = __shfl_sync(0xffffffffu, s0l, src_lane);
       const int64_t qo = __shfl_sync(0xffffffffu, qol, src_lane);
-      const int64_t cnt = __shfl_sync(0xffffffffu, qel, src_lane) - qo;
-      if (cnt == 0) continue;
-      if (k > 32 || cnt > kMergeSmem) {  // long lists / many runs: CTA-wide pass
-        if (lane == 0) {
-          const int idx = atomicAdd(&h->n_big, 1);
-          d.big_list[idx] = (int32_t)(q0 + src_lane);
+      int64_t pre = 0;
+      for (int j0 = 0; j0 < k; j0 += 32) {
+        const int j = j0 + lane;
+        int64_t cj = 0, oj = 0;
+        if (j < k) {
+          cj = slot_count(d, s0 + j);
+          oj = d.run_off[s0 + j];
         }
-        continue;
-      }
-      if (!mono) {  // unsorted runs: sort the list, then check duplicates
-        for (int64_t p = lane; p < cnt; p += 32) buf[p] = d.stage[qo + p];
-        __syncwarp();
-        warp_bitonic(buf, (int)cnt);
-        int dup = 0;
-        for (int p = lane; p < (int)cnt; p += 32) {
-          d.out_ids[qo + p] = buf[p];
-          dup |= (p + 1 < (int)cnt) && buf[p] == buf[p + 1];
-        }
-        if (__any_sync(0xffffffffu, dup) && lane == 0) h->dup = 1;
-        __syncwarp();
-        continue;
-      }
-      const int rs = lane < k ? (int)(d.slot_out[s0 + lane] - qo) : (int)cnt;  // run starts in lanes
-      for (int64_t p = lane; p < cnt; p += 32) buf[p] = d.stage[qo + p];
-      __syncwarp();
-      for (int p0 = 0; p0 < (int)cnt; p0 += 32) {  // uniform trip count: shuffles below
-        const int p = p0 + lane;
-        const bool act = p < (int)cnt;
-        const int64_t key = act ? buf[p] : 0;
-        int rank = 0;
-        for (int j = 0; j < k; ++j) {
-          const int a = __shfl_sync(0xffffffffu, rs, j);
-          const int b = __shfl_sync(0xffffffffu, rs, j + 1 < 32 ? j + 1 : 31);
-          const int bb = (j + 1 < k) ? b : (int)cnt;
-          if (!act) continue;
-          if (p >= a && p < bb) {
-            rank += p - a;
-          } else {
-            int lo = a, hi = bb;
-            while (lo < hi) {
-              const int mid = (lo + hi) >> 1;
-              if (buf[mid] < key) lo = mid + 1; else hi = mid;
-            }
-            rank += lo - a;
+        const int64_t inc = warp_incl_scan(cj);
+        const int64_t seg = __shfl_sync(0xffffffffu, inc, 31);
+        for (int64_t x0 = 0; x0 < seg; x0 += 32) {  // flattened copy of these <= 32 runs
+          const int64_t x = x0 + lane;
+          int jj = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int64_t v = __shfl_sync(0xffffffffu, inc - cj, jj + step);  // exclusive starts
+            if (v <= x && j0 + jj + step < k) jj += step;
           }
+          const int64_t st_j = __shfl_sync(0xffffffffu, inc - cj, jj);
+          const int64_t of_j = __shfl_sync(0xffffffffu, oj, jj);
+          if (x < seg) d.out_ids[qo + pre + x] = idof(stage[of_j + (x - st_j)]);
         }
-        if (act)
-        d.out_ids[qo + rank] = key;
+        pre += seg;
       }
-      __syncwarp();
+      if (lane == 0) {
+        const int idx = atomicAdd(&h->n_big, 1);
+        d.big_list[idx] = (int32_t)(q0 + src_lane);
+      }
     }
   }
 }
@@ -1105,10 +1295,8 @@ __global__ void __launch_bounds__(256) k_merge_big(const Dev d) {
     const int32_t q = d.big_list[i];
     const int64_t qo = d.out_off[q], qe = d.out_off[q + 1];
     const int64_t len = qe - qo;
-    int64_t* a = d.out_ids + qo;
-    for (int64_t k = threadIdx.x; k < len; k += blockDim.x) a[k] = d.stage[qo + k];
-    __syncthreads();
-    cta_sort<int64_t>(a, len, d.stage + qo, sm, (int64_t)0x7fffffffffffffffll);
+    int64_t* a = d.out_ids + qo;  // runs already concatenated here by k_assemble
+    cta_sort<int64_t>(a, len, d.scratch + qo, sm, (int64_t)0x7fffffffffffffffll);
     int dup = 0;
     for (int64_t k = threadIdx.x; k + 1 < len; k += blockDim.x) dup |= (a[k] == a[k + 1]);
     if (__syncthreads_or(dup) && threadIdx.x == 0) h->dup = 1;

@@ -17,17 +17,33 @@ constexpr int kScanThreads = 256;
 // `In`  : int64_t operator()(int64_t i) const        — value of item i
 // `Out` : void operator()(int64_t i, int64_t excl, int64_t v) const
 // ---------------------------------------------------------------------------
+constexpr int kScanItems = 8;  // items per thread per step: 8 independent loads in flight (ILP)
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ void scan_chunk(int64_t n, int64_t G, int64_t blk, int64_t* b, int64_t* e) {
+  const int64_t chunk = ((n + G - 1) / G + kScanTile - 1) / kScanTile * kScanTile;
+  *b = blk * chunk;
+  *e = (*b + chunk < n) ? *b + chunk : n;
+}
+
 template <typename In>
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_reduce(In in, const int64_t* n_ptr, const DevHdr* h, int64_t* partial) {
   if (h->abort) return;
   __shared__ int64_t sh[33];
-  const int64_t n = *n_ptr, G = gridDim.x;
-  const int64_t chunk = (n + G - 1) / G;
-  const int64_t b = blockIdx.x * chunk;
-  const int64_t e = (b + chunk < n) ? b + chunk : n;
+  int64_t b, e;
+  scan_chunk(*n_ptr, gridDim.x, blockIdx.x, &b, &e);
   int64_t s = 0;
-  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) s += in(i);
+  for (int64_t base = b; base < e; base += kScanTile) {
+    int64_t v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + threadIdx.x;  // striped: coalesced
+      v[k] = i < e ? in(i) : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) s += v[k];
+  }
   s = warp_sum(s);
   if (lane_id() == 0) sh[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -50,23 +66,50 @@ k_scan_partials(int64_t* partial, int G, int64_t* total_out, DevHdr* h) {
   if (threadIdx.x == 0 && total_out) *total_out = tot;
 }
 
+// Items are loaded striped (coalesced; 8 independent loads per thread),
+// transposed through shared memory to a blocked arrangement for the scan, and
+// the exclusive prefixes transposed back so `Out` writes are coalesced too.
 template <typename In, typename Out>
 __global__ void __launch_bounds__(kScanThreads)
 k_scan_down(In in, Out out, const int64_t* n_ptr, const DevHdr* h, const int64_t* partial) {
   if (h->abort) return;
   __shared__ int64_t sh[33];
-  const int64_t n = *n_ptr, G = gridDim.x;
-  const int64_t chunk = (n + G - 1) / G;
-  const int64_t b = blockIdx.x * chunk;
-  const int64_t e = (b + chunk < n) ? b + chunk : n;
+  __shared__ int64_t tile[kScanTile];
+  int64_t b, e;
+  scan_chunk(*n_ptr, gridDim.x, blockIdx.x, &b, &e);
   int64_t carry = partial[blockIdx.x];
-  for (int64_t base = b; base < e; base += blockDim.x) {  // uniform trip count per block
-    const int64_t i = base + threadIdx.x;
-    const int64_t v = (i < e) ? in(i) : 0;
+  const int t = threadIdx.x;
+  for (int64_t base = b; base < e; base += kScanTile) {  // uniform trip count per block
+    int64_t v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + t;
+      v[k] = i < e ? in(i) : 0;
+      tile[k * kScanThreads + t] = v[k];
+    }
+    __syncthreads();
+    int64_t blk[kScanItems];
+    int64_t loc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      blk[k] = tile[t * kScanItems + k];
+      loc += blk[k];
+    }
     int64_t tot;
-    const int64_t ex = block_excl_scan(v, sh, &tot);
-    if (i < e) out(i, carry + ex, v);
+    int64_t ex = carry + block_excl_scan(loc, sh, &tot);  // (contains __syncthreads)
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      tile[t * kScanItems + k] = ex;
+      ex += blk[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + t;
+      if (i < e) out(i, tile[k * kScanThreads + t], v[k]);
+    }
     carry += tot;
+    __syncthreads();
   }
 }
 
@@ -139,7 +182,7 @@ k_radix_upsweep(const uint32_t* keys, const int64_t* n_ptr, const DevHdr* h, int
   }
 }
 
-__global__ void __launch_bounds__(kRadixThreads)
+__global__ void __launch_bounds__(kRadixThreads, 4)
 k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out,
                   int32_t* vals_out, const int64_t* n_ptr, const DevHdr* h, int shift,
                   const int64_t* offs /* [digits][G] exclusive */) {
@@ -159,18 +202,28 @@ k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* key
   for (int j = 0; j < kRadixDPT; ++j)
     base[t + j * kRadixThreads] = (uint32_t)offs[(int64_t)(t + j * kRadixThreads) * G + blockIdx.x];
   const uint32_t lt = (1u << lane) - 1u;
-  for (int64_t tb = b; tb < e; tb += kRadixTile) {
-    for (int k = t; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&wcnt[0][0])[k] = 0;
-    __syncthreads();
-    uint32_t key[kRadixIPT], dig[kRadixIPT], rk[kRadixIPT];
-    int32_t val[kRadixIPT];
-    // warp w owns items [tb + w*32*IPT, ...), processed in rounds of 32 in order
+  // keys/values of the current tile are loaded one tile ahead (all IPT loads in flight)
+  uint32_t key[kRadixIPT];
+  int32_t val[kRadixIPT];
+  auto load_tile = [&](int64_t tb) {
 #pragma unroll
     for (int r = 0; r < kRadixIPT; ++r) {
       const int64_t i = tb + (int64_t)w * 32 * kRadixIPT + r * 32 + lane;
       const bool ok = i < e;
       key[r] = ok ? keys_in[i] : 0u;
       val[r] = ok ? vals_in[i] : 0;
+    }
+  };
+  if (b < e) load_tile(b);
+  for (int64_t tb = b; tb < e; tb += kRadixTile) {
+    for (int k = t; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&wcnt[0][0])[k] = 0;
+    __syncthreads();
+    uint32_t dig[kRadixIPT], rk[kRadixIPT];
+    // warp w owns items [tb + w*32*IPT, ...), processed in rounds of 32 in order
+#pragma unroll
+    for (int r = 0; r < kRadixIPT; ++r) {
+      const int64_t i = tb + (int64_t)w * 32 * kRadixIPT + r * 32 + lane;
+      const bool ok = i < e;
       // invalid lanes get digit kRadixDigits (the extra bit below)
       dig[r] = ok ? ((key[r] >> shift) & (kRadixDigits - 1)) : (uint32_t)kRadixDigits;
       uint32_t peers = 0xffffffffu;
@@ -219,6 +272,7 @@ k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* key
         sval[pos] = val[r];
       }
     }
+    if (tb + kRadixTile < e) load_tile(tb + kRadixTile);  // next tile in flight during the scatter
     __syncthreads();
     const int tile_n = (int)((e - tb) < kRadixTile ? (e - tb) : kRadixTile);
     for (int p = t; p < tile_n; p += kRadixThreads) {
