@@ -154,6 +154,15 @@ int tj_get_bitmaps(tj_ctx* ctx, int64_t* n_tasks, int64_t* n_words, int64_t* tas
  * greedy least-loaded assignment of task weights n_isq*n_obj. */
 int tj_get_imbalance(tj_ctx* ctx, int32_t sim_processors, int32_t heaviest_first, double* imbalance);
 
+/* Multi-GPU leaf-range sharding (no reference counterpart —
+ * the reference is single-process).  With nranks > 1 every
+ * tick builds the full index and subquery directory, then joins / decodes
+ * only the leaves of this rank's contiguous Morton range (balanced by work
+ * weight); the output CSR holds each query's results restricted to those
+ * leaves.  Partial lists of the ranks are disjoint and individually sorted;
+ * their per-query merge is the full result.  nranks == 1 (default): off. */
+int tj_set_shard(tj_ctx* ctx, int32_t rank, int32_t nranks);
+
 /* The context's CUDA stream (cudaStream_t), for callers that time or order
  * work against the tick with their own events. */
 int tj_get_stream(tj_ctx* ctx, void** stream);

@@ -74,7 +74,7 @@ class TjIndexInfo(ctypes.Structure):
 EXPORTED = (
     "tj_abi_version", "tj_device_count", "tj_create", "tj_destroy", "tj_last_error", "tj_tick",
     "tj_get_index", "tj_get_object_cells", "tj_get_subqueries", "tj_get_directory", "tj_get_bitmaps",
-    "tj_get_imbalance", "tj_get_stream", "tj_host_alloc", "tj_host_free",
+    "tj_get_imbalance", "tj_set_shard", "tj_get_stream", "tj_host_alloc", "tj_host_free",
 )
 
 _lib: Optional[ctypes.CDLL] = None
@@ -104,6 +104,7 @@ def load_library() -> ctypes.CDLL:
     lib.tj_get_bitmaps.argtypes = [c_void_p, i64p, i64p] + [c_void_p] * 6 + [c_int64] * 3
     lib.tj_get_imbalance.argtypes = [c_void_p, c_int32, c_int32, POINTER(c_double)]
     lib.tj_get_stream.argtypes = [c_void_p, POINTER(c_void_p)]
+    lib.tj_set_shard.argtypes = [c_void_p, c_int32, c_int32]
     lib.tj_host_alloc.argtypes = [c_int64, POINTER(c_void_p)]
     lib.tj_host_free.argtypes = [c_void_p]
     _lib = lib
@@ -182,6 +183,10 @@ class NativeContext:
         st = TjStats()
         self._check(self.lib.tj_tick(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
         return tout, st
+
+    def set_shard(self, rank: int, nranks: int) -> None:
+        """Leaf-range sharding: this context joins only rank's Morton range of leaves."""
+        self._check(self.lib.tj_set_shard(self.h, rank, nranks))
 
     def stream(self) -> int:
         s = c_void_p()

@@ -45,9 +45,9 @@ struct tj_ctx {
   // queries
   DBuf crect, qwin, nsub, qsbase, biglist;
   // subqueries
-  DBuf sqleaf, sqq, sqcov, sqcount, ecount, slotout, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
+  DBuf sqleaf, sqq, sqcov, sqcount, ecount, srect, slotout, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
   // join / outputs
-  DBuf bitmap, stage, outids, outoff, runoff, scratch;
+  DBuf bitmap, stage, outids, outoff, runinfo, scratch;
   // scan / radix scratch
   DBuf partial, rhist, roffs;
   // pinned host outputs
@@ -64,6 +64,8 @@ struct tj_ctx {
   DevHdr last{};
   Dev dv{};
   int obj_passes = 0, sq_passes = 0;
+  int shard_rank = 0, shard_n = 1;
+  DBuf lactive, lwpre;
 };
 
 namespace {
@@ -168,6 +170,8 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(lwoff, c->cap_L * 8);
   ENS(lubase, c->cap_L * 8);
   ENS(runs0, c->cap_L * 2 * 4);
+  ENS(lactive, c->cap_L);
+  ENS(lwpre, c->cap_L * 8);
   ENS(runs1, c->cap_L * 2 * 4);
   ENS(crect, m * sizeof(Rect4));
   ENS(qwin, m * sizeof(int4));
@@ -196,6 +200,7 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sqcov, c->cap_S);
   ENS(sqcount, c->cap_S * 4);
   ENS(ecount, c->cap_S * 4);
+  ENS(srect, c->cap_S * sizeof(Rect4));
   ENS(slotout, c->cap_S * 8);
   ENS(skey0, c->cap_S * 4);
   ENS(skey1, c->cap_S * 4);
@@ -205,7 +210,7 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(unitleaf, c->cap_U * 4);
   ENS(stage, c->cap_R * 4);
   ENS(scratch, c->cap_R * 8);
-  ENS(runoff, c->cap_S * 8);
+  ENS(runinfo, c->cap_S * 8);
   ENS(outids, c->cap_R * 8);
 #undef ENS
   return TJ_OK;
@@ -254,6 +259,7 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.sq_cov = P<uint8_t>(c->sqcov);
   d.sq_count = P<int32_t>(c->sqcount);
   d.ecount = P<int32_t>(c->ecount);
+  d.srect = P<Rect4>(c->srect);
   d.slot_out = P<int64_t>(c->slotout);
   d.skey[0] = P<uint32_t>(c->skey0);
   d.skey[1] = P<uint32_t>(c->skey1);
@@ -272,7 +278,9 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.run_end = P<int32_t>(c->runs1);
   d.unit_leaf = P<int32_t>(c->unitleaf);
   d.big_list = P<int32_t>(c->biglist);
-  d.run_off = P<int64_t>(c->runoff);
+  d.leaf_active = c->shard_n > 1 ? P<uint8_t>(c->lactive) : nullptr;
+  d.leaf_wpre = P<int64_t>(c->lwpre);
+  d.run_info = P<uint64_t>(c->runinfo);
   d.scratch = P<int64_t>(c->scratch);
 }
 
@@ -341,9 +349,18 @@ int launch_tick(tj_ctx* c) {
   k_sq_runs<<<Gbig, 256, 0, st>>>(d);
   k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[1], st);
+  int extra = 0;
+  if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range
+    scan_launch(sp, LeafWeightIn{d.leaf_nobj, d.leaf_nisq, d.leaf_ncov}, PrefOut{d.leaf_wpre}, &h->L, h,
+                &h->shard_total, st);
+    k_shard_mark<<<Gbig, 256, 0, st>>>(d);
+    extra = 4;
+  }
   // ---- K3: join -----------------------------------------------------------
-  scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h, &h->W, st);
-  scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h, &h->U, st);
+  scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h, &h->W,
+              st);
+  scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h,
+              &h->U, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 2, 0, 0);
   k_unit_map<<<Gbig, 256, 0, st>>>(d);
   k_zero_counts<<<Gbig, 256, 0, st>>>(d);
@@ -356,14 +373,15 @@ int launch_tick(tj_ctx* c) {
   scan_launch(sp, QueryCntIn{d}, ExclOut<int64_t>{d.out_off}, &h->m, h, &h->R_check, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
   k_close_offsets<<<1, 1, 0, st>>>(d);
-  k_decode_leaf<<<Gbig, kDecodeThreads, 0, st>>>(d);
+  k_decode_rows<<<Gbig, kDecodeThreads, 0, st>>>(d);
+  k_decode_cov<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[4], st);
   k_assemble<<<Gbig, 256, 0, st>>>(d);
   k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[5], st);
   // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-  const int scans = 7, singles = 26 + F + (D > 0 ? 3 + (D - 1) : 0);
-  return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles;
+  const int scans = 7, singles = 27 + F + (D > 0 ? 3 + (D - 1) : 0);
+  return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles + extra;
 }
 
 void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
@@ -384,6 +402,8 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.kmin_x = H.kmin_y = ~0ull;
   H.kmax_x = H.kmax_y = 0ull;
   H.l_deep = 1;
+  H.shard_rank = c->shard_rank;
+  H.shard_n = c->shard_n;
 }
 
 int passes_for(int64_t maxkey) { return std::max(1, (bits_for(maxkey) + kRadixBits - 1) / kRadixBits); }
@@ -458,9 +478,9 @@ int tj_destroy(tj_ctx* c) {
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
-                 &c->sqcount, &c->ecount, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
-                 &c->runs1, &c->unitleaf, &c->bitmap,
-                 &c->stage, &c->outids, &c->outoff, &c->runoff, &c->scratch, &c->partial, &c->rhist, &c->roffs};
+                 &c->sqcount, &c->ecount, &c->srect, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
+                 &c->runs1, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
+                 &c->stage, &c->outids, &c->outoff, &c->runinfo, &c->scratch, &c->partial, &c->rhist, &c->roffs};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->h_off) cudaFreeHost(c->h_off);
@@ -480,6 +500,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
   const int64_t n = in->n_obj, m = in->n_q;
   if (n < 0 || m < 0) return fail(c, TJ_E_INVALID_ARG, "negative size");
   if (n > INT32_MAX / 2 || m > INT32_MAX / 2) return fail(c, TJ_E_INVALID_ARG, "tick too large for 32-bit rows");
+  if (n >= (int64_t(1) << 28)) return fail(c, TJ_E_INVALID_ARG, "more than 2^28 objects per tick is not supported");
   if ((n && (!in->obj_id || !in->obj_x || !in->obj_y)) ||
       (m && (!in->q_issuer || !in->q_xa || !in->q_ya || !in->q_xb || !in->q_yb)))
     return fail(c, TJ_E_INVALID_ARG, "null input array");
@@ -790,9 +811,10 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
   std::vector<uint32_t> bm;
-  std::vector<int32_t> ss, cnt;
+  std::vector<int32_t> ss;
+  std::vector<uint64_t> info;
   if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, ss, c->dv.ssorted, H.S)) ||
-      (rc = d2h(c, cnt, c->sqcount.p, H.S)))
+      (rc = d2h(c, info, c->runinfo.p, H.S)))
     return rc;
   int64_t t = 0, w = 0, k = 0;
   if (task_woff) task_woff[0] = 0;
@@ -806,7 +828,7 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
     if (words) std::memcpy(words + w, bm.data() + lv.woff[r], nw * 4);
     if (counts) {
       if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
-      for (int64_t j = 0; j < ni; ++j) counts[k + j] = cnt[ss[lv.sbase[r] + j]];
+      for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)(info[ss[lv.sbase[r] + j]] & ((1ull << 28) - 1));
     }
     w += nw;
     k += ni;
@@ -839,6 +861,14 @@ int tj_get_imbalance(tj_ctx* c, int32_t sim_processors, int32_t heaviest_first, 
   const int64_t top = *std::max_element(tot.begin(), tot.end());
   const int64_t low = *std::min_element(tot.begin(), tot.end());
   *imbalance = top == 0 ? 0.0 : (double)(top - low) / (double)top;
+  return TJ_OK;
+}
+
+int tj_set_shard(tj_ctx* c, int32_t rank, int32_t nranks) {
+  if (!c || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TJ_E_INVALID_ARG, "bad shard");
+  c->shard_rank = rank;
+  c->shard_n = nranks;
+  c->have = false;
   return TJ_OK;
 }
 

@@ -52,6 +52,8 @@ struct DevHdr {
   int32_t count_mismatch;   // CountMismatch
   int32_t n_big;            // queries queued for k_merge_big
   unsigned long long overfull2, overfull8;  // needs_rebuild counters
+  int32_t shard_rank, shard_n;              // leaf-range sharding (n == 1: off)
+  int64_t shard_total;                      // total leaf work weight
 };
 
 // dense pyramid layout: level 0 (root) padded to 4 entries, level l >= 1 at

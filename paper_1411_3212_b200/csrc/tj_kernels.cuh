@@ -67,6 +67,8 @@ struct Dev {
   uint8_t* sq_cov;
   int32_t* sq_count;
   int32_t* ecount;          // result count per decode entry e (entry order of ssorted)
+  Rect4* srect;             // clipped rect per subquery slot (query order)
+  uint64_t* run_info;       // per slot: (start of its decoded run in stage) << 28 | result count
   int64_t* slot_out;       // per decode row e: start of its list in `stage`
   uint32_t* skey[2];
   int32_t* sval[2];
@@ -75,6 +77,8 @@ struct Dev {
   int32_t* run_start;      // per subquery key (2*leaf + covering): first sorted position
   int32_t* run_end;        // one past the last
   int32_t* unit_leaf;      // join work unit -> leaf
+  uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
+  int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
   int32_t* big_list;       // queries whose lists need the CTA-wide merge
   int64_t* run_off;        // per subquery slot: start of its decoded run in `stage`
   int64_t* scratch;        // R entries: merge-pass scratch for k_merge_big
@@ -552,6 +556,7 @@ __device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, int64_
   const bool cv = cov_on && covers(r, lev, z, d.h);
   d.sq_leaf[slot] = (int32_t)rank;
   d.sq_q[slot] = (int32_t)q;
+  d.srect[slot] = r;  // clipped rect per subquery slot (query order: sequential writes)
   d.sq_cov[slot] = (uint8_t)((cv ? kFlagCov : 0) | (n == 1 ? kFlagSingle : 0));
   // radix key = 2*leaf + covering: per leaf, intersecting subqueries then
   // covering ones, each in slot (= query input) order — directory.py:131
@@ -673,30 +678,64 @@ constexpr int kJoinWarps = kJoinThreads / 32;
 constexpr int kST = 32;   // subqueries per work unit (one warp, lane = subquery)
 constexpr int kOTB = 32;  // 32-object blocks per work unit (1024 objects)
 
+__device__ __forceinline__ bool leaf_on(const uint8_t* active, int64_t r) { return !active || active[r]; }
+
 struct WordsIn {
   const int32_t* nobj;
   const int32_t* nisq;
+  const uint8_t* active;
   __device__ int64_t operator()(int64_t r) const {
     const int64_t no = nobj[r], ni = nisq[r];
-    return (no > 0 && ni > 0) ? ni * ((no + 31) / 32) : 0;
+    return (no > 0 && ni > 0 && leaf_on(active, r)) ? ni * ((no + 31) / 32) : 0;
   }
 };
 struct UnitsIn {
   const int32_t* nobj;
   const int32_t* nisq;
+  const uint8_t* active;
   __device__ int64_t operator()(int64_t r) const {
     const int64_t no = nobj[r], ni = nisq[r];
-    if (!(no > 0 && ni > 0)) return 0;
+    if (!(no > 0 && ni > 0 && leaf_on(active, r))) return 0;
     const int64_t nb = (no + 31) / 32;
     return ((ni + kST - 1) / kST) * ((nb + kOTB - 1) / kOTB);
   }
 };
 
+// Multi-GPU leaf-range sharding: every rank builds the same
+// index and subquery directory; leaves are cut into contiguous Morton ranges
+// balanced by a work weight (objects x subqueries + both), and a rank joins,
+// decodes and assembles only its own leaves — its per-query lists are the
+// restriction of the full lists to its leaves (disjoint across ranks).
+struct LeafWeightIn {
+  const int32_t* nobj;
+  const int32_t* nisq;
+  const int32_t* ncov;
+  __device__ int64_t operator()(int64_t r) const {
+    const int64_t no = nobj[r], sq = (int64_t)nisq[r] + ncov[r];
+    return no * sq + no + sq;
+  }
+};
+struct PrefOut {
+  int64_t* a;
+  __device__ void operator()(int64_t i, int64_t ex, int64_t) const { a[i] = ex; }
+};
+__global__ void __launch_bounds__(256) k_shard_mark(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const int64_t T = h->shard_total > 0 ? h->shard_total : 1;
+  const LeafWeightIn wt{d.leaf_nobj, d.leaf_nisq, d.leaf_ncov};
+  TJ_GRID_STRIDE(r, h->L) {
+    const int64_t mid = 2 * d.leaf_wpre[r] + wt(r);  // 2 x midpoint of the leaf's weight interval
+    const int64_t owner = (mid * h->shard_n) / (2 * T);
+    d.leaf_active[r] = (owner == h->shard_rank) || (owner >= h->shard_n && h->shard_rank == h->shard_n - 1);
+  }
+}
+
 // work unit -> leaf (so a join CTA finds its leaf with one load)
 __global__ void __launch_bounds__(256) k_unit_map(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  const UnitsIn units{d.leaf_nobj, d.leaf_nisq};
+  const UnitsIn units{d.leaf_nobj, d.leaf_nisq, d.leaf_active};
   TJ_GRID_STRIDE(r, h->L) {
     const int64_t nu = units(r), b = d.leaf_ubase[r];
     for (int64_t k = 0; k < nu; ++k) d.unit_leaf[b + k] = (int32_t)r;
@@ -706,10 +745,7 @@ __global__ void __launch_bounds__(256) k_unit_map(const Dev d) {
 __global__ void __launch_bounds__(256) k_zero_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  TJ_GRID_STRIDE(s, h->S) {
-    d.sq_count[s] = 0;
-    d.ecount[s] = 0;
-  }
+  TJ_GRID_STRIDE(s, h->S) d.ecount[s] = 0;
 }
 
 // Warp-level work units: (leaf, 32 intersecting subqueries, up to 1024
@@ -759,14 +795,11 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(const Dev d) {
     const int b0 = ot * kOTB, nbt = min(kOTB, nb - b0);
     const int32_t ob = d.leaf_obase[r];
     const bool live = lane < ns;
-    int32_t slot = 0;
+    const int64_t e = (int64_t)d.leaf_sbase[r] + s0 + lane;  // decode entry of this lane's subquery
     Rect4 R;
     R.xa = R.ya = __longlong_as_double(0x7ff0000000000000ll);   // +inf: empty rect
     R.xb = R.yb = __longlong_as_double((long long)0xfff0000000000000ull);  // -inf
-    if (live) {
-      slot = d.ssorted[d.leaf_sbase[r] + s0 + lane];
-      R = d.crect[d.sq_q[slot]];
-    }
+    if (live) R = d.srect[d.ssorted[e]];  // the one random access per subquery of the regrouping
     uint32_t cnt = 0;
     XY nxt = load_obj(d, ob, b0 * 32 + lane, nobj);
     for (int bl = 0; bl < nbt; ++bl) {
@@ -806,14 +839,8 @@ __global__ void __launch_bounds__(kJoinThreads, 4) k_join(const Dev d) {
       }
     }
     if (live) {
-      const int64_t e = (int64_t)d.leaf_sbase[r] + s0 + lane;
-      if (n_ot == 1) {
-        d.sq_count[slot] = (int32_t)cnt;
-        d.ecount[e] = (int32_t)cnt;
-      } else {
-        atomicAdd(&d.sq_count[slot], (int32_t)cnt);
-        atomicAdd(&d.ecount[e], (int32_t)cnt);
-      }
+      if (n_ot == 1) d.ecount[e] = (int32_t)cnt;
+      else atomicAdd(&d.ecount[e], (int32_t)cnt);
     }
     __syncwarp();
   }
@@ -827,13 +854,10 @@ __global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < h->L; r += nwarp) {
     const int nc = d.leaf_ncov[r];
-    if (nc == 0) continue;
+    if (nc == 0 || !leaf_on(d.leaf_active, r)) continue;
     const int32_t base = d.leaf_sbase[r] + d.leaf_nisq[r];
     const int32_t nobj = d.leaf_nobj[r];
-    for (int c = lane; c < nc; c += 32) {
-      d.sq_count[d.ssorted[base + c]] = nobj;
-      d.ecount[base + c] = nobj;
-    }
+    for (int c = lane; c < nc; c += 32) d.ecount[base + c] = nobj;
   }
 }
 
@@ -842,8 +866,15 @@ __global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
 // ===========================================================================
 // Result counts: an intersecting subquery contributes its popcount, a
 // covering one its leaf's whole block (decode.py:83-99).
-// (sq_count holds both after the join: covering entries are filled by k_cov_counts)
-__device__ __forceinline__ int64_t slot_count(const Dev& d, int32_t slot) { return (int64_t)d.sq_count[slot]; }
+// (run_info is filled per slot by the decode-order scan, RowOut: one packed
+// random write per subquery instead of two)
+constexpr int kRunCountBits = 28;
+__device__ __forceinline__ int64_t slot_count(const Dev& d, int32_t slot) {
+  return (int64_t)(d.run_info[slot] & ((1ull << kRunCountBits) - 1));
+}
+__device__ __forceinline__ int64_t slot_off(const Dev& d, int32_t slot) {
+  return (int64_t)(d.run_info[slot] >> kRunCountBits);
+}
 
 // decode order: entries e of `ssorted` (leaf by leaf, intersecting then
 // covering) — every leaf's decoded lists form one contiguous chunk of `stage`
@@ -853,9 +884,9 @@ struct RowCntIn {
 };
 struct RowOut {
   Dev d;
-  __device__ void operator()(int64_t e, int64_t ex, int64_t) const {
-    d.slot_out[e] = ex;            // row e's list starts at stage[ex]
-    d.run_off[d.ssorted[e]] = ex;  // ... which is subquery slot's run
+  __device__ void operator()(int64_t e, int64_t ex, int64_t v) const {
+    d.slot_out[e] = ex;  // row e's list starts at stage[ex] ...
+    d.run_info[d.ssorted[e]] = ((uint64_t)ex << kRunCountBits) | (uint64_t)v;  // ... = slot's run
   }
 };
 // output order: queries in input order, lists concatenated (ResultSet CSR)
@@ -875,40 +906,48 @@ __global__ void k_close_offsets(const Dev d) {
   if (h->abort) return;
   d.out_off[h->m] = h->R;
   if (h->R != h->R_check) h->count_mismatch = 1;  // CountMismatch (bitmap.py:131-132)
+  if (h->R >= (int64_t(1) << (64 - kRunCountBits))) h->count_mismatch = 1;  // run_info packing bound
 }
 
 constexpr int kDecodeThreads = 256;
-constexpr int kDecodeIds = 1024;     // leaf id blocks up to this size are staged in shared memory
-constexpr int kDecodeWords = 4096;   // leaf bitmaps up to this many words are staged too
-
 constexpr int kDecodeBatch = 512;  // per-warp staging of 32 rows' decoded rows
 
-// Alg. 4 per leaf (decode.py:40-99, bitmap.py:122-133, engine.py:306-326):
-// one CTA per leaf stages the leaf's object ids and bitmap rows in shared
-// memory.  Intersecting rows are decoded lane-per-row, 32 rows per warp step:
-// a lane walks its row's words and, for every set bit (ascending = block
-// order), puts the object's id at the row's next position.  The 32 rows'
-// lists are adjacent in `stage` (decode order), so they are assembled in a
-// per-warp shared-memory buffer and stored with full-width coalesced writes.
-// Covering subqueries copy the whole block.
-template <bool kStaged>
-__device__ __forceinline__ void decode_rows(const Dev& d, const int32_t* ids, const uint32_t* rows, int ni,
-                                            int nb, int32_t sb, int32_t* wbuf) {
+// Alg. 4 (decode.py:40-99, bitmap.py:122-133, engine.py:306-326) as warp
+// tasks over the join's work units (leaf, 32 intersecting subquery rows):
+// lane = row; the lane walks its row's words and, for every set bit
+// (ascending = block order), puts the object's input row at the row's next
+// position.  The 32 rows' lists are adjacent in `stage` (decode order), so
+// they are assembled in a per-warp shared-memory buffer and stored with
+// full-width coalesced writes.  No block barriers: warps are independent.
+__global__ void __launch_bounds__(kDecodeThreads) k_decode_rows(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  __shared__ int32_t sbatch[kDecodeThreads / 32][kDecodeBatch];
+  const int64_t U = h->U, S = h->S, R = h->R;
   const int lane = lane_id(), wp = threadIdx.x >> 5;
-  constexpr int nw = kDecodeThreads / 32;
-  const int64_t S = d.h->S, R = d.h->R;
-  for (int r0 = wp * 32; r0 < ni; r0 += nw * 32) {
-    const int row = r0 + lane;
-    const bool live = row < ni;
-    const int64_t off = live ? d.slot_out[sb + row] : 0;
-    const int nrow = min(32, ni - r0);
-    const int64_t e_end = (int64_t)sb + r0 + nrow;
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int32_t* wbuf = sbatch[wp];
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarp) {
+    const int64_t r = d.unit_leaf[u];
+    const int nobj = d.leaf_nobj[r], ni = d.leaf_nisq[r];
+    const int nb = (nobj + 31) >> 5;
+    const int n_ot = (nb + kOTB - 1) / kOTB;
+    const int lu = (int)(u - d.leaf_ubase[r]);
+    const int st = lu / n_ot, ot = lu - st * n_ot;
+    if (ot != 0) continue;  // one decode task per 32-row chunk (all object tiles at once)
+    const int r0 = st * kST, nrow = min(32, ni - r0);
+    const int32_t sb = d.leaf_sbase[r];
+    const int32_t* ids = d.sidx + d.leaf_obase[r];  // input rows of the leaf's objects (block order)
+    const bool live = lane < nrow;
+    const int64_t e = (int64_t)sb + r0 + lane;
+    const int64_t off = live ? d.slot_out[e] : 0;
     const int64_t base = __shfl_sync(0xffffffffu, off, 0);
+    const int64_t e_end = (int64_t)sb + r0 + nrow;
     const int64_t end = e_end < S ? d.slot_out[e_end] : R;
     const int64_t total = end - base;
     const bool buffered = total <= kDecodeBatch;
     if (live) {
-      const uint32_t* words = rows + (int64_t)row * nb;
+      const uint32_t* words = d.bitmap + d.leaf_woff[r] + (int64_t)(r0 + lane) * nb;
       if (buffered) {
         int32_t* dst = wbuf + (off - base);  // shared memory
         for (int b = 0; b < nb; ++b) {
@@ -938,40 +977,25 @@ __device__ __forceinline__ void decode_rows(const Dev& d, const int32_t* ids, co
   }
 }
 
-__global__ void __launch_bounds__(kDecodeThreads) k_decode_leaf(const Dev d) {
+// covering subqueries copy the whole block (decode.py:83-99), a warp per leaf
+__global__ void __launch_bounds__(256) k_decode_cov(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  __shared__ int32_t sids[kDecodeIds];
-  __shared__ uint32_t swords[kDecodeWords];
-  __shared__ int32_t sbatch[kDecodeThreads / 32][kDecodeBatch];
-  const int64_t L = h->L;
-  const int t = threadIdx.x, wp = t >> 5, lane = t & 31;
-  constexpr int nw = kDecodeThreads / 32;
+  const int lane = lane_id();
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
   unsigned long long covres = 0;
-  for (int64_t r = blockIdx.x; r < L; r += gridDim.x) {
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < h->L; r += nwarp) {
+    const int nc = d.leaf_ncov[r];
+    if (nc == 0 || !leaf_on(d.leaf_active, r)) continue;
     const int nobj = d.leaf_nobj[r];
-    const int ni = d.leaf_nisq[r], nc = d.leaf_ncov[r];
-    if (nobj == 0 || (ni == 0 && nc == 0)) continue;
-    const int32_t ob = d.leaf_obase[r], sb = d.leaf_sbase[r];
-    const int nb = (nobj + 31) >> 5;
-    const int32_t* gids = d.sidx + ob;  // input rows of the leaf's objects (block order)
-    const uint32_t* grows = d.bitmap + d.leaf_woff[r];
-    const int64_t nwords = (int64_t)ni * nb;
-    const bool staged = nobj <= kDecodeIds && nwords <= kDecodeWords;
-    if (staged) {
-      for (int k = t; k < nobj; k += kDecodeThreads) sids[k] = gids[k];
-      for (int k = t; k < nwords; k += kDecodeThreads) swords[k] = grows[k];
-      __syncthreads();
-      decode_rows<true>(d, sids, swords, ni, nb, sb, sbatch[wp]);
-    } else {
-      decode_rows<false>(d, gids, grows, ni, nb, sb, sbatch[wp]);
+    if (nobj == 0) continue;
+    const int32_t* ids = d.sidx + d.leaf_obase[r];
+    const int32_t e0 = d.leaf_sbase[r] + d.leaf_nisq[r];
+    for (int c = 0; c < nc; ++c) {
+      int32_t* dst = d.stage + d.slot_out[e0 + c];
+      for (int k = lane; k < nobj; k += 32) dst[k] = ids[k];
     }
-    for (int c = wp; c < nc; c += nw) {
-      int32_t* dst = d.stage + d.slot_out[sb + ni + c];
-      for (int k = lane; k < nobj; k += 32) dst[k] = gids[k];
-      if (lane == 0) covres += (unsigned long long)nobj;
-    }
-    __syncthreads();
+    if (lane == 0) covres += (unsigned long long)nobj * nc;
   }
   if (lane == 0 && covres) atomicAdd(&h->cov_results, covres);
 }
@@ -1074,7 +1098,7 @@ __global__ void __launch_bounds__(256) k_assemble(const Dev d) {
     // otherwise): flattened copy of the warp's output range — independent
     // loads, coalesced stores
     const bool single = kl == 1 && (mono || cntl <= 1);
-    const int64_t srcl = (single && cntl > 0) ? d.run_off[s0l] : -1;
+    const int64_t srcl = (single && cntl > 0) ? slot_off(d, s0l) : -1;
     const bool done = kl == 0 || cntl == 0 || single;
     {
       const int64_t lo = __shfl_sync(0xffffffffu, qol, 0);
@@ -1082,22 +1106,75 @@ __global__ void __launch_bounds__(256) k_assemble(const Dev d) {
       const int64_t hi2 = q0 + 32 <= m ? hi : d.out_off[m];
       const int nvalid = (int)min((int64_t)32, m - q0);
       const uint32_t rel = lane < nvalid ? (uint32_t)(qol - lo) : 0xffffffffu;
-      for (int64_t p0 = lo; p0 < hi2; p0 += 32) {
-        const uint32_t pr = (uint32_t)(p0 - lo) + lane;
-        int j = 0;
+      constexpr int U = 4;  // 4 x 32 outputs per step: 4 independent loads in flight per lane
+      for (int64_t p0 = lo; p0 < hi2; p0 += 32 * U) {
+        int64_t src[U];
 #pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const uint32_t v = __shfl_sync(0xffffffffu, rel, j + step);
-          if (v <= pr) j += step;
+        for (int u = 0; u < U; ++u) {
+          const uint32_t pr = (uint32_t)(p0 - lo) + u * 32 + lane;
+          int j = 0;
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const uint32_t v = __shfl_sync(0xffffffffu, rel, j + step);
+            if (v <= pr) j += step;
+          }
+          const uint32_t relj = __shfl_sync(0xffffffffu, rel, j);
+          const int64_t srcj = __shfl_sync(0xffffffffu, srcl, j);
+          src[u] = (p0 + u * 32 + lane < hi2 && srcj >= 0) ? srcj + (pr - relj) : -1;
         }
-        const uint32_t relj = __shfl_sync(0xffffffffu, rel, j);
-        const int64_t srcj = __shfl_sync(0xffffffffu, srcl, j);
-        if (p0 + lane < hi2 && srcj >= 0) d.out_ids[p0 + lane] = idof(stage[srcj + (pr - relj)]);
+        int32_t val[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) val[u] = src[u] >= 0 ? stage[src[u]] : 0;
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+          if (src[u] >= 0) d.out_ids[p0 + u * 32 + lane] = idof(val[u]);
+      }
+    }
+    // monotone ids, 2..4 runs: lane-per-query k-way merge straight from the
+    // decoded runs (heads in registers, one-element lookahead per run); the
+    // 32 queries of the warp merge concurrently
+    const bool lanemerge = mono && !done && kl >= 2 && kl <= 4 && cntl <= 512;
+    if (__any_sync(0xffffffffu, lanemerge) && lanemerge) {
+      int64_t pos[4], end[4];
+      int32_t head[4];
+      int64_t acc = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        pos[j] = 0;
+        end[j] = 0;
+        head[j] = 0x7fffffff;
+        if (j < kl) {
+          const int64_t c = slot_count(d, s0l + j);
+          pos[j] = slot_off(d, s0l + j);
+          end[j] = pos[j] + c;
+          acc += c;
+          if (c > 0) head[j] = stage[pos[j]];
+        }
+      }
+      int64_t* out = d.out_ids + qol;
+      for (int64_t o = 0; o < cntl; ++o) {
+        int bj = 0;
+        int32_t bv = head[0];
+#pragma unroll
+        for (int j = 1; j < 4; ++j)
+          if (head[j] < bv) {
+            bv = head[j];
+            bj = j;
+          }
+        out[o] = idof(bv);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (j == bj) {
+            ++pos[j];
+            head[j] = pos[j] < end[j] ? stage[pos[j]] : 0x7fffffff;
+            if (((pos[j] & 7) == 0) && pos[j] + 16 < end[j])  // pull the sector two ahead into L1
+              asm volatile("prefetch.global.L1 [%0];" ::"l"(stage + pos[j] + 16));
+          }
       }
     }
     // short multi-run lists (<= 64 entries, <= 32 runs): one query at a
     // time, the next query's run metadata in flight meanwhile
-    const bool smallq = !done && cntl <= 64 && kl <= 32;
+    const bool smallq = !done && !lanemerge && cntl <= 64 && kl <= 32;
     unsigned pend = __ballot_sync(0xffffffffu, smallq);
     {
       auto meta = [&](int src, int64_t& c, int64_t& o) {
@@ -1107,7 +1184,7 @@ __global__ void __launch_bounds__(256) k_assemble(const Dev d) {
         o = 0;
         if (lane < kk) {
           c = slot_count(d, ss + lane);
-          o = d.run_off[ss + lane];
+          o = slot_off(d, ss + lane);
         }
       };
       int cur = pend ? __ffs(pend) - 1 : -1;
@@ -1176,7 +1253,7 @@ __global__ void __launch_bounds__(256) k_assemble(const Dev d) {
     }
     // long lists / many runs: concatenate the runs (as ids) into the output
     // and queue the query for the CTA-wide sort
-    unsigned todo = __ballot_sync(0xffffffffu, !done && !smallq);
+    unsigned todo = __ballot_sync(0xffffffffu, !done && !smallq && !lanemerge);
     while (todo) {
       const int src_lane = __ffs(todo) - 1;
       todo &= todo - 1;
@@ -1189,7 +1266,7 @@ __global__ void __launch_bounds__(256) k_assemble(const Dev d) {
         int64_t cj = 0, oj = 0;
         if (j < k) {
           cj = slot_count(d, s0 + j);
-          oj = d.run_off[s0 + j];
+          oj = slot_off(d, s0 + j);
         }
         const int64_t inc = warp_incl_scan(cj);
         const int64_t seg = __shfl_sync(0xffffffffu, inc, 31);
