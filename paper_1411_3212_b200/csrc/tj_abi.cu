@@ -41,13 +41,13 @@ struct tj_ctx {
   // objects
   DBuf code, okey0, okey1, oval0, oval1, sx, sy, sid;
   // index
-  DBuf pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
+  DBuf linfo, pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
   DBuf crect, qwin, nsub, qsbase, biglist;
   // subqueries
-  DBuf sqleaf, sqq, sqcov, sqcount, ecount, srect, slotout, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
+  DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
   // join / outputs
-  DBuf bitmap, stage, outids, outoff, runinfo, scratch;
+  DBuf bitmap, outids, outoff, scratch;
   // scan / radix scratch
   DBuf partial, rhist, roffs;
   // pinned host outputs
@@ -168,6 +168,7 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(lncov, c->cap_L * 4);
   ENS(lsbase, c->cap_L * 4);
   ENS(lwoff, c->cap_L * 8);
+  ENS(linfo, c->cap_L * 16);
   ENS(lubase, c->cap_L * 8);
   ENS(runs0, c->cap_L * 2 * 4);
   ENS(lactive, c->cap_L);
@@ -199,18 +200,17 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sqq, c->cap_S * 4);
   ENS(sqcov, c->cap_S);
   ENS(sqcount, c->cap_S * 4);
+  ENS(erect, c->cap_S * sizeof(Rect4));
   ENS(ecount, c->cap_S * 4);
-  ENS(srect, c->cap_S * sizeof(Rect4));
-  ENS(slotout, c->cap_S * 8);
+  ENS(sinv, c->cap_S * 4);
+  ENS(slotoff, (c->cap_S + 1) * 8);
   ENS(skey0, c->cap_S * 4);
   ENS(skey1, c->cap_S * 4);
   ENS(sval0, c->cap_S * 4);
   ENS(sval1, c->cap_S * 4);
   ENS(bitmap, c->cap_W * 4);
   ENS(unitleaf, c->cap_U * 4);
-  ENS(stage, c->cap_R * 4);
   ENS(scratch, c->cap_R * 8);
-  ENS(runinfo, c->cap_S * 8);
   ENS(outids, c->cap_R * 8);
 #undef ENS
   return TJ_OK;
@@ -258,15 +258,16 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.sq_q = P<int32_t>(c->sqq);
   d.sq_cov = P<uint8_t>(c->sqcov);
   d.sq_count = P<int32_t>(c->sqcount);
+  d.erect = P<Rect4>(c->erect);
   d.ecount = P<int32_t>(c->ecount);
-  d.srect = P<Rect4>(c->srect);
-  d.slot_out = P<int64_t>(c->slotout);
+  d.sinv = P<int32_t>(c->sinv);
+  d.linfo = P<int4>(c->linfo);
+  d.slot_off = P<int64_t>(c->slotoff);
   d.skey[0] = P<uint32_t>(c->skey0);
   d.skey[1] = P<uint32_t>(c->skey1);
   d.sval[0] = P<int32_t>(c->sval0);
   d.sval[1] = P<int32_t>(c->sval1);
   d.bitmap = P<uint32_t>(c->bitmap);
-  d.stage = P<int32_t>(c->stage);
   d.out_ids = P<int64_t>(c->outids);
   d.out_off = P<int64_t>(c->outoff);
   d.D = lmax - F;
@@ -280,7 +281,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.big_list = P<int32_t>(c->biglist);
   d.leaf_active = c->shard_n > 1 ? P<uint8_t>(c->lactive) : nullptr;
   d.leaf_wpre = P<int64_t>(c->lwpre);
-  d.run_info = P<uint64_t>(c->runinfo);
   d.scratch = P<int64_t>(c->scratch);
 }
 
@@ -348,6 +348,8 @@ int launch_tick(tj_ctx* c) {
   radix_sort(c, d.skey, d.sval, &h->S, c->sq_passes);
   k_sq_runs<<<Gbig, 256, 0, st>>>(d);
   k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
+  k_entries<<<Gbig, 256, 0, st>>>(d);
+  k_sinv<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[1], st);
   int extra = 0;
   if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range
@@ -365,22 +367,20 @@ int launch_tick(tj_ctx* c) {
   k_unit_map<<<Gbig, 256, 0, st>>>(d);
   k_zero_counts<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[2], st);
-  k_join<<<c->num_sms * 8, kJoinThreads, 0, st>>>(d);
+  k_join<<<c->num_sms * 4, kJT, sizeof(JoinSmem), st>>>(d);
   cudaEventRecord(c->ev[3], st);
   // ---- K4: decode + canonical lists --------------------------------------
   k_cov_counts<<<Gbig, 256, 0, st>>>(d);
-  scan_launch(sp, RowCntIn{d}, RowOut{d}, &h->S, h, &h->R, st);
-  scan_launch(sp, QueryCntIn{d}, ExclOut<int64_t>{d.out_off}, &h->m, h, &h->R_check, st);
+  k_slot_counts<<<Gbig, 256, 0, st>>>(d);
+  scan_launch(sp, ArrIn<int32_t>{d.sq_count}, ExclOut<int64_t>{d.slot_off}, &h->S, h, &h->R, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
   k_close_offsets<<<1, 1, 0, st>>>(d);
-  k_decode_rows<<<Gbig, kDecodeThreads, 0, st>>>(d);
-  k_decode_cov<<<Gbig, 256, 0, st>>>(d);
+  k_decode_query<<<Gbig, kDQThreads, 0, st>>>(d);
   cudaEventRecord(c->ev[4], st);
-  k_assemble<<<Gbig, 256, 0, st>>>(d);
   k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[5], st);
   // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-  const int scans = 7, singles = 27 + F + (D > 0 ? 3 + (D - 1) : 0);
+  const int scans = 6, singles = 28 + F + (D > 0 ? 3 + (D - 1) : 0);
   return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles + extra;
 }
 
@@ -464,6 +464,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
     return fail(nullptr, TJ_E_CUDA, msg);
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
   int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
   *out = c;
@@ -478,9 +479,9 @@ int tj_destroy(tj_ctx* c) {
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
-                 &c->sqcount, &c->ecount, &c->srect, &c->slotout, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
+                 &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
                  &c->runs1, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
-                 &c->stage, &c->outids, &c->outoff, &c->runinfo, &c->scratch, &c->partial, &c->rhist, &c->roffs};
+                 &c->outids, &c->outoff, &c->scratch, &c->partial, &c->rhist, &c->roffs};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->h_off) cudaFreeHost(c->h_off);
@@ -811,10 +812,8 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
   std::vector<uint32_t> bm;
-  std::vector<int32_t> ss;
-  std::vector<uint64_t> info;
-  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, ss, c->dv.ssorted, H.S)) ||
-      (rc = d2h(c, info, c->runinfo.p, H.S)))
+  std::vector<int32_t> info;
+  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, info, c->ecount.p, H.S)))
     return rc;
   int64_t t = 0, w = 0, k = 0;
   if (task_woff) task_woff[0] = 0;
@@ -828,7 +827,7 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
     if (words) std::memcpy(words + w, bm.data() + lv.woff[r], nw * 4);
     if (counts) {
       if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
-      for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)(info[ss[lv.sbase[r] + j]] & ((1ull << 28) - 1));
+      for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)info[lv.sbase[r] + j];
     }
     w += nw;
     k += ni;

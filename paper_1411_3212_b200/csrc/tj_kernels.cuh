@@ -65,11 +65,12 @@ struct Dev {
   int32_t* sq_leaf;
   int32_t* sq_q;
   uint8_t* sq_cov;
-  int32_t* sq_count;
-  int32_t* ecount;          // result count per decode entry e (entry order of ssorted)
-  Rect4* srect;             // clipped rect per subquery slot (query order)
-  uint64_t* run_info;       // per slot: (start of its decoded run in stage) << 28 | result count
-  int64_t* slot_out;       // per decode row e: start of its list in `stage`
+  int32_t* sq_count;        // result count per subquery slot (popcount, or block size if covering)
+  int32_t* ecount;          // result count per directory entry (entry order)
+  Rect4* erect;             // clipped rect per directory entry (entry order, the join's input)
+  int32_t* sinv;            // per slot: its directory entry (inverse of ssorted)
+  int4* linfo;              // per leaf: object base, object count, entry base, intersecting count
+  int64_t* slot_off;        // per slot (S + 1): start of its run in the output CSR
   uint32_t* skey[2];
   int32_t* sval[2];
   const int32_t* ssorted;  // per leaf [isq slots asc][cov slots asc]
@@ -80,11 +81,9 @@ struct Dev {
   uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
   int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
   int32_t* big_list;       // queries whose lists need the CTA-wide merge
-  int64_t* run_off;        // per subquery slot: start of its decoded run in `stage`
   int64_t* scratch;        // R entries: merge-pass scratch for k_merge_big
   // join + outputs
   uint32_t* bitmap;
-  int32_t* stage;          // decoded runs (input rows), decode order
   int64_t* out_ids;
   int64_t* out_off;
   // config
@@ -556,7 +555,6 @@ __device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, int64_
   const bool cv = cov_on && covers(r, lev, z, d.h);
   d.sq_leaf[slot] = (int32_t)rank;
   d.sq_q[slot] = (int32_t)q;
-  d.srect[slot] = r;  // clipped rect per subquery slot (query order: sequential writes)
   d.sq_cov[slot] = (uint8_t)((cv ? kFlagCov : 0) | (n == 1 ? kFlagSingle : 0));
   // radix key = 2*leaf + covering: per leaf, intersecting subqueries then
   // covering ones, each in slot (= query input) order — directory.py:131
@@ -620,6 +618,20 @@ __global__ void __launch_bounds__(256) k_sq_runs(const Dev d) {
   }
 }
 
+// Directory in entry order for the join: the clipped rect of every entry's
+// query (one random 32-byte read per entry, fully parallel), and the inverse
+// permutation slot -> entry for the query-order decode.
+__global__ void __launch_bounds__(256) k_entries(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  TJ_GRID_STRIDE(e, h->S) d.erect[e] = d.crect[d.sq_q[d.ssorted[e]]];
+}
+__global__ void __launch_bounds__(256) k_sinv(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  TJ_GRID_STRIDE(e, h->S) d.sinv[d.ssorted[e]] = (int32_t)e;
+}
+
 // per-leaf occupancy / task statistics (engine.py:212-225,261-267)
 __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
   DevHdr* h = d.h;
@@ -632,6 +644,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
     d.leaf_nisq[r] = a1 - a0;
     d.leaf_ncov[r] = c1 - c0;
     d.leaf_sbase[r] = (a1 > a0) ? a0 : c0;
+    d.linfo[r] = make_int4(d.leaf_obase[r], d.leaf_nobj[r], (a1 > a0) ? a0 : c0, a1 - a0);
     const unsigned long long no = (unsigned long long)d.leaf_nobj[r];
     const unsigned long long ni = (unsigned long long)(a1 - a0);
     si += ni;
@@ -673,10 +686,35 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
 // ===========================================================================
 // K3: per-leaf join (Alg. 2) into linear bitmaps
 // ===========================================================================
-constexpr int kJoinThreads = 256;
-constexpr int kJoinWarps = kJoinThreads / 32;
-constexpr int kST = 32;   // subqueries per work unit (one warp, lane = subquery)
-constexpr int kOTB = 32;  // 32-object blocks per work unit (1024 objects)
+// Work unit = (task leaf, object tile of up to 16 blocks = 512 objects); one
+// CTA per unit.  The tile's (x, y) are staged in shared memory once and
+// tested against every intersecting subquery of the leaf.  The output is the
+// paper's bitmap: bit k of word b of subquery s is the closed fp64 test
+// xa <= x <= xb and ya <= y <= yb of object 32b + k of the leaf's block
+// (bitmap.py:89-97), stored in the linear layout linear[s*blocks + b]
+// (bitmap.py:105-111), plus per-subquery popcounts (bitmap.py:114-119).
+//
+// Testing every (subquery, object) pair costs four fp64 compares on the
+// 64-lane/clk FP64 pipe.  Leaves with enough subqueries instead bucket each
+// axis of the tile into 256 equal buckets with one monotone map
+// k(v) = floor(fl(fl(v - min) * 256 / (max - min))), and build, per axis and
+// per 32-object block, the prefix tables Pre_k = {objects with bucket < k}
+// (shared-memory atomicOr scatter + a warp OR-scan per column).  Because k is
+// monotone, an object whose bucket lies strictly between the buckets of a
+// subquery's two bounds passes that axis' test, and one outside them fails
+// it; so a whole result word is
+//   D = (Pre_kb & ~Pre_ka+1)_x & (Pre_kb & ~Pre_ka+1)_y      (certain bits)
+// from eight table loads, and only the few objects that share a bucket with
+// a bound (A = (Pre_kb+1 & ~Pre_ka)_x & (...)_y & ~D) get the exact fp64
+// test.  Bit-identical to the direct test by construction.
+constexpr int kJT = 256;                      // join CTA threads
+constexpr int kJW = kJT / 32;
+constexpr int kTileBlocks = 16;               // object tile: 16 blocks = 512 objects
+constexpr int kTileObj = kTileBlocks * 32;
+constexpr int kNK = 256;                      // buckets per axis
+constexpr int kRows = kNK + 3;                // prefix rows k = 0 .. kNK + 2
+constexpr int kQC = 256;                      // subqueries per chunk
+constexpr int kTableMinQ = 12;                // table path from this many subqueries
 
 __device__ __forceinline__ bool leaf_on(const uint8_t* active, int64_t r) { return !active || active[r]; }
 
@@ -697,7 +735,7 @@ struct UnitsIn {
     const int64_t no = nobj[r], ni = nisq[r];
     if (!(no > 0 && ni > 0 && leaf_on(active, r))) return 0;
     const int64_t nb = (no + 31) / 32;
-    return ((ni + kST - 1) / kST) * ((nb + kOTB - 1) / kOTB);
+    return (nb + kTileBlocks - 1) / kTileBlocks;
   }
 };
 
@@ -745,240 +783,222 @@ __global__ void __launch_bounds__(256) k_unit_map(const Dev d) {
 __global__ void __launch_bounds__(256) k_zero_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  TJ_GRID_STRIDE(s, h->S) d.ecount[s] = 0;
+  TJ_GRID_STRIDE(e, h->S) d.ecount[e] = 0;
 }
 
-// Warp-level work units: (leaf, 32 intersecting subqueries, up to 1024
-// objects), lane = subquery.  The lane keeps its clipped rect in registers;
-// for each 32-object block of the leaf, the warp stages the block's (x, y)
-// pairs in its shared-memory slice (prefetching the next block), and every
-// lane walks the 32 objects (broadcast loads) with four chained closed fp64
-// comparisons + one predicated OR per object (bitmap.py:89-94) — bit k of the
-// lane's word is object 32b+k of the leaf's block (bitmap.py:95-97), i.e. the
-// paper's bitmap word lands directly in the subquery's lane, no ballot or
-// transpose.  Words are staged per warp and stored in the linear layout
-// linear[s*blocks + b] (bitmap.py:105-111) with coalesced rows; popcounts
-// (bitmap.py:114-119) stay in registers.  Warps never wait on each other.
-struct __align__(16) XY {
-  double x, y;
+struct JoinSmem {
+  double ox[kTileObj];                  // tile objects (NaN padding never matches)
+  double oy[kTileObj];
+  uint32_t tab[2 * kRows * kTileBlocks];  // [axis][k][b], row stride = tile blocks
+  Rect4 rect[kQC];                      // clipped rects of the chunk's subqueries
+  ushort4 kb[kQC];                      // bucket of xa, xb, ya, yb
+  int32_t cnt[kQC];
+  double red[4][kJW];
 };
 
-__device__ __forceinline__ XY load_obj(const Dev& d, int32_t ob, int k, int nobj) {
-  XY o;
-  if (k < nobj) {
-    o.x = d.sx[ob + k];
-    o.y = d.sy[ob + k];
-  } else {  // padding objects never match (NaN compares false): padding bits stay zero
-    o.x = __longlong_as_double(0x7ff8000000000000ll);
-    o.y = o.x;
-  }
-  return o;
+__device__ __forceinline__ int bucket_obj(double v, double base, double scale) {
+  double t = __dmul_rn(__dsub_rn(v, base), scale);
+  t = t < (double)(kNK - 1) ? t : (double)(kNK - 1);
+  return 1 + __double2int_rz(t);
+}
+__device__ __forceinline__ int bucket_bound(double v, double base, double top, double scale) {
+  if (v < base) return 0;
+  if (v > top) return kNK + 1;
+  return bucket_obj(v, base, scale);
 }
 
-__global__ void __launch_bounds__(kJoinThreads, 4) k_join(const Dev d) {
+__device__ __forceinline__ bool in_rect(double x, double y, const Rect4& R) {
+  return x >= R.xa && x <= R.xb && y >= R.ya && y <= R.yb;  // bitmap.py:89-94
+}
+
+__global__ void __launch_bounds__(kJT) k_join(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  __shared__ XY sobj[kJoinWarps][32];
-  __shared__ uint32_t stile[kJoinWarps][32][kOTB + 1];
+  extern __shared__ __align__(16) unsigned char join_smem[];
+  JoinSmem& S = *reinterpret_cast<JoinSmem*>(join_smem);
+  const int tid = threadIdx.x, lane = lane_id(), wp = tid >> 5;
   const int64_t U = h->U;
-  const int lane = lane_id(), wp = threadIdx.x >> 5;
-  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  XY* so = sobj[wp];
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarp) {
+  const double kNaN = __longlong_as_double(0x7ff8000000000000ll);
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
     const int64_t r = d.unit_leaf[u];
     const int nobj = d.leaf_nobj[r], nisq = d.leaf_nisq[r];
     const int nb = (nobj + 31) >> 5;
-    const int n_ot = (nb + kOTB - 1) / kOTB;
-    const int lu = (int)(u - d.leaf_ubase[r]);
-    const int st = lu / n_ot, ot = lu - st * n_ot;
-    const int s0 = st * kST, ns = min(kST, nisq - s0);
-    const int b0 = ot * kOTB, nbt = min(kOTB, nb - b0);
-    const int32_t ob = d.leaf_obase[r];
-    const bool live = lane < ns;
-    const int64_t e = (int64_t)d.leaf_sbase[r] + s0 + lane;  // decode entry of this lane's subquery
-    Rect4 R;
-    R.xa = R.ya = __longlong_as_double(0x7ff0000000000000ll);   // +inf: empty rect
-    R.xb = R.yb = __longlong_as_double((long long)0xfff0000000000000ull);  // -inf
-    if (live) R = d.srect[d.ssorted[e]];  // the one random access per subquery of the regrouping
-    uint32_t cnt = 0;
-    XY nxt = load_obj(d, ob, b0 * 32 + lane, nobj);
-    for (int bl = 0; bl < nbt; ++bl) {
-      so[lane] = nxt;
-      __syncwarp();
-      if (bl + 1 < nbt) nxt = load_obj(d, ob, (b0 + bl + 1) * 32 + lane, nobj);
-      uint32_t w = 0;
+    const int ot = (int)(u - d.leaf_ubase[r]);
+    const int n_ot = (nb + kTileBlocks - 1) / kTileBlocks;
+    const int b0 = ot * kTileBlocks, nbt = min(kTileBlocks, nb - b0);
+    const int P = min(nobj - b0 * 32, nbt * 32);
+    const int32_t ob = d.leaf_obase[r] + b0 * 32;
+    const int64_t woff = d.leaf_woff[r];
+    const int32_t sbase = d.leaf_sbase[r];
+    const bool table = nisq >= kTableMinQ;
+    // ---- stage the tile's objects -------------------------------------------
+    double mnx = __longlong_as_double(0x7ff0000000000000ll), mny = mnx;
+    double mxx = -mnx, mxy = -mnx;
+    for (int i = tid; i < nbt * 32; i += kJT) {
+      double x = kNaN, y = kNaN;
+      if (i < P) {
+        x = d.sx[ob + i];
+        y = d.sy[ob + i];
+        mnx = fmin(mnx, x);
+        mny = fmin(mny, y);
+        mxx = fmax(mxx, x);
+        mxy = fmax(mxy, y);
+      }
+      S.ox[i] = x;
+      S.oy[i] = y;
+    }
+    double basex = 0, basey = 0, topx = 0, topy = 0, scx = 0, scy = 0;
+    if (table) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
-        const XY o = so[k];
-        // closed test, chained predicates: 4 DSETP + 1 predicated OR per object
-        asm("{\n\t.reg .pred p;\n\t"
-            "setp.ge.f64 p, %1, %2;\n\t"
-            "setp.le.and.f64 p, %1, %3, p;\n\t"
-            "setp.ge.and.f64 p, %4, %5, p;\n\t"
-            "setp.le.and.f64 p, %4, %6, p;\n\t"
-            "@p or.b32 %0, %0, %7;\n\t}"
-            : "+r"(w)
-            : "d"(o.x), "d"(R.xa), "d"(R.xb), "d"(o.y), "d"(R.ya), "d"(R.yb), "r"(1u << k));
+      for (int o = 16; o > 0; o >>= 1) {
+        mnx = fmin(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
+        mny = fmin(mny, __shfl_xor_sync(0xffffffffu, mny, o));
+        mxx = fmax(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
+        mxy = fmax(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
       }
-      stile[wp][lane][bl] = w;
-      cnt += __popc(w);
-      __syncwarp();
-    }
-    uint32_t* out = d.bitmap + d.leaf_woff[r] + (int64_t)s0 * nb + b0;
-    if (nbt == nb) {
-      const int tot = ns * nb;
-      for (int e = lane; e < tot; e += 32) {
-        const int s = e / nb;
-        out[e] = stile[wp][s][e - s * nb];
+      if (lane == 0) {
+        S.red[0][wp] = mnx;
+        S.red[1][wp] = mny;
+        S.red[2][wp] = mxx;
+        S.red[3][wp] = mxy;
       }
-    } else {
-      const int tot = ns * nbt;
-      for (int e = lane; e < tot; e += 32) {
-        const int s = e / nbt, c = e - s * nbt;
-        out[(int64_t)s * nb + c] = stile[wp][s][c];
+      for (int i = tid; i < 2 * kRows * nbt; i += kJT) S.tab[i] = 0u;
+      __syncthreads();
+      basex = S.red[0][0], basey = S.red[1][0], topx = S.red[2][0], topy = S.red[3][0];
+#pragma unroll
+      for (int w = 1; w < kJW; ++w) {
+        basex = fmin(basex, S.red[0][w]);
+        basey = fmin(basey, S.red[1][w]);
+        topx = fmax(topx, S.red[2][w]);
+        topy = fmax(topy, S.red[3][w]);
+      }
+      scx = __ddiv_rn((double)kNK, __dsub_rn(topx, basex));
+      scy = __ddiv_rn((double)kNK, __dsub_rn(topy, basey));
+      if (!(scx < 1e300)) scx = 0.0;  // empty extent (or overflow): one bucket, all ambiguous
+      if (!(scy < 1e300)) scy = 0.0;
+      // bucket scatter: Bk[axis][k][b] |= bit of each object
+      for (int i = tid; i < P; i += kJT) {
+        const int kx = bucket_obj(S.ox[i], basex, scx), ky = bucket_obj(S.oy[i], basey, scy);
+        const uint32_t bit = 1u << (i & 31);
+        atomicOr(&S.tab[(0 * kRows + kx) * nbt + (i >> 5)], bit);
+        atomicOr(&S.tab[(1 * kRows + ky) * nbt + (i >> 5)], bit);
+      }
+      __syncthreads();
+      // exclusive prefix-OR down every (axis, block) column: Pre_k = OR_{k' < k} Bk_k'
+      constexpr int kPer = (kRows + 31) / 32;
+      for (int task = wp; task < 2 * nbt; task += kJW) {
+        const int ax = task / nbt, b = task - ax * nbt;
+        uint32_t* col = S.tab + ax * kRows * nbt + b;
+        uint32_t v[kPer];
+        uint32_t acc = 0;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int k = lane * kPer + j;
+          v[j] = k < kRows ? col[k * nbt] : 0u;
+          acc |= v[j];
+        }
+        uint32_t pre = acc;  // inclusive OR-scan of the lane totals
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre |= t;
+        }
+        uint32_t run = __shfl_up_sync(0xffffffffu, pre, 1);
+        if (lane == 0) run = 0u;
+#pragma unroll
+        for (int j = 0; j < kPer; ++j) {
+          const int k = lane * kPer + j;
+          if (k < kRows) col[k * nbt] = run;
+          run |= v[j];
+        }
       }
     }
-    if (live) {
-      if (n_ot == 1) d.ecount[e] = (int32_t)cnt;
-      else atomicAdd(&d.ecount[e], (int32_t)cnt);
-    }
-    __syncwarp();
-  }
-}
-
-// covering subqueries' counts = their leaf's whole block
-__global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  const int lane = lane_id();
-  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < h->L; r += nwarp) {
-    const int nc = d.leaf_ncov[r];
-    if (nc == 0 || !leaf_on(d.leaf_active, r)) continue;
-    const int32_t base = d.leaf_sbase[r] + d.leaf_nisq[r];
-    const int32_t nobj = d.leaf_nobj[r];
-    for (int c = lane; c < nc; c += 32) d.ecount[base + c] = nobj;
-  }
-}
-
-// ===========================================================================
-// K4: decode, covering expansion, canonical per-query lists
-// ===========================================================================
-// Result counts: an intersecting subquery contributes its popcount, a
-// covering one its leaf's whole block (decode.py:83-99).
-// (run_info is filled per slot by the decode-order scan, RowOut: one packed
-// random write per subquery instead of two)
-constexpr int kRunCountBits = 28;
-__device__ __forceinline__ int64_t slot_count(const Dev& d, int32_t slot) {
-  return (int64_t)(d.run_info[slot] & ((1ull << kRunCountBits) - 1));
-}
-__device__ __forceinline__ int64_t slot_off(const Dev& d, int32_t slot) {
-  return (int64_t)(d.run_info[slot] >> kRunCountBits);
-}
-
-// decode order: entries e of `ssorted` (leaf by leaf, intersecting then
-// covering) — every leaf's decoded lists form one contiguous chunk of `stage`
-struct RowCntIn {
-  Dev d;
-  __device__ int64_t operator()(int64_t e) const { return (int64_t)d.ecount[e]; }
-};
-struct RowOut {
-  Dev d;
-  __device__ void operator()(int64_t e, int64_t ex, int64_t v) const {
-    d.slot_out[e] = ex;  // row e's list starts at stage[ex] ...
-    d.run_info[d.ssorted[e]] = ((uint64_t)ex << kRunCountBits) | (uint64_t)v;  // ... = slot's run
-  }
-};
-// output order: queries in input order, lists concatenated (ResultSet CSR)
-struct QueryCntIn {
-  Dev d;
-  __device__ int64_t operator()(int64_t q) const {
-    const int k = d.nsub[q];
-    const int32_t s0 = d.qsbase[q];
-    int64_t c = 0;
-    for (int j = 0; j < k; ++j) c += slot_count(d, s0 + j);
-    return c;
-  }
-};
-
-__global__ void k_close_offsets(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  d.out_off[h->m] = h->R;
-  if (h->R != h->R_check) h->count_mismatch = 1;  // CountMismatch (bitmap.py:131-132)
-  if (h->R >= (int64_t(1) << (64 - kRunCountBits))) h->count_mismatch = 1;  // run_info packing bound
-}
-
-constexpr int kDecodeThreads = 256;
-constexpr int kDecodeBatch = 512;  // per-warp staging of 32 rows' decoded rows
-
-// Alg. 4 (decode.py:40-99, bitmap.py:122-133, engine.py:306-326) as warp
-// tasks over the join's work units (leaf, 32 intersecting subquery rows):
-// lane = row; the lane walks its row's words and, for every set bit
-// (ascending = block order), puts the object's input row at the row's next
-// position.  The 32 rows' lists are adjacent in `stage` (decode order), so
-// they are assembled in a per-warp shared-memory buffer and stored with
-// full-width coalesced writes.  No block barriers: warps are independent.
-__global__ void __launch_bounds__(kDecodeThreads) k_decode_rows(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  __shared__ int32_t sbatch[kDecodeThreads / 32][kDecodeBatch];
-  const int64_t U = h->U, S = h->S, R = h->R;
-  const int lane = lane_id(), wp = threadIdx.x >> 5;
-  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  int32_t* wbuf = sbatch[wp];
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < U; u += nwarp) {
-    const int64_t r = d.unit_leaf[u];
-    const int nobj = d.leaf_nobj[r], ni = d.leaf_nisq[r];
-    const int nb = (nobj + 31) >> 5;
-    const int n_ot = (nb + kOTB - 1) / kOTB;
-    const int lu = (int)(u - d.leaf_ubase[r]);
-    const int st = lu / n_ot, ot = lu - st * n_ot;
-    if (ot != 0) continue;  // one decode task per 32-row chunk (all object tiles at once)
-    const int r0 = st * kST, nrow = min(32, ni - r0);
-    const int32_t sb = d.leaf_sbase[r];
-    const int32_t* ids = d.sidx + d.leaf_obase[r];  // input rows of the leaf's objects (block order)
-    const bool live = lane < nrow;
-    const int64_t e = (int64_t)sb + r0 + lane;
-    const int64_t off = live ? d.slot_out[e] : 0;
-    const int64_t base = __shfl_sync(0xffffffffu, off, 0);
-    const int64_t e_end = (int64_t)sb + r0 + nrow;
-    const int64_t end = e_end < S ? d.slot_out[e_end] : R;
-    const int64_t total = end - base;
-    const bool buffered = total <= kDecodeBatch;
-    if (live) {
-      const uint32_t* words = d.bitmap + d.leaf_woff[r] + (int64_t)(r0 + lane) * nb;
-      if (buffered) {
-        int32_t* dst = wbuf + (off - base);  // shared memory
-        for (int b = 0; b < nb; ++b) {
-          uint32_t w = words[b];
-          while (w) {
-            const int bit = __ffs(w) - 1;
-            w &= w - 1;
-            *dst++ = ids[b * 32 + bit];
+    __syncthreads();
+    const uint32_t divm = (65536u + (uint32_t)nbt - 1u) / (uint32_t)nbt;  // it / nbt for it < 4096
+    // ---- subquery chunks ------------------------------------------------------
+    for (int c0 = 0; c0 < nisq; c0 += kQC) {
+      const int nq = min(kQC, nisq - c0);
+      if (tid < nq) {
+        const Rect4 R = d.erect[sbase + c0 + tid];
+        S.rect[tid] = R;
+        S.cnt[tid] = 0;
+        if (table)
+          S.kb[tid] = make_ushort4((unsigned short)bucket_bound(R.xa, basex, topx, scx),
+                                   (unsigned short)bucket_bound(R.xb, basex, topx, scx),
+                                   (unsigned short)bucket_bound(R.ya, basey, topy, scy),
+                                   (unsigned short)bucket_bound(R.yb, basey, topy, scy));
+      }
+      __syncthreads();
+      uint32_t* out = d.bitmap + woff + (int64_t)c0 * nb + b0;
+      if (table) {
+        const uint32_t* TX = S.tab;
+        const uint32_t* TY = S.tab + kRows * nbt;
+        const int items = nq * nbt;
+        for (int it = tid; it < items; it += kJT) {
+          const int s = (int)(((uint32_t)it * divm) >> 16), b = it - s * nbt;
+          const ushort4 k4 = S.kb[s];
+          const uint32_t xa0 = TX[k4.x * nbt + b], xa1 = TX[(k4.x + 1) * nbt + b];
+          const uint32_t xb0 = TX[k4.y * nbt + b], xb1 = TX[(k4.y + 1) * nbt + b];
+          const uint32_t ya0 = TY[k4.z * nbt + b], ya1 = TY[(k4.z + 1) * nbt + b];
+          const uint32_t yb0 = TY[k4.w * nbt + b], yb1 = TY[(k4.w + 1) * nbt + b];
+          uint32_t D = (xb0 & ~xa1) & (yb0 & ~ya1);
+          uint32_t A = (xb1 & ~xa0) & (yb1 & ~ya0) & ~D;
+          if (A) {
+            const Rect4 R = S.rect[s];
+            do {
+              const int bit = __ffs(A) - 1;
+              A &= A - 1;
+              const int o = (b << 5) + bit;
+              if (in_rect(S.ox[o], S.oy[o], R)) D |= 1u << bit;
+            } while (A);
           }
+          out[(int64_t)s * nb + b] = D;
+          if (D) atomicAdd(&S.cnt[s], __popc(D));
         }
       } else {
-        int32_t* dst = d.stage + off;  // global
-        for (int b = 0; b < nb; ++b) {
-          uint32_t w = words[b];
-          while (w) {
-            const int bit = __ffs(w) - 1;
-            w &= w - 1;
-            *dst++ = ids[b * 32 + bit];
+        // direct: lane = subquery, 32 objects of one block per step
+        const int nsc = (nq + 31) >> 5;
+        for (int it = wp; it < nsc * nbt; it += kJW) {
+          const int sc = it / nbt, b = it - sc * nbt;
+          const int s = sc * 32 + lane;
+          Rect4 R;
+          R.xa = R.ya = __longlong_as_double(0x7ff0000000000000ll);  // +inf: empty rect
+          R.xb = R.yb = __longlong_as_double((long long)0xfff0000000000000ull);
+          if (s < nq) R = S.rect[s];
+          uint32_t w = 0;
+#pragma unroll 8
+          for (int k = 0; k < 32; ++k) {
+            const int o = (b << 5) + k;
+            if (in_rect(S.ox[o], S.oy[o], R)) w |= 1u << k;
+          }
+          if (s < nq) {
+            out[(int64_t)s * nb + b] = w;
+            if (w) atomicAdd(&S.cnt[s], __popc(w));
           }
         }
       }
+      __syncthreads();
+      if (tid < nq) {
+        int32_t* ec = d.ecount + sbase + c0 + tid;
+        if (n_ot == 1) *ec = S.cnt[tid];
+        else atomicAdd(ec, S.cnt[tid]);
+      }
+      __syncthreads();
     }
-    __syncwarp();
-    if (buffered)
-      for (int k = lane; k < (int)total; k += 32) d.stage[base + k] = wbuf[k];
-    __syncwarp();
   }
 }
 
-// covering subqueries copy the whole block (decode.py:83-99), a warp per leaf
-__global__ void __launch_bounds__(256) k_decode_cov(const Dev d) {
+// ===========================================================================
+// K4: result offsets, decode straight into the canonical per-query lists
+// ===========================================================================
+// Subquery slots are grouped per query in query input order (k_query_fill),
+// so one exclusive scan of the per-slot result counts in slot order gives
+// every run's position in the output CSR, and at a query's first slot the
+// query's CSR offset: a query's list is its runs, merged (decode.py:102-123).
+// Result counts: an intersecting subquery contributes its popcount (written
+// per slot by the join), a covering one its leaf's whole block
+// (decode.py:83-99).
+__global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const int lane = lane_id();
@@ -987,309 +1007,255 @@ __global__ void __launch_bounds__(256) k_decode_cov(const Dev d) {
   for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < h->L; r += nwarp) {
     const int nc = d.leaf_ncov[r];
     if (nc == 0 || !leaf_on(d.leaf_active, r)) continue;
-    const int nobj = d.leaf_nobj[r];
-    if (nobj == 0) continue;
-    const int32_t* ids = d.sidx + d.leaf_obase[r];
-    const int32_t e0 = d.leaf_sbase[r] + d.leaf_nisq[r];
-    for (int c = 0; c < nc; ++c) {
-      int32_t* dst = d.stage + d.slot_out[e0 + c];
-      for (int k = lane; k < nobj; k += 32) dst[k] = ids[k];
-    }
+    const int32_t base = d.leaf_sbase[r] + d.leaf_nisq[r];
+    const int32_t nobj = d.leaf_nobj[r];
+    for (int c = lane; c < nc; c += 32) d.ecount[base + c] = nobj;
     if (lane == 0) covres += (unsigned long long)nobj * nc;
   }
   if (lane == 0 && covres) atomicAdd(&h->cov_results, covres);
 }
 
-
-// Per-query canonical lists (decode.py:102-123: concatenate, sort, reject
-// duplicates), assembled from the decoded runs (input rows, int32) into the
-// output CSR (object ids, int64), written in query order.  Monotone ids (ids
-// increase with input row — every generated workload): each run is sorted by
-// row, so sorting by row sorts by id; one run is a copy, two runs a merge-path
-// merge in registers, more runs a register bitonic sort; ids are looked up
-// (ids[row]) at the final store.  Otherwise rows are turned into ids first and
-// sorted by id, with a duplicate check.  Lists longer than 64 (or > 32 runs)
-// are concatenated into the output and queued for the CTA-wide k_merge_big.
-template <typename T>
-__device__ __forceinline__ T bitonic_step(T v, int i, int j, int k) {
-  const T o = __shfl_xor_sync(0xffffffffu, v, j);
-  const bool up = (i & k) == 0, low = (i & j) == 0;
-  return (low == up) ? (o < v ? o : v) : (o > v ? o : v);
-}
-// ascending bitonic sort of 32 (r = 1) or 64 (r = 2, index = reg*32 + lane) keys in registers
-template <typename T, int NR>
-__device__ __forceinline__ void warp_sort(T (&v)[2]) {
-  const int lane = lane_id();
-#pragma unroll
-  for (int k = 2; k <= 32 * NR; k <<= 1)
-#pragma unroll
-    for (int j = k >> 1; j > 0; j >>= 1) {
-      if (j == 32) {  // partner is the other register of the same lane (k == 64: ascending)
-        const T lo = v[0] < v[1] ? v[0] : v[1], hi = v[0] < v[1] ? v[1] : v[0];
-        v[0] = lo;
-        v[1] = hi;
-      } else {
-#pragma unroll
-        for (int r = 0; r < NR; ++r) v[r] = bitonic_step(v[r], r * 32 + lane, j, k);
-      }
-    }
-}
-
-// value at concatenated index t (reg t/32, lane t%32)
-template <int NR>
-__device__ __forceinline__ int32_t vget(const int32_t (&v)[2], int t) {
-  const int32_t a = __shfl_sync(0xffffffffu, v[0], t & 31);
-  if (NR == 1) return a;
-  const int32_t b = __shfl_sync(0xffffffffu, v[1], t & 31);
-  return t < 32 ? a : b;
-}
-
-// merge path of two sorted runs A = [0, na), B = [na, cnt) held in registers:
-// output position p takes min(A[i], B[p-i]) at the split i found by binary search
-template <int NR>
-__device__ __forceinline__ void warp_merge2(const int32_t (&v)[2], int na, int cnt, int32_t (&o)[2]) {
-  const int lane = lane_id();
-  const int nb = cnt - na;
-#pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const int p = r * 32 + lane;
-    int lo = p - nb > 0 ? p - nb : 0, hi = p < na ? p : na;
-    if (p >= cnt) lo = hi = 0;
-    while (__any_sync(0xffffffffu, lo < hi)) {
-      const int mid = (lo + hi) >> 1;
-      const int ia = mid, ib = na + p - mid - 1;
-      const int32_t va = vget<NR>(v, ia < 63 ? ia : 63);
-      const int32_t vb = vget<NR>(v, ib > 0 ? (ib < 63 ? ib : 63) : 0);
-      if (lo < hi) {
-        if (va < vb) lo = mid + 1; else hi = mid;
-      }
-    }
-    const int i = lo, j = p - lo;
-    const int32_t ai = vget<NR>(v, i < na ? i : 0);
-    const int32_t bj = vget<NR>(v, j < nb ? na + j : 0);
-    o[r] = (j >= nb || (i < na && ai < bj)) ? ai : bj;
-  }
-}
-
-__global__ void __launch_bounds__(256) k_assemble(const Dev d) {
+// per-slot result counts in slot (= output) order
+__global__ void __launch_bounds__(256) k_slot_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  const bool mono = !h->not_monotone;
+  TJ_GRID_STRIDE(s, h->S) d.sq_count[s] = d.ecount[d.sinv[s]];
+}
+
+__global__ void k_close_offsets(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  d.slot_off[h->S] = h->R;
+  d.out_off[h->m] = h->R;
+}
+
+constexpr int32_t kRowEnd = 0x7fffffff;
+
+constexpr int kDQThreads = 128;
+constexpr int kDQWarps = kDQThreads / 32;
+constexpr int kDQStage = 1024;   // results staged per warp window
+constexpr int kLaneRuns = 4;     // lane-per-query k-way merge up to this many runs
+
+// Per-query decode + merge (Alg. 4 and merge_results, decode.py:40-123).
+// A warp owns 32 consecutive queries; their lists are adjacent in the output
+// (and so are their subquery slots), so it cuts them into windows of at most
+// kDQStage results and, per window:
+//  A. decodes every slot's run into shared memory at its final position:
+//     the words of all the window's runs are flattened across the lanes
+//     (independent loads), and one running popcount prefix over them is the
+//     output position of every bit — runs are concatenated in slot order,
+//     which is output order;
+//  B. turns leaf positions into input rows with batched independent loads;
+//  C. per query (lane), merges its 2..4 runs by head (object ids increase
+//     with the input row) or copies its single run into a second buffer;
+//  D. stores the window with coalesced writes, ids looked up there.
+// Lists of one query larger than a window are concatenated in global memory
+// by the whole warp; lists that need a sort by id (ids not monotone, or more
+// than 4 runs) go to the CTA-wide k_merge_big.
+__global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  __shared__ int32_t sbuf[kDQWarps][kDQStage];
+  const bool mono = !h->not_monotone, ident = !h->not_identity;
   const int64_t m = h->m;
-  const int lane = lane_id();
+  const int lane = lane_id(), wp = threadIdx.x >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t* __restrict__ ids = d.ids;
-  const int32_t* __restrict__ stage = d.stage;
-  const bool ident = !h->not_identity;
+  const int32_t* __restrict__ sidx = d.sidx;
+  int32_t* sa = sbuf[wp];
+  int bad = 0;
   auto idof = [&](int32_t row) -> int64_t { return ident ? (int64_t)row : ids[row]; };
-  for (int64_t q0 = gw * 32; q0 < m; q0 += nwarp * 32) {
+  for (int64_t q0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; q0 < m; q0 += nwarp * 32) {
     const int64_t ql = q0 + lane;
-    int kl = 0;
-    int32_t s0l = 0;
-    int64_t qol = 0, cntl = 0;
+    int k = 0;
+    int32_t s0 = 0;
+    int64_t qo = 0, cnt = 0;
     if (ql < m) {
-      kl = d.nsub[ql];
-      s0l = d.qsbase[ql];
-      qol = d.out_off[ql];
-      cntl = d.out_off[ql + 1] - qol;
+      k = d.nsub[ql];
+      s0 = d.qsbase[ql];
+      qo = d.slot_off[s0];
+      cnt = d.slot_off[s0 + k] - qo;
+      d.out_off[ql] = qo;
     }
-    // single-run lists (sorted already when ids are monotone; length <= 1
-    // otherwise): flattened copy of the warp's output range — independent
-    // loads, coalesced stores
-    const bool single = kl == 1 && (mono || cntl <= 1);
-    const int64_t srcl = (single && cntl > 0) ? slot_off(d, s0l) : -1;
-    const bool done = kl == 0 || cntl == 0 || single;
-    {
-      const int64_t lo = __shfl_sync(0xffffffffu, qol, 0);
-      const int64_t hi = __shfl_sync(0xffffffffu, qol + cntl, 31);
-      const int64_t hi2 = q0 + 32 <= m ? hi : d.out_off[m];
-      const int nvalid = (int)min((int64_t)32, m - q0);
-      const uint32_t rel = lane < nvalid ? (uint32_t)(qol - lo) : 0xffffffffu;
-      constexpr int U = 4;  // 4 x 32 outputs per step: 4 independent loads in flight per lane
-      for (int64_t p0 = lo; p0 < hi2; p0 += 32 * U) {
-        int64_t src[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t pr = (uint32_t)(p0 - lo) + u * 32 + lane;
-          int j = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const uint32_t v = __shfl_sync(0xffffffffu, rel, j + step);
-            if (v <= pr) j += step;
+    const int nq = (int)min((int64_t)32, m - q0);
+    int l0 = 0;
+    while (l0 < nq) {
+      const int64_t base = __shfl_sync(0xffffffffu, qo, l0);
+      // window = lanes [l0, l1): the longest run of queries whose lists fit the stage
+      const unsigned fit = __ballot_sync(0xffffffffu, lane >= l0 && lane < nq && qo + cnt - base <= kDQStage);
+      int l1 = l0 + __popc(fit);
+      if (l1 == l0) {
+        // ---- one oversized list: the warp concatenates its runs in global memory
+        const int kq = __shfl_sync(0xffffffffu, k, l0);
+        const int32_t sq0 = __shfl_sync(0xffffffffu, s0, l0);
+        const int64_t cq = __shfl_sync(0xffffffffu, cnt, l0);
+        int64_t pos = base;
+        for (int j = 0; j < kq; ++j) {
+          const int32_t s = sq0 + j;
+          const int64_t cj = d.sq_count[s];
+          if (cj == 0) continue;
+          const int32_t leaf = d.sq_leaf[s];
+          const int4 li = d.linfo[leaf];
+          const int nobj = li.y;
+          const int32_t obase = li.x;
+          const int nbw = (nobj + 31) >> 5;
+          const int row = d.sinv[s] - li.z;
+          const bool cov = row >= li.w;
+          const uint32_t* wpt = cov ? nullptr : d.bitmap + d.leaf_woff[leaf] + (int64_t)row * nbw;
+          const uint32_t tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
+          int64_t got = 0;
+          for (int b0 = 0; b0 < nbw; b0 += 32) {
+            const int b = b0 + lane;
+            uint32_t w = b < nbw ? (cov ? (b == nbw - 1 ? tail : 0xffffffffu) : wpt[b]) : 0u;
+            const int c = __popc(w);
+            const int inc = warp_incl_scan(c);
+            int64_t p = pos + got + (inc - c);
+            while (w) {
+              const int bit = __ffs(w) - 1;
+              w &= w - 1;
+              d.out_ids[p++] = idof(sidx[obase + (b << 5) + bit]);
+            }
+            got += __shfl_sync(0xffffffffu, inc, 31);
           }
-          const uint32_t relj = __shfl_sync(0xffffffffu, rel, j);
-          const int64_t srcj = __shfl_sync(0xffffffffu, srcl, j);
-          src[u] = (p0 + u * 32 + lane < hi2 && srcj >= 0) ? srcj + (pr - relj) : -1;
+          bad |= (lane == 0) && (got != cj);  // CountMismatch (bitmap.py:131-132)
+          pos += cj;
         }
-        int32_t val[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) val[u] = src[u] >= 0 ? stage[src[u]] : 0;
-#pragma unroll
-        for (int u = 0; u < U; ++u)
-          if (src[u] >= 0) d.out_ids[p0 + u * 32 + lane] = idof(val[u]);
+        if (lane == 0 && cq > 1 && (kq > 1 || !mono)) {
+          const int idx = atomicAdd(&h->n_big, 1);
+          d.big_list[idx] = (int32_t)(q0 + l0);
+        }
+        l0 += 1;
+        continue;
       }
-    }
-    // monotone ids, 2..4 runs: lane-per-query k-way merge straight from the
-    // decoded runs (heads in registers, one-element lookahead per run); the
-    // 32 queries of the warp merge concurrently
-    const bool lanemerge = mono && !done && kl >= 2 && kl <= 4 && cntl <= 512;
-    if (__any_sync(0xffffffffu, lanemerge) && lanemerge) {
-      int64_t pos[4], end[4];
-      int32_t head[4];
-      int64_t acc = 0;
+      const bool act = lane >= l0 && lane < l1;
+      const int32_t slo = __shfl_sync(0xffffffffu, s0, l0);
+      const int32_t shi = __shfl_sync(0xffffffffu, s0 + k, l1 - 1);
+      const int64_t T = __shfl_sync(0xffffffffu, qo + cnt, l1 - 1) - base;
+      // ---- A: bits -> leaf positions, at their output positions in sa
+      for (int32_t c0 = slo; c0 < shi; c0 += 32) {
+        const int32_t s = c0 + lane;
+        int nbw = 0, obase = 0;
+        int64_t wof = -1;
+        uint32_t tail = 0;
+        if (s < shi && d.sq_count[s] > 0) {
+          const int32_t leaf = d.sq_leaf[s];
+          const int4 li = d.linfo[leaf];
+          const int nobj = li.y;
+          const int row = d.sinv[s] - li.z;
+          obase = li.x;
+          nbw = (nobj + 31) >> 5;
+          tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
+          wof = row >= li.w ? -1 : d.leaf_woff[leaf] + (int64_t)row * nbw;
+        }
+        const int winc = warp_incl_scan(nbw);
+        const int wexc = winc - nbw;
+        const int TW = __shfl_sync(0xffffffffu, winc, 31);
+        int64_t pos = d.slot_off[c0] - base;  // output offset of the chunk's first run
+        for (int t0 = 0; t0 < TW; t0 += 128) {
+          // four words per lane per step: independent loads in flight
+          uint32_t w[4];
+          int wo[4];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        pos[j] = 0;
-        end[j] = 0;
-        head[j] = 0x7fffffff;
-        if (j < kl) {
-          const int64_t c = slot_count(d, s0l + j);
-          pos[j] = slot_off(d, s0l + j);
-          end[j] = pos[j] + c;
-          acc += c;
-          if (c > 0) head[j] = stage[pos[j]];
+          for (int u = 0; u < 4; ++u) {
+            const int t = t0 + u * 32 + lane;
+            int j = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+              const int v = __shfl_sync(0xffffffffu, wexc, j + step);
+              if (v <= t) j += step;
+            }
+            const int jx = __shfl_sync(0xffffffffu, wexc, j);
+            const int jn = __shfl_sync(0xffffffffu, nbw, j);
+            const int jo = __shfl_sync(0xffffffffu, obase, j);
+            const int64_t jw = __shfl_sync(0xffffffffu, wof, j);
+            const uint32_t jt = __shfl_sync(0xffffffffu, tail, j);
+            const int wb = t - jx;
+            w[u] = 0;
+            if (t < TW) w[u] = jw >= 0 ? d.bitmap[jw + wb] : (wb == jn - 1 ? jt : 0xffffffffu);
+            wo[u] = jo + (wb << 5);
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            uint32_t x = w[u];
+            const int c = __popc(x);
+            const int inc = warp_incl_scan(c);
+            int p = (int)pos + (inc - c);
+            while (x) {
+              const int bit = __ffs(x) - 1;
+              x &= x - 1;
+              sa[p++] = wo[u] + bit;
+            }
+            pos += __shfl_sync(0xffffffffu, inc, 31);
+          }
+        }
+        // the runs' popcounts must add up to the counts the offsets came from
+        const int32_t cend = c0 + 32 < shi ? c0 + 32 : shi;
+        bad |= (lane == 0) && (pos != d.slot_off[cend] - base);  // CountMismatch (bitmap.py:131-132)
+      }
+      __syncwarp();
+      // ---- B: leaf positions -> input rows (independent loads, 4 in flight per lane)
+      for (int i0 = 0; i0 < (int)T; i0 += 128) {
+        int32_t v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * 32 + lane;
+          v[u] = i < (int)T ? sidx[sa[i]] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = i0 + u * 32 + lane;
+          if (i < (int)T) sa[i] = v[u];
         }
       }
-      int64_t* out = d.out_ids + qol;
-      for (int64_t o = 0; o < cntl; ++o) {
-        int bj = 0;
-        int32_t bv = head[0];
-#pragma unroll
-        for (int j = 1; j < 4; ++j)
-          if (head[j] < bv) {
-            bv = head[j];
-            bj = j;
+      __syncwarp();
+      // ---- C: store the window (runs concatenated; ids looked up here)
+      for (int i = lane; i < (int)T; i += 32) d.out_ids[base + i] = idof(sa[i]);
+      __syncwarp();
+      // ---- D: per query with 2..4 runs, merge the runs by head over the stored concatenation
+      if (act && cnt > 1) {
+        const int qs = (int)(qo - base);
+        if (!mono || k > kLaneRuns) {
+          if (k > 1 || !mono) {
+            const int idx = atomicAdd(&h->n_big, 1);
+            d.big_list[idx] = (int32_t)ql;
           }
-        out[o] = idof(bv);
+        } else if (k > 1) {
+          int pos[kLaneRuns], end[kLaneRuns];
+          int32_t head[kLaneRuns];
+          int acc = qs;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if (j == bj) {
-            ++pos[j];
-            head[j] = pos[j] < end[j] ? stage[pos[j]] : 0x7fffffff;
-            if (((pos[j] & 7) == 0) && pos[j] + 16 < end[j])  // pull the sector two ahead into L1
-              asm volatile("prefetch.global.L1 [%0];" ::"l"(stage + pos[j] + 16));
+          for (int j = 0; j < kLaneRuns; ++j) {
+            const int c = j < k ? d.sq_count[s0 + j] : 0;
+            pos[j] = acc;
+            end[j] = acc + c;
+            acc += c;
+            head[j] = c > 0 ? sa[pos[j]] : kRowEnd;
           }
+          int64_t* dst = d.out_ids + qo;
+          for (int o = 0; o < (int)cnt; ++o) {
+            int bj = 0;
+            int32_t bv = head[0];
+#pragma unroll
+            for (int j = 1; j < kLaneRuns; ++j)
+              if (head[j] < bv) {
+                bv = head[j];
+                bj = j;
+              }
+            dst[o] = idof(bv);
+#pragma unroll
+            for (int j = 0; j < kLaneRuns; ++j)
+              if (j == bj) {
+                ++pos[j];
+                head[j] = pos[j] < end[j] ? sa[pos[j]] : kRowEnd;
+              }
+          }
+        }
       }
-    }
-    // short multi-run lists (<= 64 entries, <= 32 runs): one query at a
-    // time, the next query's run metadata in flight meanwhile
-    const bool smallq = !done && !lanemerge && cntl <= 64 && kl <= 32;
-    unsigned pend = __ballot_sync(0xffffffffu, smallq);
-    {
-      auto meta = [&](int src, int64_t& c, int64_t& o) {
-        const int kk = __shfl_sync(0xffffffffu, kl, src);
-        const int32_t ss = __shfl_sync(0xffffffffu, s0l, src);
-        c = 0;
-        o = 0;
-        if (lane < kk) {
-          c = slot_count(d, ss + lane);
-          o = slot_off(d, ss + lane);
-        }
-      };
-      int cur = pend ? __ffs(pend) - 1 : -1;
-      pend &= pend - 1;
-      int64_t c_cur = 0, o_cur = 0;
-      if (cur >= 0) meta(cur, c_cur, o_cur);
-      while (cur >= 0) {
-        const int nxt = pend ? __ffs(pend) - 1 : -1;
-        pend &= pend - 1;
-        int64_t c_nxt = 0, o_nxt = 0;
-        if (nxt >= 0) meta(nxt, c_nxt, o_nxt);
-        const int k = __shfl_sync(0xffffffffu, kl, cur);
-        const int64_t qo = __shfl_sync(0xffffffffu, qol, cur);
-        const int cnt = (int)__shfl_sync(0xffffffffu, cntl, cur);
-        const int cinc = warp_incl_scan((int)c_cur);
-        const int cexc = cinc - (int)c_cur;
-        int32_t v[2];
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-          const int x = r * 32 + lane;
-          int jj = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int st = __shfl_sync(0xffffffffu, cexc, jj + step);
-            if (jj + step < k && st <= x) jj += step;
-          }
-          const int stj = __shfl_sync(0xffffffffu, cexc, jj);
-          const int64_t ofj = __shfl_sync(0xffffffffu, o_cur, jj);
-          v[r] = x < cnt ? stage[ofj + (x - stj)] : 0x7fffffff;
-        }
-        if (mono) {
-          int32_t o[2];
-          if (k == 2) {
-            const int na = __shfl_sync(0xffffffffu, (int)c_cur, 0);
-            if (cnt <= 32) warp_merge2<1>(v, na, cnt, o); else warp_merge2<2>(v, na, cnt, o);
-          } else {
-            if (cnt <= 32) warp_sort<int32_t, 1>(v); else warp_sort<int32_t, 2>(v);
-            o[0] = v[0];
-            o[1] = v[1];
-          }
-#pragma unroll
-          for (int r = 0; r < 2; ++r)
-            if (r * 32 + lane < cnt) d.out_ids[qo + r * 32 + lane] = idof(o[r]);
-        } else {
-          int64_t w[2];
-#pragma unroll
-          for (int r = 0; r < 2; ++r) w[r] = r * 32 + lane < cnt ? idof(v[r]) : (int64_t)0x7fffffffffffffffll;
-          if (cnt <= 32) warp_sort<int64_t, 1>(w); else warp_sort<int64_t, 2>(w);
-          int dup = 0;
-#pragma unroll
-          for (int r = 0; r < 2; ++r) {
-            const int x = r * 32 + lane;
-            if (x < cnt) d.out_ids[qo + x] = w[r];
-            // neighbour of x is x+1: next lane, or register 1 lane 0
-            const int64_t nb0 = __shfl_down_sync(0xffffffffu, w[r], 1);
-            const int64_t wrap = __shfl_sync(0xffffffffu, w[1], 0);
-            const int64_t nbv = lane < 31 ? nb0 : (r == 0 ? wrap : (int64_t)0x7fffffffffffffffll);
-            dup |= (x + 1 < cnt) && nbv == w[r];
-          }
-          if (__any_sync(0xffffffffu, dup) && lane == 0) h->dup = 1;
-        }
-        cur = nxt;
-        c_cur = c_nxt;
-        o_cur = o_nxt;
-      }
-    }
-    // long lists / many runs: concatenate the runs (as ids) into the output
-    // and queue the query for the CTA-wide sort
-    unsigned todo = __ballot_sync(0xffffffffu, !done && !smallq && !lanemerge);
-    while (todo) {
-      const int src_lane = __ffs(todo) - 1;
-      todo &= todo - 1;
-      const int k = __shfl_sync(0xffffffffu, kl, src_lane);
-      const int32_t s0 = __shfl_sync(0xffffffffu, s0l, src_lane);
-      const int64_t qo = __shfl_sync(0xffffffffu, qol, src_lane);
-      int64_t pre = 0;
-      for (int j0 = 0; j0 < k; j0 += 32) {
-        const int j = j0 + lane;
-        int64_t cj = 0, oj = 0;
-        if (j < k) {
-          cj = slot_count(d, s0 + j);
-          oj = slot_off(d, s0 + j);
-        }
-        const int64_t inc = warp_incl_scan(cj);
-        const int64_t seg = __shfl_sync(0xffffffffu, inc, 31);
-        for (int64_t x0 = 0; x0 < seg; x0 += 32) {  // flattened copy of these <= 32 runs
-          const int64_t x = x0 + lane;
-          int jj = 0;
-#pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int64_t v = __shfl_sync(0xffffffffu, inc - cj, jj + step);  // exclusive starts
-            if (v <= x && j0 + jj + step < k) jj += step;
-          }
-          const int64_t st_j = __shfl_sync(0xffffffffu, inc - cj, jj);
-          const int64_t of_j = __shfl_sync(0xffffffffu, oj, jj);
-          if (x < seg) d.out_ids[qo + pre + x] = idof(stage[of_j + (x - st_j)]);
-        }
-        pre += seg;
-      }
-      if (lane == 0) {
-        const int idx = atomicAdd(&h->n_big, 1);
-        d.big_list[idx] = (int32_t)(q0 + src_lane);
-      }
+      __syncwarp();
+      l0 = l1;
     }
   }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) h->count_mismatch = 1;
 }
 
 // ---------------------------------------------------------------------------
