@@ -45,7 +45,7 @@ struct tj_ctx {
   // queries
   DBuf crect, qwin, nsub, qsbase, biglist;
   // subqueries
-  DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, skey0, skey1, sval0, sval1, runs0, runs1, unitleaf;
+  DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, leafcur, unitleaf;
   // join / outputs
   DBuf bitmap, outids, outoff, scratch;
   // scan / radix scratch
@@ -63,7 +63,7 @@ struct tj_ctx {
   int64_t n = 0, m = 0;
   DevHdr last{};
   Dev dv{};
-  int obj_passes = 0, sq_passes = 0;
+  int obj_passes = 0;
   int shard_rank = 0, shard_n = 1;
   DBuf lactive, lwpre;
 };
@@ -170,10 +170,9 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(lwoff, c->cap_L * 8);
   ENS(linfo, c->cap_L * 16);
   ENS(lubase, c->cap_L * 8);
-  ENS(runs0, c->cap_L * 2 * 4);
+  ENS(leafcur, c->cap_L * 2 * 4);
   ENS(lactive, c->cap_L);
   ENS(lwpre, c->cap_L * 8);
-  ENS(runs1, c->cap_L * 2 * 4);
   ENS(crect, m * sizeof(Rect4));
   ENS(qwin, m * sizeof(int4));
   ENS(nsub, m * 4);
@@ -204,10 +203,6 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(ecount, c->cap_S * 4);
   ENS(sinv, c->cap_S * 4);
   ENS(slotoff, (c->cap_S + 1) * 8);
-  ENS(skey0, c->cap_S * 4);
-  ENS(skey1, c->cap_S * 4);
-  ENS(sval0, c->cap_S * 4);
-  ENS(sval1, c->cap_S * 4);
   ENS(bitmap, c->cap_W * 4);
   ENS(unitleaf, c->cap_U * 4);
   ENS(scratch, c->cap_R * 8);
@@ -263,20 +258,13 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.sinv = P<int32_t>(c->sinv);
   d.linfo = P<int4>(c->linfo);
   d.slot_off = P<int64_t>(c->slotoff);
-  d.skey[0] = P<uint32_t>(c->skey0);
-  d.skey[1] = P<uint32_t>(c->skey1);
-  d.sval[0] = P<int32_t>(c->sval0);
-  d.sval[1] = P<int32_t>(c->sval1);
   d.bitmap = P<uint32_t>(c->bitmap);
   d.out_ids = P<int64_t>(c->outids);
   d.out_off = P<int64_t>(c->outoff);
   d.D = lmax - F;
   d.SUB = sub_size(d.D);
   d.sidx = d.oval[c->obj_passes & 1];
-  d.ssorted = d.sval[c->sq_passes & 1];
-  d.skey_sorted = d.skey[c->sq_passes & 1];
-  d.run_start = P<int32_t>(c->runs0);
-  d.run_end = P<int32_t>(c->runs1);
+  d.leaf_cur = P<int32_t>(c->leafcur);
   d.unit_leaf = P<int32_t>(c->unitleaf);
   d.big_list = P<int32_t>(c->biglist);
   d.leaf_active = c->shard_n > 1 ? P<uint8_t>(c->lactive) : nullptr;
@@ -314,8 +302,9 @@ int launch_tick(tj_ctx* c) {
   ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
 
   cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
-  cudaMemsetAsync(d.run_start, 0, c->cap_L * 2 * 4, st);
-  cudaMemsetAsync(d.run_end, 0, c->cap_L * 2 * 4, st);
+  cudaMemsetAsync(d.leaf_cur, 0, c->cap_L * 2 * 4, st);
+  cudaMemsetAsync(d.leaf_nisq, 0, c->cap_L * 4, st);
+  cudaMemsetAsync(d.leaf_ncov, 0, c->cap_L * 4, st);
 
   cudaEventRecord(c->ev[0], st);
   // ---- K0 / K1: index build -------------------------------------------
@@ -333,7 +322,7 @@ int launch_tick(tj_ctx* c) {
   k_finalize_index<<<1, 1, 0, st>>>(h);
   k_cell_level<<<Gbig, 256, 0, st>>>(d);
   scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
-  k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, kRadixBits * c->sq_passes);
+  k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
   k_obj_keys<<<Gn, 256, 0, st>>>(d);
   radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
   scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr, st);
@@ -344,12 +333,10 @@ int launch_tick(tj_ctx* c) {
   k_query_count<<<Gm, 256, 0, st>>>(d);
   scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
   k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
+  scan_launch(sp, LeafSqIn{d.leaf_nisq, d.leaf_ncov}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h, (int64_t*)nullptr,
+              st);
   k_query_fill<<<Gm, 256, 0, st>>>(d);
-  radix_sort(c, d.skey, d.sval, &h->S, c->sq_passes);
-  k_sq_runs<<<Gbig, 256, 0, st>>>(d);
   k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
-  k_entries<<<Gbig, 256, 0, st>>>(d);
-  k_sinv<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[1], st);
   int extra = 0;
   if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range
@@ -380,8 +367,8 @@ int launch_tick(tj_ctx* c) {
   k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[5], st);
   // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-  const int scans = 6, singles = 28 + F + (D > 0 ? 3 + (D - 1) : 0);
-  return 3 * scans + 5 * (c->obj_passes + c->sq_passes) + singles + extra;
+  const int scans = 7, singles = 25 + F + (D > 0 ? 3 + (D - 1) : 0);
+  return 3 * scans + 5 * c->obj_passes + singles + extra + 3;  // + 3 memsets
 }
 
 void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
@@ -479,8 +466,7 @@ int tj_destroy(tj_ctx* c) {
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
-                 &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->skey0, &c->skey1, &c->sval0, &c->sval1, &c->runs0,
-                 &c->runs1, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
+                 &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->partial, &c->rhist, &c->roffs};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
@@ -550,7 +536,6 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     if ((rc = prepare_static(c, n, m))) return rc;
     if (c->last_L == 0) c->last_L = c->cap_L;
     c->obj_passes = passes_for(std::max<int64_t>(c->last_L + c->last_L / 2, 1) - 1);
-    c->sq_passes = passes_for(2 * (c->last_L + c->last_L / 2) - 1);
     bool done = false;
     for (int attempt = 0; attempt < 8 && !done; ++attempt) {
       if ((rc = prepare_dynamic(c))) return rc;
@@ -570,7 +555,6 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       if (H.abort & (8 | 16)) return fail(c, TJ_E_CUDA, "internal capacity bound violated (heavy/leaves)");
       if (H.abort & 32) {
         c->obj_passes = passes_for(H.L - 1);
-        c->sq_passes = passes_for(2 * H.L - 1);
       }
       if (H.abort & 1) c->cap_S = std::max<int64_t>(2 * c->cap_S, H.S + H.S / 4 + 256);
       if (H.abort & 2) {
@@ -688,6 +672,24 @@ int load_leaves(tj_ctx* c, LeafView& lv) {
   return TJ_OK;
 }
 
+// Directory entries of leaf r's block [e0, e0 + cnt) in the reference's
+// order (ascending slot = query input order, directory.py:131): the device
+// keeps fill order inside a block; entry -> slot is the inverse of sinv.
+int entry_slots(tj_ctx* c, std::vector<int32_t>& eslot) {
+  std::vector<int32_t> sinv;
+  int rc;
+  if ((rc = d2h(c, sinv, c->sinv.p, c->last.S))) return rc;
+  eslot.assign(sinv.size(), -1);
+  for (size_t s = 0; s < sinv.size(); ++s) eslot[sinv[s]] = (int32_t)s;
+  return TJ_OK;
+}
+std::vector<int32_t> block_in_ref_order(const std::vector<int32_t>& eslot, int64_t e0, int64_t cnt) {
+  std::vector<int32_t> es((size_t)cnt);
+  for (int64_t j = 0; j < cnt; ++j) es[j] = (int32_t)(e0 + j);
+  std::sort(es.begin(), es.end(), [&](int32_t x, int32_t y) { return eslot[x] < eslot[y]; });
+  return es;
+}
+
 int need_tick(tj_ctx* c) {
   if (!c) return TJ_E_INVALID_ARG;
   if (!c->have) return fail(c, TJ_E_INVALID_ARG, "no completed tick with objects to introspect");
@@ -786,14 +788,14 @@ int tj_get_directory(tj_ctx* c, int64_t* obj_rows, int64_t obj_cap, int64_t* isq
   }
   if (isq || cov) {
     if (sq_cap < (int64_t)std::max(H.sum_isq, H.sum_cov)) return fail(c, TJ_E_INVALID_ARG, "sq buffers too small");
-    std::vector<int32_t> ss;
-    if ((rc = d2h(c, ss, c->dv.ssorted, H.S))) return rc;
+    std::vector<int32_t> eslot;
+    if ((rc = entry_slots(c, eslot))) return rc;
     int64_t ki = 0, kc = 0;
     for (int64_t r : lv.order) {
-      for (int32_t j = 0; j < lv.nisq[r]; ++j)
-        if (isq) isq[ki++] = ss[lv.sbase[r] + j];
-      for (int32_t j = 0; j < lv.ncov[r]; ++j)
-        if (cov) cov[kc++] = ss[lv.sbase[r] + lv.nisq[r] + j];
+      if (isq)
+        for (int32_t e : block_in_ref_order(eslot, lv.sbase[r], lv.nisq[r])) isq[ki++] = eslot[e];
+      if (cov)
+        for (int32_t e : block_in_ref_order(eslot, lv.sbase[r] + lv.nisq[r], lv.ncov[r])) cov[kc++] = eslot[e];
     }
   }
   return TJ_OK;
@@ -812,8 +814,9 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
   std::vector<uint32_t> bm;
-  std::vector<int32_t> info;
-  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, info, c->ecount.p, H.S)))
+  std::vector<int32_t> info, eslot;
+  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, info, c->ecount.p, H.S)) ||
+      (rc = entry_slots(c, eslot)))
     return rc;
   int64_t t = 0, w = 0, k = 0;
   if (task_woff) task_woff[0] = 0;
@@ -824,10 +827,14 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
     if (task_cell) task_cell[t] = lv.packed[r];
     if (task_nobj) task_nobj[t] = no;
     if (task_nisq) task_nisq[t] = ni;
-    if (words) std::memcpy(words + w, bm.data() + lv.woff[r], nw * 4);
+    const int64_t nb = (no + 31) / 32;
+    const std::vector<int32_t> rows = block_in_ref_order(eslot, lv.sbase[r], ni);
+    if (words)
+      for (int64_t j = 0; j < ni; ++j)
+        std::memcpy(words + w + j * nb, bm.data() + lv.woff[r] + (rows[j] - lv.sbase[r]) * nb, nb * 4);
     if (counts) {
       if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
-      for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)info[lv.sbase[r] + j];
+      for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)info[rows[j]];
     }
     w += nw;
     k += ni;

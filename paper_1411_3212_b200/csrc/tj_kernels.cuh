@@ -68,15 +68,10 @@ struct Dev {
   int32_t* sq_count;        // result count per subquery slot (popcount, or block size if covering)
   int32_t* ecount;          // result count per directory entry (entry order)
   Rect4* erect;             // clipped rect per directory entry (entry order, the join's input)
-  int32_t* sinv;            // per slot: its directory entry (inverse of ssorted)
+  int32_t* sinv;            // per slot: its directory entry
   int4* linfo;              // per leaf: object base, object count, entry base, intersecting count
   int64_t* slot_off;        // per slot (S + 1): start of its run in the output CSR
-  uint32_t* skey[2];
-  int32_t* sval[2];
-  const int32_t* ssorted;  // per leaf [isq slots asc][cov slots asc]
-  const uint32_t* skey_sorted;
-  int32_t* run_start;      // per subquery key (2*leaf + covering): first sorted position
-  int32_t* run_end;        // one past the last
+  int32_t* leaf_cur;       // per leaf x {intersecting, covering}: fill cursor
   int32_t* unit_leaf;      // join work unit -> leaf
   uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
   int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
@@ -492,7 +487,33 @@ __device__ __forceinline__ int enum_small(const int4 w, int ld, const uint32_t* 
 }
 #undef TJ_CSWAP
 
+// Covering flag with the reference's exact op order (quadtree.py:219-231):
+// w = width / 2^level; lxa = xa + li*w; covering iff qxa <= lxa and
+// qxb >= min(lxa + w, mbr.xb), likewise in y.
+__device__ __forceinline__ bool covers(const Rect4& q, int lev, uint32_t z, const DevHdr* h) {
+  const double side = (double)(1u << lev);
+  const double w = __ddiv_rn(h->width, side);
+  const double hh = __ddiv_rn(h->height, side);
+  const double li = (double)compact2(z), lj = (double)compact2(z >> 1);
+  const double lxa = __dadd_rn(h->xa, __dmul_rn(li, w));
+  const double lya = __dadd_rn(h->ya, __dmul_rn(lj, hh));
+  double ux = __dadd_rn(lxa, w);
+  ux = ux < h->xb ? ux : h->xb;
+  double uy = __dadd_rn(lya, hh);
+  uy = uy < h->yb ? uy : h->yb;
+  return (q.xa <= lxa) && (q.xb >= ux) && (q.ya <= lya) && (q.yb >= uy);
+}
+
+// a (query, leaf) pair found by the count pass: the leaf's intersecting /
+// covering directory block grows by one (counting sort by leaf, no radix sort)
+__device__ __forceinline__ void count_pair(const Dev& d, int lev, uint32_t z, uint32_t rank, const Rect4& r,
+                                           int cov_on) {
+  const bool cv = cov_on && covers(r, lev, z, d.h);
+  atomicAdd(cv ? &d.leaf_ncov[rank] : &d.leaf_nisq[rank], 1);
+}
+
 // clip (geometry.py:80-88), window (quadtree.py:182-183), count subqueries
+// per query and (query, leaf) pairs per leaf block
 __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
@@ -501,6 +522,7 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
   const double sx = h->sx_deep, sy = h->sy_deep;
   const int wpos = h->wpos, hpos = h->hpos, ld = h->l_deep;
   const uint32_t side = 1u << ld;
+  const int cov_on = h->covering;
   TJ_GRID_STRIDE(q, m) {
     double cxa = d.qxa[q], cya = d.qya[q], cxb = d.qxb[q], cyb = d.qyb[q];
     cxa = cxa < xa ? xa : cxa;  // max(q.xa, mbr.xa)
@@ -520,30 +542,17 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
       if (is_small(w)) {
         uint32_t key[4], rank[4];
         cnt = enum_small(w, ld, d.zmap, key, rank);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (k < cnt) count_pair(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, rank[k], r, cov_on);
       } else {
-        cnt = enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [](int, uint32_t, uint32_t) {});
+        cnt = enum_window(w.x, w.y, w.z, w.w, ld, d.zmap,
+                          [&](int lev, uint32_t z, uint32_t rank) { count_pair(d, lev, z, rank, r, cov_on); });
       }
     }
     d.qwin[q] = w;
     d.nsub[q] = cnt;
   }
-}
-
-// Covering flag with the reference's exact op order (quadtree.py:219-231):
-// w = width / 2^level; lxa = xa + li*w; covering iff qxa <= lxa and
-// qxb >= min(lxa + w, mbr.xb), likewise in y.
-__device__ __forceinline__ bool covers(const Rect4& q, int lev, uint32_t z, const DevHdr* h) {
-  const double side = (double)(1u << lev);
-  const double w = __ddiv_rn(h->width, side);
-  const double hh = __ddiv_rn(h->height, side);
-  const double li = (double)compact2(z), lj = (double)compact2(z >> 1);
-  const double lxa = __dadd_rn(h->xa, __dmul_rn(li, w));
-  const double lya = __dadd_rn(h->ya, __dmul_rn(lj, hh));
-  double ux = __dadd_rn(lxa, w);
-  ux = ux < h->xb ? ux : h->xb;
-  double uy = __dadd_rn(lya, hh);
-  uy = uy < h->yb ? uy : h->yb;
-  return (q.xa <= lxa) && (q.xb >= ux) && (q.ya <= lya) && (q.yb >= uy);
 }
 
 // Subquery flags: bit 0 covering, bit 1 the query has a single subquery
@@ -556,10 +565,14 @@ __device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, int64_
   d.sq_leaf[slot] = (int32_t)rank;
   d.sq_q[slot] = (int32_t)q;
   d.sq_cov[slot] = (uint8_t)((cv ? kFlagCov : 0) | (n == 1 ? kFlagSingle : 0));
-  // radix key = 2*leaf + covering: per leaf, intersecting subqueries then
-  // covering ones, each in slot (= query input) order — directory.py:131
-  d.skey[0][slot] = 2u * rank + (cv ? 1u : 0u);
-  d.sval[0][slot] = slot;
+  // directory entry: the leaf's intersecting block, then its covering block
+  // (directory.py:131-142); within a block, entries take fill order — the
+  // join and decode are invariant to it, and the introspection entry points
+  // return the reference's query order
+  const int32_t e = d.leaf_sbase[rank] + (cv ? d.leaf_nisq[rank] : 0) +
+                    atomicAdd(&d.leaf_cur[2 * rank + (cv ? 1 : 0)], 1);
+  d.sinv[slot] = e;
+  d.erect[e] = r;  // the join's input, in entry order
 }
 
 // Fill: per query, subqueries in ascending packed (level, z) order — the
@@ -604,34 +617,6 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   }
 }
 
-// Run boundaries of the sorted subquery keys give every leaf's intersecting
-// and covering block (directory.py:137-142) without atomics.
-__global__ void __launch_bounds__(256) k_sq_runs(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  const int64_t S = h->S;
-  const uint32_t* ks = d.skey_sorted;
-  TJ_GRID_STRIDE(e, S) {
-    const uint32_t k = ks[e];
-    if (e == 0 || ks[e - 1] != k) d.run_start[k] = (int32_t)e;
-    if (e == S - 1 || ks[e + 1] != k) d.run_end[k] = (int32_t)(e + 1);
-  }
-}
-
-// Directory in entry order for the join: the clipped rect of every entry's
-// query (one random 32-byte read per entry, fully parallel), and the inverse
-// permutation slot -> entry for the query-order decode.
-__global__ void __launch_bounds__(256) k_entries(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  TJ_GRID_STRIDE(e, h->S) d.erect[e] = d.crect[d.sq_q[d.ssorted[e]]];
-}
-__global__ void __launch_bounds__(256) k_sinv(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  TJ_GRID_STRIDE(e, h->S) d.sinv[d.ssorted[e]] = (int32_t)e;
-}
-
 // per-leaf occupancy / task statistics (engine.py:212-225,261-267)
 __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
   DevHdr* h = d.h;
@@ -639,16 +624,12 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
   const int64_t L = h->L;
   unsigned long long act = 0, s1 = 0, s2 = 0, tasks = 0, tests = 0, si = 0, sc = 0, pa = 0, sa = 0;
   TJ_GRID_STRIDE(r, L) {
-    const int32_t a0 = d.run_start[2 * r], a1 = d.run_end[2 * r];
-    const int32_t c0 = d.run_start[2 * r + 1], c1 = d.run_end[2 * r + 1];
-    d.leaf_nisq[r] = a1 - a0;
-    d.leaf_ncov[r] = c1 - c0;
-    d.leaf_sbase[r] = (a1 > a0) ? a0 : c0;
-    d.linfo[r] = make_int4(d.leaf_obase[r], d.leaf_nobj[r], (a1 > a0) ? a0 : c0, a1 - a0);
+    const int32_t nisq = d.leaf_nisq[r], ncov = d.leaf_ncov[r];
+    d.linfo[r] = make_int4(d.leaf_obase[r], d.leaf_nobj[r], d.leaf_sbase[r], nisq);
     const unsigned long long no = (unsigned long long)d.leaf_nobj[r];
-    const unsigned long long ni = (unsigned long long)(a1 - a0);
+    const unsigned long long ni = (unsigned long long)nisq;
     si += ni;
-    sc += (unsigned long long)(c1 - c0);
+    sc += (unsigned long long)ncov;
     if (no) {
       act += 1;
       s1 += no;
@@ -737,6 +718,13 @@ struct UnitsIn {
     const int64_t nb = (no + 31) / 32;
     return (nb + kTileBlocks - 1) / kTileBlocks;
   }
+};
+
+// directory blocks: per leaf, intersecting entries then covering entries
+struct LeafSqIn {
+  const int32_t* nisq;
+  const int32_t* ncov;
+  __device__ int64_t operator()(int64_t r) const { return (int64_t)nisq[r] + ncov[r]; }
 };
 
 // Multi-GPU leaf-range sharding: every rank builds the same
