@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -354,7 +355,7 @@ int launch_tick(tj_ctx* c) {
   k_unit_map<<<Gbig, 256, 0, st>>>(d);
   k_zero_counts<<<Gbig, 256, 0, st>>>(d);
   cudaEventRecord(c->ev[2], st);
-  k_join<<<c->num_sms * 4, kJT, sizeof(JoinSmem), st>>>(d);
+  k_join<<<c->num_sms * 5, kJT, sizeof(JoinSmem), st>>>(d);
   cudaEventRecord(c->ev[3], st);
   // ---- K4: decode + canonical lists --------------------------------------
   k_cov_counts<<<Gbig, 256, 0, st>>>(d);
@@ -391,6 +392,8 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.l_deep = 1;
   H.shard_rank = c->shard_rank;
   H.shard_n = c->shard_n;
+  const char* dbg = std::getenv("TJ_DEBUG");
+  H.dbg = dbg ? std::atoi(dbg) : 0;
 }
 
 int passes_for(int64_t maxkey) { return std::max(1, (bits_for(maxkey) + kRadixBits - 1) / kRadixBits); }
@@ -452,6 +455,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
+
   int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
   *out = c;

@@ -51,6 +51,7 @@ struct DevHdr {
   int32_t oob;              // OutOfBounds (adaptive reuse: object outside old MBR)
   int32_t count_mismatch;   // CountMismatch
   int32_t n_big;            // queries queued for k_merge_big
+  int32_t dbg;              // experiment switches (TJ_DEBUG env), 0 in production
   unsigned long long overfull2, overfull8;  // needs_rebuild counters
   int32_t shard_rank, shard_n;              // leaf-range sharding (n == 1: off)
   int64_t shard_total;                      // total leaf work weight

@@ -690,11 +690,11 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
 // test.  Bit-identical to the direct test by construction.
 constexpr int kJT = 256;                      // join CTA threads
 constexpr int kJW = kJT / 32;
-constexpr int kTileBlocks = 16;               // object tile: 16 blocks = 512 objects
+constexpr int kTileBlocks = 12;               // object tile: 12 blocks = 384 objects (th_quad)
 constexpr int kTileObj = kTileBlocks * 32;
 constexpr int kNK = 256;                      // buckets per axis
-constexpr int kRows = kNK + 3;                // prefix rows k = 0 .. kNK + 2
-constexpr int kQC = 256;                      // subqueries per chunk
+constexpr int kRows = kNK + 2;                // prefix rows k = 0 .. kNK + 1
+constexpr int kQC = 512;                      // subqueries per chunk
 constexpr int kTableMinQ = 12;                // table path from this many subqueries
 
 __device__ __forceinline__ bool leaf_on(const uint8_t* active, int64_t r) { return !active || active[r]; }
@@ -775,24 +775,22 @@ __global__ void __launch_bounds__(256) k_zero_counts(const Dev d) {
 }
 
 struct JoinSmem {
-  double ox[kTileObj];                  // tile objects (NaN padding never matches)
+  double ox[kTileObj];                    // tile objects (NaN padding never matches)
   double oy[kTileObj];
   uint32_t tab[2 * kRows * kTileBlocks];  // [axis][k][b], row stride = tile blocks
-  Rect4 rect[kQC];                      // clipped rects of the chunk's subqueries
-  ushort4 kb[kQC];                      // bucket of xa, xb, ya, yb
+  ushort4 kb[kQC];                        // bucket of xa, xb, ya, yb
   int32_t cnt[kQC];
-  double red[4][kJW];
 };
 
-__device__ __forceinline__ int bucket_obj(double v, double base, double scale) {
+// Monotone bucket map of one axis of a leaf.  Any base and positive scale
+// keep it monotone (fl(v - base), the product, the clamps and the
+// truncation are all non-decreasing in v); the leaf's own extent makes the
+// buckets even.  Objects and bounds use the same map.
+__device__ __forceinline__ int bucket(double v, double base, double scale) {
   double t = __dmul_rn(__dsub_rn(v, base), scale);
+  t = t > 0.0 ? t : 0.0;
   t = t < (double)(kNK - 1) ? t : (double)(kNK - 1);
   return 1 + __double2int_rz(t);
-}
-__device__ __forceinline__ int bucket_bound(double v, double base, double top, double scale) {
-  if (v < base) return 0;
-  if (v > top) return kNK + 1;
-  return bucket_obj(v, base, scale);
 }
 
 __device__ __forceinline__ bool in_rect(double x, double y, const Rect4& R) {
@@ -807,75 +805,58 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
   const int tid = threadIdx.x, lane = lane_id(), wp = tid >> 5;
   const int64_t U = h->U;
   const double kNaN = __longlong_as_double(0x7ff8000000000000ll);
+  const double gxa = h->xa, gya = h->ya, gw = h->width, gh = h->height;
+  const double sxm = h->sx_max, sym = h->sy_max;  // 2^l_max / extent (0 for an empty extent)
+  const int lmax = h->l_max;
   for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
     const int64_t r = d.unit_leaf[u];
-    const int nobj = d.leaf_nobj[r], nisq = d.leaf_nisq[r];
+    const int4 li = d.linfo[r];  // object base, object count, entry base, intersecting count
+    const int nobj = li.y, nisq = li.w;
     const int nb = (nobj + 31) >> 5;
     const int ot = (int)(u - d.leaf_ubase[r]);
     const int n_ot = (nb + kTileBlocks - 1) / kTileBlocks;
     const int b0 = ot * kTileBlocks, nbt = min(kTileBlocks, nb - b0);
     const int P = min(nobj - b0 * 32, nbt * 32);
-    const int32_t ob = d.leaf_obase[r] + b0 * 32;
+    const int32_t ob = li.x + b0 * 32;
     const int64_t woff = d.leaf_woff[r];
-    const int32_t sbase = d.leaf_sbase[r];
+    const int32_t sbase = li.z;
     const bool table = nisq >= kTableMinQ;
     // ---- stage the tile's objects -------------------------------------------
-    double mnx = __longlong_as_double(0x7ff0000000000000ll), mny = mnx;
-    double mxx = -mnx, mxy = -mnx;
     for (int i = tid; i < nbt * 32; i += kJT) {
       double x = kNaN, y = kNaN;
       if (i < P) {
         x = d.sx[ob + i];
         y = d.sy[ob + i];
-        mnx = fmin(mnx, x);
-        mny = fmin(mny, y);
-        mxx = fmax(mxx, x);
-        mxy = fmax(mxy, y);
       }
       S.ox[i] = x;
       S.oy[i] = y;
     }
-    double basex = 0, basey = 0, topx = 0, topy = 0, scx = 0, scy = 0;
+    double bx = 0.0, by = 0.0, scx = 0.0, scy = 0.0;
     if (table) {
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        mnx = fmin(mnx, __shfl_xor_sync(0xffffffffu, mnx, o));
-        mny = fmin(mny, __shfl_xor_sync(0xffffffffu, mny, o));
-        mxx = fmax(mxx, __shfl_xor_sync(0xffffffffu, mxx, o));
-        mxy = fmax(mxy, __shfl_xor_sync(0xffffffffu, mxy, o));
-      }
-      if (lane == 0) {
-        S.red[0][wp] = mnx;
-        S.red[1][wp] = mny;
-        S.red[2][wp] = mxx;
-        S.red[3][wp] = mxy;
-      }
+      const uint32_t code = d.leaf_code[r];
+      const int lev = (int)(code >> kLevelShift);
+      const uint32_t z = code & kPayloadMask;
+      const double inv = 1.0 / (double)(1u << lev);
+      bx = gxa + (double)compact2(z) * inv * gw;
+      by = gya + (double)compact2(z >> 1) * inv * gh;
+      // kNK buckets across the leaf: sx_max = 2^l_max / width
+      const double f = (double)kNK / (double)(1u << (lmax - lev));
+      scx = sxm * f;
+      scy = sym * f;
       for (int i = tid; i < 2 * kRows * nbt; i += kJT) S.tab[i] = 0u;
       __syncthreads();
-      basex = S.red[0][0], basey = S.red[1][0], topx = S.red[2][0], topy = S.red[3][0];
-#pragma unroll
-      for (int w = 1; w < kJW; ++w) {
-        basex = fmin(basex, S.red[0][w]);
-        basey = fmin(basey, S.red[1][w]);
-        topx = fmax(topx, S.red[2][w]);
-        topy = fmax(topy, S.red[3][w]);
-      }
-      scx = __ddiv_rn((double)kNK, __dsub_rn(topx, basex));
-      scy = __ddiv_rn((double)kNK, __dsub_rn(topy, basey));
-      if (!(scx < 1e300)) scx = 0.0;  // empty extent (or overflow): one bucket, all ambiguous
-      if (!(scy < 1e300)) scy = 0.0;
       // bucket scatter: Bk[axis][k][b] |= bit of each object
       for (int i = tid; i < P; i += kJT) {
-        const int kx = bucket_obj(S.ox[i], basex, scx), ky = bucket_obj(S.oy[i], basey, scy);
+        const int kx = bucket(S.ox[i], bx, scx), ky = bucket(S.oy[i], by, scy);
         const uint32_t bit = 1u << (i & 31);
-        atomicOr(&S.tab[(0 * kRows + kx) * nbt + (i >> 5)], bit);
-        atomicOr(&S.tab[(1 * kRows + ky) * nbt + (i >> 5)], bit);
+        atomicOr(&S.tab[kx * nbt + (i >> 5)], bit);
+        atomicOr(&S.tab[(kRows + ky) * nbt + (i >> 5)], bit);
       }
       __syncthreads();
       // exclusive prefix-OR down every (axis, block) column: Pre_k = OR_{k' < k} Bk_k'
       constexpr int kPer = (kRows + 31) / 32;
       for (int task = wp; task < 2 * nbt; task += kJW) {
-        const int ax = task / nbt, b = task - ax * nbt;
+        const int ax = task >= nbt ? 1 : 0, b = task - ax * nbt;
         uint32_t* col = S.tab + ax * kRows * nbt + b;
         uint32_t v[kPer];
         uint32_t acc = 0;
@@ -902,19 +883,18 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       }
     }
     __syncthreads();
-    const uint32_t divm = (65536u + (uint32_t)nbt - 1u) / (uint32_t)nbt;  // it / nbt for it < 4096
+    const uint32_t divm = (65536u + (uint32_t)nbt - 1u) / (uint32_t)nbt;  // it / nbt for it < 65536 / 16
+    const Rect4* erect = d.erect + sbase;
     // ---- subquery chunks ------------------------------------------------------
     for (int c0 = 0; c0 < nisq; c0 += kQC) {
       const int nq = min(kQC, nisq - c0);
-      if (tid < nq) {
-        const Rect4 R = d.erect[sbase + c0 + tid];
-        S.rect[tid] = R;
-        S.cnt[tid] = 0;
-        if (table)
-          S.kb[tid] = make_ushort4((unsigned short)bucket_bound(R.xa, basex, topx, scx),
-                                   (unsigned short)bucket_bound(R.xb, basex, topx, scx),
-                                   (unsigned short)bucket_bound(R.ya, basey, topy, scy),
-                                   (unsigned short)bucket_bound(R.yb, basey, topy, scy));
+      for (int t = tid; t < nq; t += kJT) {
+        S.cnt[t] = 0;
+        if (table) {
+          const Rect4 R = erect[c0 + t];
+          S.kb[t] = make_ushort4((unsigned short)bucket(R.xa, bx, scx), (unsigned short)bucket(R.xb, bx, scx),
+                                 (unsigned short)bucket(R.ya, by, scy), (unsigned short)bucket(R.yb, by, scy));
+        }
       }
       __syncthreads();
       uint32_t* out = d.bitmap + woff + (int64_t)c0 * nb + b0;
@@ -932,7 +912,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
           uint32_t D = (xb0 & ~xa1) & (yb0 & ~ya1);
           uint32_t A = (xb1 & ~xa0) & (yb1 & ~ya0) & ~D;
           if (A) {
-            const Rect4 R = S.rect[s];
+            const Rect4 R = erect[c0 + s];
             do {
               const int bit = __ffs(A) - 1;
               A &= A - 1;
@@ -952,7 +932,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
           Rect4 R;
           R.xa = R.ya = __longlong_as_double(0x7ff0000000000000ll);  // +inf: empty rect
           R.xb = R.yb = __longlong_as_double((long long)0xfff0000000000000ull);
-          if (s < nq) R = S.rect[s];
+          if (s < nq) R = erect[c0 + s];
           uint32_t w = 0;
 #pragma unroll 8
           for (int k = 0; k < 32; ++k) {
@@ -966,12 +946,11 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
         }
       }
       __syncthreads();
-      if (tid < nq) {
-        int32_t* ec = d.ecount + sbase + c0 + tid;
-        if (n_ot == 1) *ec = S.cnt[tid];
-        else atomicAdd(ec, S.cnt[tid]);
+      for (int t = tid; t < nq; t += kJT) {
+        int32_t* ec = d.ecount + sbase + c0 + t;
+        if (n_ot == 1) *ec = S.cnt[t];
+        else atomicAdd(ec, S.cnt[t]);
       }
-      __syncthreads();
     }
   }
 }
