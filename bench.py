@@ -14,9 +14,11 @@ A step = one `tj_tick` (index build -> query scatter -> per-leaf bitmap join
   python bench.py [--gpus N --steps K --warmup W]           # our arm
   python bench.py --impl reference [...]                    # CPU reference arm (oracle port)
 
-Under torchrun (N>1) every rank processes its own 10M-object population
-(independent seeds; no data-path collective) and rank 0 prints the whole-job
-number: weak scaling, max-over-ranks device time.
+Under torchrun (N>1) the same 10M-object tick is split over the ranks: each
+rank holds 1/N of the updates and queries, an NCCL all-gather gives every rank
+the whole tick, every rank builds the (bit-identical) index and joins and
+decodes only its contiguous Morton leaf range.
+Strong scaling; rank 0 prints the max-over-ranks device time.
 """
 
 from __future__ import annotations
@@ -192,6 +194,38 @@ def run_reference(args):
     return 0
 
 
+class Shard:
+    """This rank's slice of one tick (1/G of the updates and queries, device
+    resident) and the all-gathered full tick it ingests each step (SURVEY.md
+    §8e: NCCL all-gather of the position updates over NVLink, then every rank
+    builds the same index and joins only its contiguous leaf range)."""
+
+    def __init__(self, tick, rank, world, dev, pinned=False):
+        import torch
+
+        self.n, self.m = int(tick.n_objects), int(tick.n_queries)
+        self.cn, self.cm = -(-self.n // world), -(-self.m // world)
+        self.world = world
+
+        def part(a, c):
+            t = torch.zeros(c, dtype=torch.from_numpy(a[:0]).dtype)
+            lo = min(rank * c, len(a))
+            hi = min(lo + c, len(a))
+            t[: hi - lo] = torch.from_numpy(a[lo:hi])
+            return t.pin_memory() if pinned else t.to(dev)
+
+        cols = (tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb)
+        self.mine = [part(a, self.cn if i < 3 else self.cm) for i, a in enumerate(cols)]
+        self.full = [torch.empty(world * (self.cn if i < 3 else self.cm), dtype=t.dtype, device=dev)
+                     for i, t in enumerate(self.mine)]
+
+    def gather(self, dev_slices=None):
+        import torch.distributed as dist
+
+        for f, p in zip(self.full, dev_slices or self.mine):
+            dist.all_gather_into_tensor(f, p)
+
+
 def run_ours(args):
     import numpy as np
     import torch
@@ -200,26 +234,37 @@ def run_ours(args):
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
-    if world > 1:
+    dev = torch.device("cuda", local)
+    sharded = world > 1 or args.sharded
+    if sharded:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29517"), ("RANK", "0"), ("WORLD_SIZE", "1")):
+            os.environ.setdefault(k, v)
+        dist.init_process_group("nccl", device_id=dev)
     pool = max(1, min(args.pool, args.steps + args.warmup))
-    ticks = gen_ticks(args.workload, pool, seed_offset=1000 * rank)
-    dev = torch.device("cuda", local)
-
-    def to_dev(t):
-        return [torch.from_numpy(a).to(dev) for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb, t.qyb)]
-
-    dticks = [to_dev(t) for t in ticks]
+    ticks = gen_ticks(args.workload, pool)  # the same ticks on every rank
     eng = Engine(MethodConfig(method="quad", device=local))
     ctx = eng.native
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
+    if sharded:
+        ctx.set_shard(rank, world)
+        shards = [Shard(t, rank, world, dev) for t in ticks]
+    else:
+        dticks = [[torch.from_numpy(a).to(dev) for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb, t.qyb)]
+                  for t in ticks]
 
     def tick_dev(k):
-        a = dticks[k % pool]
-        return ctx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
-                             *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
+        if sharded:
+            sh = shards[k % pool]
+            with torch.cuda.stream(stream):  # the collectives order before the tick on the library stream
+                sh.gather()
+            a, n, m = sh.full, sh.n, sh.m
+        else:
+            a = dticks[k % pool]
+            n, m = a[0].numel(), a[3].numel()
+        return ctx.tick_ptrs(n, *(x.data_ptr() for x in a[:3]), m, *(x.data_ptr() for x in a[3:]),
+                             _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
 
     for k in range(args.warmup):
         tick_dev(k)
@@ -237,54 +282,70 @@ def run_ours(args):
         _, st = tick_dev(args.warmup + k)
         ev[k + 1].record(stream)
         stats.append(st)
-        queries += int(st.n_queries)
+        queries += int(st.n_queries)  # every rank sees the whole tick: count once
     torch.cuda.synchronize()
     clk = clocks.stop()
     total_ms = ev[0].elapsed_time(ev[-1])
     per_tick = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     if world > 1:
-        t = torch.tensor([total_ms], device=dev)
+        t = torch.tensor([total_ms] + per_tick, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
-        qt = torch.tensor([queries], device=dev, dtype=torch.int64)
-        torch.distributed.all_reduce(qt)
-        queries = int(qt.item())
+        total_ms, per_tick = float(t[0].item()), [float(x) for x in t[1:].tolist()]
     value = queries / (total_ms / 1e3)
 
-    # roofline of the dominant kernel (the per-leaf join): algorithmic bytes per launch
-    # = 16*P_a (x, y of task objects) + 44*S_a (slot 4 + query row 4 + clipped rect 32 + count 4)
-    # + 4*W (bitmap words written); SURVEY.md §8(d) K3 row.
-    join_ms = statistics.mean(s.t_join_ms for s in stats)
     st0 = stats[-1]
-    join_bytes = 16 * st0.task_objects + 44 * st0.task_subqueries + 4 * st0.bitmap_words
+    n = int(st0.n_objects)
+    mean = lambda key: statistics.mean(getattr(s, key) for s in stats)  # noqa: E731
     peak, peak_src = measured_peak()
+    # roofline of the dominant kernel (the per-leaf join, K3): algorithmic bytes per launch =
+    # 16*P_a (x, y of the task objects) + 36*S_a (clipped rect 32 + result count 4 per
+    # intersecting entry) + 4*W (bitmap words written), DESIGN.md §4.
+    join_ms = mean("t_join_ms")
+    join_bytes = 16 * st0.task_objects + 36 * st0.task_subqueries + 4 * st0.bitmap_words
     achieved = join_bytes / (join_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic("k_join")
-    # index build (K1) roofline for the record: compulsory 44n + 4Z + 12L
-    idx_ms = statistics.mean(s.t_index_ms for s in stats)
-    n = int(st0.n_objects)
+    # index build (K0 + K1) against its compulsory bytes 44n + 4Z + 12L
+    build_ms = mean("t_build_ms")
+    build_bytes = 44 * n + 4 * (4 ** int(st0.l_deep)) + 12 * int(st0.n_leaves)
 
     # end to end through the C ABI with pinned host buffers: H2D inputs + D2H CSR per step
     e2e = None
     if not args.no_e2e:
-        hticks = [[torch.from_numpy(a).pin_memory() for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb,
-                                                                t.qyb)] for t in ticks]
+        e_steps = max(1, min(args.steps, args.e2e_steps))
+        if sharded:
+            hsh = [Shard(t, rank, world, dev, pinned=True) for t in ticks]
+            dsl = [[torch.empty_like(x, device=dev) for x in hsh[0].mine] for _ in range(1)][0]
 
-        def tick_host(k):
-            a = hticks[k % pool]
-            return ctx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
-                                 *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST)
+            def tick_host(k):
+                sh = hsh[k % pool]
+                with torch.cuda.stream(stream):
+                    for d_, h_ in zip(dsl, sh.mine):
+                        d_.copy_(h_, non_blocking=True)
+                    sh.gather(dsl)
+                a = sh.full
+                return ctx.tick_ptrs(sh.n, *(x.data_ptr() for x in a[:3]), sh.m, *(x.data_ptr() for x in a[3:]),
+                                     _native.TJ_MEM_DEVICE, _native.TJ_MEM_HOST), \
+                    sum(x.numel() * x.element_size() for x in sh.mine)
+        else:
+            hticks = [[torch.from_numpy(a).pin_memory() for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb,
+                                                                    t.qyb)] for t in ticks]
+
+            def tick_host(k):
+                a = hticks[k % pool]
+                return ctx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
+                                     *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST), \
+                    sum(x.numel() * x.element_size() for x in a)
 
         tick_host(0)
         torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e_steps = max(1, min(args.steps, args.e2e_steps))
         e0.record(stream)
         h2d = d2h = eq = 0
         for k in range(e_steps):
-            out, st = tick_host(k)
-            a = hticks[k % pool]
-            h2d += sum(x.numel() * x.element_size() for x in a)
+            (out, st), hb = tick_host(k)
+            h2d += hb
             d2h += 8 * (out.n_q + 1) + 8 * out.n_results
             eq += int(st.n_queries)
         e1.record(stream)
@@ -294,10 +355,11 @@ def run_ours(args):
             t = torch.tensor([e_ms], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_ms = float(t.item())
-            eq *= world
         e2e = {"value": eq / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // e_steps,
                "d2h_bytes_per_step": d2h // e_steps, "steps": e_steps,
-               "api": "tj_tick (C ABI) with pinned host input/output buffers"}
+               "api": ("tj_tick (C ABI): pinned host inputs -> device, results CSR -> pinned host"
+                       + ("; per rank: H2D of its 1/G slice, NCCL all-gather, D2H of its leaf-range CSR"
+                          if sharded else ""))}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -311,31 +373,37 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "p50_tick_ms": statistics.median(per_tick), "higher_is_better": True, "scaling": "weak",
+            "p50_tick_ms": statistics.median(per_tick), "higher_is_better": True,
+            "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
             "config": {"workload": args.workload, "description": DESCR[args.workload],
                        "n_objects": n, "queries_per_tick": int(st0.n_queries),
                        "results_per_tick": int(st0.results_total), "th_quad": 384, "l_max": 12,
                        "rebuild": "every_tick", "distinct_ticks_cycled": pool,
                        "l2": "inputs (>=560 MB/tick at 10M) exceed the 126 MB L2; no flush",
-                       "parallelism": f"{world} independent shard(s), one per GPU" if world > 1 else "1 GPU"},
+                       "parallelism": (f"leaf-range sharding over {world} GPUs: NCCL all-gather of each tick's "
+                                       f"updates, per-rank join/decode of its Morton leaf range" if sharded
+                                       else "1 GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "tj::k_join",
                          "bytes_per_launch": join_bytes, "ms_per_launch": join_ms, "peak_source": peak_src,
                          "traffic_source": traffic_src,
                          "tests_per_s": st0.containment_tests / (join_ms / 1e3)},
-            "roofline_index": {"kernel": "K1 index build (all kernels up to the leaf directory)",
-                               "ms": idx_ms, "compulsory_bytes": 44 * n + 4 * (4 ** int(st0.l_deep)) +
-                               12 * int(st0.n_leaves)},
-            "stage_ms": {k: statistics.mean(getattr(s, f"t_{k}_ms") for s in stats)
-                         for k in ("index", "filter", "join", "decode", "merge", "total")},
+            "roofline_index": {"kernels": "K0 + K1 index build (MBR .. objects in leaf order)",
+                               "ms": build_ms, "compulsory_bytes": build_bytes,
+                               "achieved": build_bytes / (build_ms / 1e3) / 1e9,
+                               "frac": build_bytes / (build_ms / 1e3) / 1e9 / peak},
+            "stage_ms": {"build": build_ms, "scatter": mean("t_scatter_ms"), "join": join_ms,
+                         "bitmaps": mean("t_filter_ms"), "decode": mean("t_decode_ms"),
+                         "merge": mean("t_merge_ms"), "total": mean("t_total_ms")},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(sum(int(s.kernel_launches) for s in stats)),
         }
         print(json.dumps(line), flush=True)
-    eng.close()
-    if world > 1:
+    torch.cuda.synchronize()
+    if sharded:  # before the library stream the collectives were ordered on goes away
         torch.distributed.destroy_process_group()
+    eng.close()
     return 0
 
 
@@ -352,6 +420,8 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="leaf-range sharded path (NCCL all-gather + tj_set_shard) even at N=1")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "ours":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)

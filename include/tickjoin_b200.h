@@ -106,6 +106,8 @@ typedef struct tj_stats {
   int64_t task_objects;        /* P_a: objects in leaves that are join tasks   */
   int64_t task_subqueries;     /* S_a: intersecting subqueries in join tasks   */
   int64_t kernel_launches;     /* kernels this call launched (all attempts)    */
+  double t_build_ms;           /* index build alone (K0 + K1: MBR .. leaf directory of objects) */
+  double t_scatter_ms;         /* query -> leaf scatter + subquery directory (K2) */
 } tj_stats;
 
 /* Reference-order index view (QuadIndex, quadtree.py:41-67). */

@@ -27,12 +27,23 @@ struct DBuf {
 
 }  // namespace
 
+// One instantiated CUDA graph of the tick's launch sequence.  Every size
+// after the index build lives on the device, so a graph is valid for any
+// tick with the same host-side launch shape: input/arena pointers (all in
+// `Dev`), n, m and the radix pass count.
+struct TickGraph {
+  Dev dv;
+  int64_t n = 0, m = 0;
+  int obj_passes = 0, shard_n = 0, launches[6] = {};
+  cudaGraphExec_t exec[6] = {};
+};
+
 struct tj_ctx {
   tj_config cfg{};
   int device = 0;
   int num_sms = 148;
   cudaStream_t st = nullptr;
-  cudaEvent_t ev[6] = {};
+  cudaEvent_t ev[7] = {};
   DevHdr* d_hdr = nullptr;
   DevHdr* h_hdr = nullptr;  // pinned
   int64_t* d_consts = nullptr;
@@ -66,6 +77,8 @@ struct tj_ctx {
   Dev dv{};
   int obj_passes = 0;
   int shard_rank = 0, shard_n = 1;
+  bool use_graphs = true;
+  std::vector<TickGraph> graphs;
   DBuf lactive, lwpre;
 };
 
@@ -288,9 +301,12 @@ void radix_sort(tj_ctx* c, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, 
   }
 }
 
-// The per-tick launch sequence.  No host synchronisation inside.
-// Returns the number of kernels launched.
-int launch_tick(tj_ctx* c) {
+// The per-tick launch sequence, in stages (index build, query scatter, join
+// preparation, join, decode, merge); no host synchronisation inside.  Stage
+// boundaries carry the timing events.  Returns the kernels launched.
+constexpr int kStages = 6;
+
+int launch_stage(tj_ctx* c, int stage) {
   cudaStream_t st = c->st;
   Dev& d = c->dv;
   DevHdr* h = c->d_hdr;
@@ -301,76 +317,81 @@ int launch_tick(tj_ctx* c) {
   const int Gn = grid_for(c, n), Gm = grid_for(c, m);
   const int Gbig = c->num_sms * 8;
   ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
-
-  cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
-  cudaMemsetAsync(d.leaf_cur, 0, c->cap_L * 2 * 4, st);
-  cudaMemsetAsync(d.leaf_nisq, 0, c->cap_L * 4, st);
-  cudaMemsetAsync(d.leaf_ncov, 0, c->cap_L * 4, st);
-
-  cudaEventRecord(c->ev[0], st);
-  // ---- K0 / K1: index build -------------------------------------------
-  k_mbr<<<Gn, 256, 0, st>>>(d);
-  k_monotone<<<Gn, 256, 0, st>>>(d);
-  k_finalize_mbr<<<1, 1, 0, st>>>(h);
-  k_codes<<<Gn, 256, 0, st>>>(d);
-  for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
-  if (D > 0) {
-    k_heavy<<<grid_for(c, int64_t(1) << (2 * F)), 256, 0, st>>>(d);
-    k_zero_sub<<<Gbig, 256, 0, st>>>(d);
-    k_sub_hist<<<Gn, 256, 0, st>>>(d);
-    for (int r = D - 1; r >= 1; --r) k_sub_level<<<Gbig, 256, 0, st>>>(d, r);
+  switch (stage) {
+    case 0:  // ---- K0 / K1: index build ------------------------------------
+      cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
+      cudaMemsetAsync(d.leaf_cur, 0, c->cap_L * 2 * 4, st);
+      cudaMemsetAsync(d.leaf_nisq, 0, c->cap_L * 4, st);
+      cudaMemsetAsync(d.leaf_ncov, 0, c->cap_L * 4, st);
+      k_mbr<<<Gn, 256, 0, st>>>(d);
+      k_monotone<<<Gn, 256, 0, st>>>(d);
+      k_finalize_mbr<<<1, 1, 0, st>>>(h);
+      k_codes<<<Gn, 256, 0, st>>>(d);
+      for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
+      if (D > 0) {
+        k_heavy<<<grid_for(c, int64_t(1) << (2 * F)), 256, 0, st>>>(d);
+        k_zero_sub<<<Gbig, 256, 0, st>>>(d);
+        k_sub_hist<<<Gn, 256, 0, st>>>(d);
+        for (int r = D - 1; r >= 1; --r) k_sub_level<<<Gbig, 256, 0, st>>>(d, r);
+      }
+      k_finalize_index<<<1, 1, 0, st>>>(h);
+      k_cell_level<<<Gbig, 256, 0, st>>>(d);
+      scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
+      k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
+      k_obj_keys<<<Gn, 256, 0, st>>>(d);
+      radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
+      scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
+                  st);
+      k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
+      k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
+      k_gather<int64_t><<<Gn, 256, 0, st>>>(d, d.ids, d.sid);
+      // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
+      return 17 + F + (D > 0 ? D + 2 : 0) + 5 * c->obj_passes;
+    case 1:  // ---- K2: query -> leaf scatter, subquery directory ----------
+      k_query_count<<<Gm, 256, 0, st>>>(d);
+      scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
+      k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
+      scan_launch(sp, LeafSqIn{d.leaf_nisq, d.leaf_ncov}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
+                  (int64_t*)nullptr, st);
+      k_query_fill<<<Gm, 256, 0, st>>>(d);
+      k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
+      return 10;
+    case 2: {  // ---- join preparation (and this rank's leaf range) -------
+      int extra = 0;
+      if (c->shard_n > 1) {
+        scan_launch(sp, LeafWeightIn{d.leaf_nobj, d.leaf_nisq, d.leaf_ncov}, PrefOut{d.leaf_wpre}, &h->L, h,
+                    &h->shard_total, st);
+        k_shard_mark<<<Gbig, 256, 0, st>>>(d);
+        extra = 4;
+      }
+      scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h,
+                  &h->W, st);
+      scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h,
+                  &h->U, st);
+      k_check_caps<<<1, 1, 0, st>>>(h, 2, 0, 0);
+      k_unit_map<<<Gbig, 256, 0, st>>>(d);
+      k_zero_counts<<<Gbig, 256, 0, st>>>(d);
+      return 9 + extra;
+    }
+    case 3:  // ---- K3: join ---------------------------------------------
+      k_join<<<c->num_sms * 5, kJT, sizeof(JoinSmem), st>>>(d);
+      return 1;
+    case 4:  // ---- K4: offsets, decode + canonical lists ------------------
+      k_cov_counts<<<Gbig, 256, 0, st>>>(d);
+      k_slot_counts<<<Gbig, 256, 0, st>>>(d);
+      scan_launch(sp, ArrIn<int32_t>{d.sq_count}, ExclOut<int64_t>{d.slot_off}, &h->S, h, &h->R, st);
+      k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
+      k_close_offsets<<<1, 1, 0, st>>>(d);
+      k_decode_query<<<Gbig, kDQThreads, 0, st>>>(d);
+      return 8;
+    default:  // ---- lists that need a sort by id ----------------------------
+      k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
+      return 1;
   }
-  k_finalize_index<<<1, 1, 0, st>>>(h);
-  k_cell_level<<<Gbig, 256, 0, st>>>(d);
-  scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
-  k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
-  k_obj_keys<<<Gn, 256, 0, st>>>(d);
-  radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
-  scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr, st);
-  k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
-  k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
-  k_gather<int64_t><<<Gn, 256, 0, st>>>(d, d.ids, d.sid);
-  // ---- K2: query -> leaf scatter ----------------------------------------
-  k_query_count<<<Gm, 256, 0, st>>>(d);
-  scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
-  k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
-  scan_launch(sp, LeafSqIn{d.leaf_nisq, d.leaf_ncov}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h, (int64_t*)nullptr,
-              st);
-  k_query_fill<<<Gm, 256, 0, st>>>(d);
-  k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
-  cudaEventRecord(c->ev[1], st);
-  int extra = 0;
-  if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range
-    scan_launch(sp, LeafWeightIn{d.leaf_nobj, d.leaf_nisq, d.leaf_ncov}, PrefOut{d.leaf_wpre}, &h->L, h,
-                &h->shard_total, st);
-    k_shard_mark<<<Gbig, 256, 0, st>>>(d);
-    extra = 4;
-  }
-  // ---- K3: join -----------------------------------------------------------
-  scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h, &h->W,
-              st);
-  scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h,
-              &h->U, st);
-  k_check_caps<<<1, 1, 0, st>>>(h, 2, 0, 0);
-  k_unit_map<<<Gbig, 256, 0, st>>>(d);
-  k_zero_counts<<<Gbig, 256, 0, st>>>(d);
-  cudaEventRecord(c->ev[2], st);
-  k_join<<<c->num_sms * 5, kJT, sizeof(JoinSmem), st>>>(d);
-  cudaEventRecord(c->ev[3], st);
-  // ---- K4: decode + canonical lists --------------------------------------
-  k_cov_counts<<<Gbig, 256, 0, st>>>(d);
-  k_slot_counts<<<Gbig, 256, 0, st>>>(d);
-  scan_launch(sp, ArrIn<int32_t>{d.sq_count}, ExclOut<int64_t>{d.slot_off}, &h->S, h, &h->R, st);
-  k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
-  k_close_offsets<<<1, 1, 0, st>>>(d);
-  k_decode_query<<<Gbig, kDQThreads, 0, st>>>(d);
-  cudaEventRecord(c->ev[4], st);
-  k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
-  cudaEventRecord(c->ev[5], st);
-  // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-  const int scans = 7, singles = 25 + F + (D > 0 ? 3 + (D - 1) : 0);
-  return 3 * scans + 5 * c->obj_passes + singles + extra + 3;  // + 3 memsets
 }
+
+// timing event recorded after each stage: build, scatter, prep, join, decode, merge
+constexpr int kStageEvent[kStages] = {6, 1, 2, 3, 4, 5};
 
 void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   DevHdr& H = *c->h_hdr;
@@ -402,6 +423,77 @@ int check_launch(tj_ctx* c) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(c, TJ_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
   return TJ_OK;
+}
+
+bool same_shape(const TickGraph& g, const tj_ctx* c) {
+  return g.n == c->n && g.m == c->m && g.obj_passes == c->obj_passes && g.shard_n == c->shard_n &&
+         std::memcmp(&g.dv, &c->dv, sizeof(Dev)) == 0;
+}
+
+void drop_graphs(tj_ctx* c) {
+  for (auto& g : c->graphs)
+    for (auto& e : g.exec)
+      if (e) cudaGraphExecDestroy(e);
+  c->graphs.clear();
+}
+
+// Capture every stage of the launch sequence as its own CUDA graph (the
+// timing events sit between the stage graphs, on the stream).
+bool capture_tick(tj_ctx* c, TickGraph& g) {
+  for (int s = 0; s < kStages; ++s) {
+    cudaGraph_t graph = nullptr;
+    if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+    g.launches[s] = launch_stage(c, s);
+    cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec[s], graph, 0);
+    if (graph) cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return false;
+  }
+  return true;
+}
+
+// Launch one tick: replay the cached stage graphs of this launch shape (the
+// tick's ~80 kernels become six graph launches), capturing them on first use.
+int run_tick(tj_ctx* c, int64_t* launches) {
+  TickGraph* g = nullptr;
+  if (c->use_graphs) {
+    for (auto& x : c->graphs)
+      if (same_shape(x, c)) g = &x;
+    if (!g) {
+      TickGraph ng;
+      std::memcpy(&ng.dv, &c->dv, sizeof(Dev));
+      ng.n = c->n;
+      ng.m = c->m;
+      ng.obj_passes = c->obj_passes;
+      ng.shard_n = c->shard_n;
+      if (capture_tick(c, ng)) {
+        if (c->graphs.size() >= 4) {
+          for (auto& e : c->graphs.front().exec)
+            if (e) cudaGraphExecDestroy(e);
+          c->graphs.erase(c->graphs.begin());
+        }
+        c->graphs.push_back(ng);
+        g = &c->graphs.back();
+      } else {  // capture unsupported here: launch directly from now on
+        for (auto& e : ng.exec)
+          if (e) cudaGraphExecDestroy(e);
+        cudaGetLastError();
+        c->use_graphs = false;
+      }
+    }
+  }
+  cudaEventRecord(c->ev[0], c->st);
+  for (int s = 0; s < kStages; ++s) {
+    if (g) {
+      *launches += g->launches[s];
+      cudaError_t e = cudaGraphLaunch(g->exec[s], c->st);
+      if (e != cudaSuccess) return fail(c, TJ_E_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
+    } else {
+      *launches += launch_stage(c, s);
+    }
+    cudaEventRecord(c->ev[kStageEvent[s]], c->st);
+  }
+  return check_launch(c);
 }
 
 }  // namespace
@@ -443,6 +535,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   c = new tj_ctx();
   c->cfg = *cfg;
   c->device = cfg->device;
+  if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
@@ -466,6 +559,7 @@ int tj_destroy(tj_ctx* c) {
   if (!c) return TJ_OK;
   cudaSetDevice(c->device);
   if (c->st) cudaStreamSynchronize(c->st);
+  drop_graphs(c);
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
@@ -546,8 +640,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       fill_dev(c, ids, xs, ys, qxa, qya, qxb, qyb);
       init_hdr(c, n, m);
       TJ_CUDA(cudaMemcpyAsync(c->d_hdr, c->h_hdr, sizeof(DevHdr), cudaMemcpyHostToDevice, c->st));
-      S.kernel_launches += launch_tick(c);
-      if ((rc = check_launch(c))) return rc;
+      if ((rc = run_tick(c, &S.kernel_launches))) return rc;
       TJ_CUDA(cudaMemcpyAsync(c->h_hdr, c->d_hdr, sizeof(DevHdr), cudaMemcpyDeviceToHost, c->st));
       TJ_CUDA(cudaStreamSynchronize(c->st));
       const DevHdr& H = *c->h_hdr;
@@ -587,6 +680,10 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     S.t_decode_ms = ms[2];
     S.t_merge_ms = ms[3];
     S.t_join_ms = ms[4];
+    float kb = 0;
+    cudaEventElapsedTime(&kb, c->ev[0], c->ev[6]);
+    S.t_build_ms = kb;
+    S.t_scatter_ms = ms[0] - kb;
     S.t_total_ms = tot;
     S.task_objects = (int64_t)H.task_obj;
     S.task_subqueries = (int64_t)H.task_isq;
