@@ -51,11 +51,11 @@ struct tj_ctx {
   // inputs
   DBuf ids, xs, ys, qxa, qya, qxb, qyb;
   // objects
-  DBuf code, okey0, okey1, oval0, oval1, sx, sy, sid;
+  DBuf code, okey0, okey1, oval0, oval1, sx, sy;
   // index
   DBuf linfo, pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf crect, qwin, nsub, qsbase, biglist;
+  DBuf crect, qwin, qpos, nsub, qsbase, biglist, leafcnt;
   // subqueries
   DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, leafcur, unitleaf;
   // join / outputs
@@ -169,7 +169,6 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(oval1, n * 4);
   ENS(sx, n * 8);
   ENS(sy, n * 8);
-  ENS(sid, n * 8);
   ENS(pyr, pyr_off(F + 1) * 4);
   ENS(heavy, (int64_t(1) << (2 * F)) * 4);
   ENS(sub, std::max<int64_t>(1, c->cap_heavy * sub_size(D)) * 4);
@@ -189,6 +188,8 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(lwpre, c->cap_L * 8);
   ENS(crect, m * sizeof(Rect4));
   ENS(qwin, m * sizeof(int4));
+  ENS(qpos, m * sizeof(int4));
+  ENS(leafcnt, c->cap_L * sizeof(int4));
   ENS(nsub, m * 4);
   ENS(qsbase, m * 4);
   ENS(biglist, m * 4);
@@ -245,7 +246,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.oval[1] = P<int32_t>(c->oval1);
   d.sx = P<double>(c->sx);
   d.sy = P<double>(c->sy);
-  d.sid = P<int64_t>(c->sid);
   d.pyr = P<uint32_t>(c->pyr);
   d.heavy_map = P<int32_t>(c->heavy);
   d.sub = P<uint32_t>(c->sub);
@@ -279,6 +279,8 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.SUB = sub_size(d.D);
   d.sidx = d.oval[c->obj_passes & 1];
   d.leaf_cur = P<int32_t>(c->leafcur);
+  d.leaf_cnt = P<int4>(c->leafcnt);
+  d.qpos = P<int4>(c->qpos);
   d.unit_leaf = P<int32_t>(c->unitleaf);
   d.big_list = P<int32_t>(c->biglist);
   d.leaf_active = c->shard_n > 1 ? P<uint8_t>(c->lactive) : nullptr;
@@ -287,17 +289,26 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
 }
 
 // stable LSD radix sort of (key, value) pairs over `passes` 8-bit digits
-void radix_sort(tj_ctx* c, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, int passes) {
+template <typename KeySrc>
+void radix_pass(tj_ctx* c, KeySrc keys, const int32_t* vin, uint32_t* kout, int32_t* vout, const int64_t* n_ptr,
+                int shift) {
   const int Gr = 2 * c->num_sms;
   ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
-  for (int p = 0; p < passes; ++p) {
+  k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(keys, n_ptr, c->d_hdr, shift, P<uint32_t>(c->rhist));
+  scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)}, c->d_consts,
+              c->d_hdr, (int64_t*)nullptr, c->st);
+  k_radix_downsweep<<<Gr, kRadixThreads, 0, c->st>>>(keys, vin, kout, vout, n_ptr, c->d_hdr, shift,
+                                                      P<int64_t>(c->roffs));
+}
+
+// stable LSD radix sort of (key, input row) pairs over `passes` 8-bit digits;
+// the first pass takes its keys from `first` and the rows implicitly
+template <typename KeySrc>
+void radix_sort(tj_ctx* c, KeySrc first, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, int passes) {
+  radix_pass(c, first, (const int32_t*)nullptr, k[1], v[1], n_ptr, 0);
+  for (int p = 1; p < passes; ++p) {
     const int src = p & 1, dst = src ^ 1;
-    k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], n_ptr, c->d_hdr, kRadixBits * p,
-                                                      P<uint32_t>(c->rhist));
-    scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)},
-                c->d_consts, c->d_hdr, (int64_t*)nullptr, c->st);
-    k_radix_downsweep<<<Gr, kRadixThreads, 0, c->st>>>(k[src], v[src], k[dst], v[dst], n_ptr, c->d_hdr,
-                                                        kRadixBits * p, P<int64_t>(c->roffs));
+    radix_pass(c, ArrKey{k[src]}, v[src], k[dst], v[dst], n_ptr, kRadixBits * p);
   }
 }
 
@@ -319,12 +330,10 @@ int launch_stage(tj_ctx* c, int stage) {
   ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
   switch (stage) {
     case 0:  // ---- K0 / K1: index build ------------------------------------
-      cudaMemsetAsync(d.pyr, 0, pyr_off(F + 1) * 4, st);
+      cudaMemsetAsync(d.pyr + pyr_off(F), 0, (pyr_off(F + 1) - pyr_off(F)) * 4, st);  // the histogram level
       cudaMemsetAsync(d.leaf_cur, 0, c->cap_L * 2 * 4, st);
-      cudaMemsetAsync(d.leaf_nisq, 0, c->cap_L * 4, st);
-      cudaMemsetAsync(d.leaf_ncov, 0, c->cap_L * 4, st);
+      cudaMemsetAsync(d.leaf_cnt, 0, c->cap_L * sizeof(int4), st);
       k_mbr<<<Gn, 256, 0, st>>>(d);
-      k_monotone<<<Gn, 256, 0, st>>>(d);
       k_finalize_mbr<<<1, 1, 0, st>>>(h);
       k_codes<<<Gn, 256, 0, st>>>(d);
       for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
@@ -338,20 +347,18 @@ int launch_stage(tj_ctx* c, int stage) {
       k_cell_level<<<Gbig, 256, 0, st>>>(d);
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
-      k_obj_keys<<<Gn, 256, 0, st>>>(d);
-      radix_sort(c, d.okey, d.oval, &h->n, c->obj_passes);
+      radix_sort(c, ObjKey{d.code, d.zmap, h}, d.okey, d.oval, &h->n, c->obj_passes);
       scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
                   st);
       k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
       k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
-      k_gather<int64_t><<<Gn, 256, 0, st>>>(d, d.ids, d.sid);
       // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-      return 17 + F + (D > 0 ? D + 2 : 0) + 5 * c->obj_passes;
+      return 14 + F + (D > 0 ? D + 2 : 0) + 5 * c->obj_passes;
     case 1:  // ---- K2: query -> leaf scatter, subquery directory ----------
       k_query_count<<<Gm, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
-      scan_launch(sp, LeafSqIn{d.leaf_nisq, d.leaf_ncov}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
+      scan_launch(sp, LeafSqIn{d.leaf_cnt}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
                   (int64_t*)nullptr, st);
       k_query_fill<<<Gm, 256, 0, st>>>(d);
       k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
@@ -561,9 +568,9 @@ int tj_destroy(tj_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   drop_graphs(c);
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
-                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->sid, &c->pyr, &c->heavy, &c->sub, &c->clev,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->crect, &c->qwin, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
+                 &c->lubase, &c->crect, &c->qwin, &c->qpos, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
                  &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->partial, &c->rhist, &c->roffs};
   for (DBuf* b : all)
@@ -633,7 +640,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     c->m = m;
     if ((rc = prepare_static(c, n, m))) return rc;
     if (c->last_L == 0) c->last_L = c->cap_L;
-    c->obj_passes = passes_for(std::max<int64_t>(c->last_L + c->last_L / 2, 1) - 1);
+    c->obj_passes = passes_for(std::max<int64_t>(c->last_L, 1) - 1);  // grows (tick replay) if L crosses a digit
     bool done = false;
     for (int attempt = 0; attempt < 8 && !done; ++attempt) {
       if ((rc = prepare_dynamic(c))) return rc;

@@ -14,7 +14,8 @@ namespace tj {
 
 constexpr int kWarp = 32;
 constexpr int kMaxLevel = 12;        // morton.py:20 L_MAX
-constexpr int kDenseTop = 8;         // dense pyramid levels 0..min(l_max, 8)
+constexpr int kDenseTop = 12;        // dense pyramid levels 0..min(l_max, 12): the histogram is taken
+                                     // at l_max (fine bins: little atomic contention in hotspots)
 constexpr int kLevelShift = 24;      // zmap / leaf code: (level << 24) | payload
 constexpr uint32_t kPayloadMask = (1u << kLevelShift) - 1u;
 
@@ -30,6 +31,7 @@ struct DevHdr {
   unsigned long long kmin_x, kmin_y, kmax_x, kmax_y;
   double xa, ya, xb, yb, width, height;
   double sx_max, sy_max, sx_deep, sy_deep;
+  double lw[13], lh[13];    // leaf extent per level: width / 2^level, height / 2^level (quadtree.py:219-231)
   int32_t wpos, hpos;       // width > 0, height > 0
   int32_t l_deep;
   int32_t n_heavy;

@@ -41,7 +41,6 @@ struct Dev {
   const int32_t* sidx;  // sorted input rows (points into oval[])
   double* sx;
   double* sy;
-  int64_t* sid;
   // index
   uint32_t* pyr;
   int32_t* heavy_map;
@@ -71,7 +70,9 @@ struct Dev {
   int32_t* sinv;            // per slot: its directory entry
   int4* linfo;              // per leaf: object base, object count, entry base, intersecting count
   int64_t* slot_off;        // per slot (S + 1): start of its run in the output CSR
-  int32_t* leaf_cur;       // per leaf x {intersecting, covering}: fill cursor
+  int32_t* leaf_cur;       // per leaf x {intersecting, covering}: fill cursor of large-window pairs
+  int4* leaf_cnt;          // per leaf: intersecting / covering pairs of small windows, of large windows
+  int4* qpos;              // per small-window query: each pair's place in its leaf block
   int32_t* unit_leaf;      // join work unit -> leaf
   uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
   int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
@@ -109,16 +110,42 @@ __device__ __forceinline__ unsigned long long shfl_max64(unsigned long long v) {
   return v;
 }
 
+// Exact MBR (order-preserving u64 keys, warp-reduced atomics) and, in the
+// same pass, whether object ids strictly increase in input order (then
+// per-leaf blocks are id-sorted and per-query merges are merges of sorted
+// runs) and whether id == input row (the generator's arange ids: then the
+// final lists need no id lookup).  Four items per thread in flight.
 __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
   DevHdr* h = d.h;
   const int64_t n = h->n;
   unsigned long long mnx = ~0ull, mny = ~0ull, mxx = 0ull, mxy = 0ull;
-  TJ_GRID_STRIDE(i, n) {
-    const unsigned long long kx = dkey(d.xs[i]), ky = dkey(d.ys[i]);
-    mnx = kx < mnx ? kx : mnx;
-    mny = ky < mny ? ky : mny;
-    mxx = kx > mxx ? kx : mxx;
-    mxy = ky > mxy ? ky : mxy;
+  int bad = 0, notid = 0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    double x[4], y[4];
+    int64_t v[4], nx[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      const bool ok = i < n;
+      x[u] = ok ? d.xs[i] : 0.0;
+      y[u] = ok ? d.ys[i] : 0.0;
+      v[u] = ok ? d.ids[i] : 0;
+      nx[u] = (i + 1 < n) ? d.ids[i + 1] : 0x7fffffffffffffffll;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        const unsigned long long kx = dkey(x[u]), ky = dkey(y[u]);
+        mnx = kx < mnx ? kx : mnx;
+        mny = ky < mny ? ky : mny;
+        mxx = kx > mxx ? kx : mxx;
+        mxy = ky > mxy ? ky : mxy;
+        notid |= (v[u] != i);
+        bad |= (i + 1 < n) && (v[u] >= nx[u]);
+      }
+    }
   }
   mnx = shfl_min64(mnx);
   mny = shfl_min64(mny);
@@ -129,22 +156,6 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
     atomicMin(&h->kmin_y, mny);
     atomicMax(&h->kmax_x, mxx);
     atomicMax(&h->kmax_y, mxy);
-  }
-}
-
-// Also detects whether object ids strictly increase in input order: then
-// per-leaf blocks (input order) are id-sorted and per-query merges are merges
-// of sorted runs.
-// (and whether id == input row, the generator's arange ids: then the final
-// lists need no id lookup at all)
-__global__ void __launch_bounds__(256) k_monotone(const Dev d) {
-  DevHdr* h = d.h;
-  const int64_t n = h->n;
-  int bad = 0, notid = 0;
-  TJ_GRID_STRIDE(i, n) {
-    const int64_t v = d.ids[i];
-    notid |= (v != i);
-    if (i + 1 < n) bad |= (v >= d.ids[i + 1]);
   }
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(&h->not_monotone, 1);
   if (__any_sync(0xffffffffu, notid) && lane_id() == 0) atomicOr(&h->not_identity, 1);
@@ -164,6 +175,10 @@ __global__ void k_finalize_mbr(DevHdr* h) {
   const double side = (double)(1u << h->l_max);
   h->sx_max = h->wpos ? __ddiv_rn(side, h->width) : 0.0;
   h->sy_max = h->hpos ? __ddiv_rn(side, h->height) : 0.0;
+  for (int l = 0; l <= kMaxLevel; ++l) {
+    h->lw[l] = __ddiv_rn(h->width, (double)(1u << l));
+    h->lh[l] = __ddiv_rn(h->height, (double)(1u << l));
+  }
 }
 
 // ===========================================================================
@@ -180,18 +195,24 @@ __global__ void __launch_bounds__(256) k_codes(const Dev d) {
   const int wpos = h->wpos, hpos = h->hpos;
   const int sh = 2 * (lmax - F);
   uint32_t* hist = d.pyr + pyr_off(F);
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = b + threadIdx.x;
-    uint32_t bin = 0xFFFFFFFFu;
-    if (i < n) {
-      const uint32_t ci = cell_of(d.xs[i], xa, sx, wpos, side);
-      const uint32_t cj = cell_of(d.ys[i], ya, sy, hpos, side);
-      const uint32_t z = morton2(ci, cj);
-      d.code[i] = z;
-      bin = z >> sh;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+    double x[4], y[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      x[u] = i < n ? d.xs[i] : 0.0;
+      y[u] = i < n ? d.ys[i] : 0.0;
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-    if (i < n && (int)(__ffs(peers) - 1) == lane_id()) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u * stride;
+      if (i < n) {
+        const uint32_t z = morton2(cell_of(x[u], xa, sx, wpos, side), cell_of(y[u], ya, sy, hpos, side));
+        d.code[i] = z;
+        if (!(h->dbg & 4)) atomicAdd(&hist[z >> sh], 1u);  // level-F histogram (fire-and-forget reductions)
+      }
+    }
   }
 }
 
@@ -270,8 +291,7 @@ __global__ void __launch_bounds__(256) k_sub_hist(const Dev d) {
       const int slot = d.heavy_map[z >> (2 * D)];
       if (slot >= 0) bin = (int64_t)slot * d.SUB + off + (z & lowmask);
     }
-    const uint32_t peers = __match_any_sync(0xffffffffu, (unsigned long long)bin);
-    if (bin >= 0 && (int)(__ffs(peers) - 1) == lane_id()) atomicAdd(&d.sub[bin], (uint32_t)__popc(peers));
+    if (bin >= 0) atomicAdd(&d.sub[bin], 1u);
   }
 }
 
@@ -366,17 +386,16 @@ struct ZOut {
   }
 };
 
-// object -> leaf rank (quadtree.py:161-165) as the radix key, input row as value
-__global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  const int64_t n = h->n;
-  const int sh = 2 * (h->l_max - h->l_deep);
-  TJ_GRID_STRIDE(i, n) {
-    d.okey[0][i] = d.zmap[d.code[i] >> sh] & kPayloadMask;
-    d.oval[0][i] = (int32_t)i;
+// object -> leaf rank (quadtree.py:161-165): the first radix pass computes
+// it on the fly from the l_max code and the zmap (the value is the input row)
+struct ObjKey {
+  const uint32_t* code;
+  const uint32_t* zmap;
+  const DevHdr* h;
+  __device__ uint32_t operator()(int64_t i) const {
+    return zmap[code[i] >> (2 * (h->l_max - h->l_deep))] & kPayloadMask;
   }
-}
+};
 
 // Payload gather into leaf order, one array per launch: each launch's random
 // reads hit one 80 MB array (at 10M objects) that stays L2-resident, instead
@@ -491,9 +510,8 @@ __device__ __forceinline__ int enum_small(const int4 w, int ld, const uint32_t* 
 // w = width / 2^level; lxa = xa + li*w; covering iff qxa <= lxa and
 // qxb >= min(lxa + w, mbr.xb), likewise in y.
 __device__ __forceinline__ bool covers(const Rect4& q, int lev, uint32_t z, const DevHdr* h) {
-  const double side = (double)(1u << lev);
-  const double w = __ddiv_rn(h->width, side);
-  const double hh = __ddiv_rn(h->height, side);
+  const double w = h->lw[lev];
+  const double hh = h->lh[lev];
   const double li = (double)compact2(z), lj = (double)compact2(z >> 1);
   const double lxa = __dadd_rn(h->xa, __dmul_rn(li, w));
   const double lya = __dadd_rn(h->ya, __dmul_rn(lj, hh));
@@ -504,12 +522,19 @@ __device__ __forceinline__ bool covers(const Rect4& q, int lev, uint32_t z, cons
   return (q.xa <= lxa) && (q.xb >= ux) && (q.ya <= lya) && (q.yb >= uy);
 }
 
-// a (query, leaf) pair found by the count pass: the leaf's intersecting /
-// covering directory block grows by one (counting sort by leaf, no radix sort)
-__device__ __forceinline__ void count_pair(const Dev& d, int lev, uint32_t z, uint32_t rank, const Rect4& r,
-                                           int cov_on) {
-  const bool cv = cov_on && covers(r, lev, z, d.h);
-  atomicAdd(cv ? &d.leaf_ncov[rank] : &d.leaf_nisq[rank], 1);
+// Counting sort of the (query, leaf) pairs into per-leaf directory blocks
+// (directory.py:119-158), two passes over the queries:
+//  count: every pair bumps its leaf's intersecting or covering counter.  A
+//    small window (<= 2x2 deepest cells, every query of configs A-C keeps
+//    the counter's old value — its place in the block — for the fill;
+//  fill: (after a scan of the block sizes) a small-window pair lands at that
+//    place with no further atomics; pairs of larger windows take places after
+//    the small ones from a cursor.
+// Within a block, entries are in this (unordered) fill order; the join and
+// the decode are invariant to it and the introspection entry points return
+// the reference's query order (directory.py:131).
+__device__ __forceinline__ bool pair_cov(const Dev& d, int lev, uint32_t z, const Rect4& r, int cov_on) {
+  return cov_on && covers(r, lev, z, d.h);
 }
 
 // clip (geometry.py:80-88), window (quadtree.py:182-183), count subqueries
@@ -542,12 +567,20 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
       if (is_small(w)) {
         uint32_t key[4], rank[4];
         cnt = enum_small(w, ld, d.zmap, key, rank);
+        int pos[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (k < cnt) count_pair(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, rank[k], r, cov_on);
+          if (k < cnt) {
+            const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
+            int4* c = d.leaf_cnt + rank[k];
+            pos[k] = atomicAdd(cv ? &c->y : &c->x, 1);
+          }
+        d.qpos[q] = make_int4(pos[0], pos[1], pos[2], pos[3]);
       } else {
-        cnt = enum_window(w.x, w.y, w.z, w.w, ld, d.zmap,
-                          [&](int lev, uint32_t z, uint32_t rank) { count_pair(d, lev, z, rank, r, cov_on); });
+        cnt = enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
+          int4* c = d.leaf_cnt + rank;
+          atomicAdd(pair_cov(d, lev, z, r, cov_on) ? &c->w : &c->z, 1);
+        });
       }
     }
     d.qwin[q] = w;
@@ -559,18 +592,11 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
 // (its list needs no merge and is decoded straight into the output).
 constexpr uint8_t kFlagCov = 1, kFlagSingle = 2;
 
-__device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, int64_t q, int n, int lev, uint32_t z,
-                                              uint32_t rank, const Rect4& r, int cov_on) {
-  const bool cv = cov_on && covers(r, lev, z, d.h);
+__device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, int64_t q, int n, uint32_t rank, bool cv,
+                                              int32_t e, const Rect4& r) {
   d.sq_leaf[slot] = (int32_t)rank;
   d.sq_q[slot] = (int32_t)q;
   d.sq_cov[slot] = (uint8_t)((cv ? kFlagCov : 0) | (n == 1 ? kFlagSingle : 0));
-  // directory entry: the leaf's intersecting block, then its covering block
-  // (directory.py:131-142); within a block, entries take fill order — the
-  // join and decode are invariant to it, and the introspection entry points
-  // return the reference's query order
-  const int32_t e = d.leaf_sbase[rank] + (cv ? d.leaf_nisq[rank] : 0) +
-                    atomicAdd(&d.leaf_cur[2 * rank + (cv ? 1 : 0)], 1);
   d.sinv[slot] = e;
   d.erect[e] = r;  // the join's input, in entry order
 }
@@ -593,9 +619,16 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
     if (is_small(w)) {
       uint32_t key[4], rank[4];
       enum_small(w, ld, d.zmap, key, rank);
+      const int4 p4 = d.qpos[q];
+      const int pos[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (k < n) emit_subquery(d, base + k, q, n, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, rank[k], r, cov_on);
+        if (k < n) {
+          const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
+          const int4 c = d.leaf_cnt[rank[k]];
+          const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pos[k];
+          emit_subquery(d, base + k, q, n, rank[k], cv, e, r);
+        }
       continue;
     }
     int cur[kMaxLevel + 1];
@@ -612,7 +645,11 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
       }
     }
     enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
-      emit_subquery(d, base + cur[lev]++, q, n, lev, z, rank, r, cov_on);
+      const bool cv = pair_cov(d, lev, z, r, cov_on);
+      const int4 c = d.leaf_cnt[rank];
+      const int32_t e = d.leaf_sbase[rank] + (cv ? c.x + c.z + c.y : c.x) +
+                        atomicAdd(&d.leaf_cur[2 * rank + (cv ? 1 : 0)], 1);
+      emit_subquery(d, base + cur[lev]++, q, n, rank, cv, e, r);
     });
   }
 }
@@ -624,7 +661,10 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
   const int64_t L = h->L;
   unsigned long long act = 0, s1 = 0, s2 = 0, tasks = 0, tests = 0, si = 0, sc = 0, pa = 0, sa = 0;
   TJ_GRID_STRIDE(r, L) {
-    const int32_t nisq = d.leaf_nisq[r], ncov = d.leaf_ncov[r];
+    const int4 c = d.leaf_cnt[r];
+    const int32_t nisq = c.x + c.z, ncov = c.y + c.w;
+    d.leaf_nisq[r] = nisq;
+    d.leaf_ncov[r] = ncov;
     d.linfo[r] = make_int4(d.leaf_obase[r], d.leaf_nobj[r], d.leaf_sbase[r], nisq);
     const unsigned long long no = (unsigned long long)d.leaf_nobj[r];
     const unsigned long long ni = (unsigned long long)nisq;
@@ -722,9 +762,11 @@ struct UnitsIn {
 
 // directory blocks: per leaf, intersecting entries then covering entries
 struct LeafSqIn {
-  const int32_t* nisq;
-  const int32_t* ncov;
-  __device__ int64_t operator()(int64_t r) const { return (int64_t)nisq[r] + ncov[r]; }
+  const int4* cnt;
+  __device__ int64_t operator()(int64_t r) const {
+    const int4 c = cnt[r];
+    return (int64_t)c.x + c.y + c.z + c.w;
+  }
 };
 
 // Multi-GPU leaf-range sharding: every rank builds the same

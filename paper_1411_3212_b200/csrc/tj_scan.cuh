@@ -145,20 +145,27 @@ struct ExclOut {
 // ballots (stable: warp w / round k / lane order), stages the tile by digit in
 // shared memory and writes digit runs coalesced.
 // ---------------------------------------------------------------------------
-constexpr int kRadixBits = 9;                       // 2 passes cover 18-bit keys
+constexpr int kRadixBits = 8;                       // 2 passes cover 16-bit keys (leaf ranks)
 constexpr int kRadixDigits = 1 << kRadixBits;       // 512
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixDPT = kRadixDigits / kRadixThreads;  // digits per thread (2)
-constexpr int kRadixIPT = 8;                        // items per thread per tile
-constexpr int kRadixTile = kRadixThreads * kRadixIPT;  // 2048
+constexpr int kRadixDPT = kRadixDigits / kRadixThreads;  // digits per thread (1)
+constexpr int kRadixIPT = 16;                       // items per thread per tile
+constexpr int kRadixTile = kRadixThreads * kRadixIPT;  // 4096
+
+// key sources: a key array, or computed on the fly (first pass)
+struct ArrKey {
+  const uint32_t* k;
+  __device__ uint32_t operator()(int64_t i) const { return k[i]; }
+};
 
 __device__ __forceinline__ int64_t radix_chunk(int64_t n, int64_t G) {
   return ((n + G - 1) / G + kRadixTile - 1) / kRadixTile * kRadixTile;
 }
 
+template <typename KeySrc>
 __global__ void __launch_bounds__(kRadixThreads)
-k_radix_upsweep(const uint32_t* keys, const int64_t* n_ptr, const DevHdr* h, int shift,
+k_radix_upsweep(KeySrc keys, const int64_t* n_ptr, const DevHdr* h, int shift,
                 uint32_t* hist /* [digits][G] */) {
   if (h->abort) return;
   __shared__ uint32_t cnt[kRadixWarps][kRadixDigits];
@@ -170,7 +177,7 @@ k_radix_upsweep(const uint32_t* keys, const int64_t* n_ptr, const DevHdr* h, int
   for (int k = threadIdx.x; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&cnt[0][0])[k] = 0;
   __syncthreads();
   for (int64_t i = b + threadIdx.x; i < e; i += kRadixThreads)
-    atomicAdd(&cnt[w][(keys[i] >> shift) & (kRadixDigits - 1)], 1u);
+    atomicAdd(&cnt[w][(keys(i) >> shift) & (kRadixDigits - 1)], 1u);
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < kRadixDPT; ++j) {
@@ -182,8 +189,10 @@ k_radix_upsweep(const uint32_t* keys, const int64_t* n_ptr, const DevHdr* h, int
   }
 }
 
-__global__ void __launch_bounds__(kRadixThreads, 4)
-k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out,
+// vals_in == nullptr: the value of item i is i (first pass over input rows)
+template <typename KeySrc>
+__global__ void __launch_bounds__(kRadixThreads, 3)
+k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
                   int32_t* vals_out, const int64_t* n_ptr, const DevHdr* h, int shift,
                   const int64_t* offs /* [digits][G] exclusive */) {
   if (h->abort) return;
@@ -210,8 +219,8 @@ k_radix_downsweep(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* key
     for (int r = 0; r < kRadixIPT; ++r) {
       const int64_t i = tb + (int64_t)w * 32 * kRadixIPT + r * 32 + lane;
       const bool ok = i < e;
-      key[r] = ok ? keys_in[i] : 0u;
-      val[r] = ok ? vals_in[i] : 0;
+      key[r] = ok ? keys_in(i) : 0u;
+      val[r] = ok ? (vals_in ? vals_in[i] : (int32_t)i) : 0;
     }
   };
   if (b < e) load_tile(b);
