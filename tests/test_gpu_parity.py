@@ -324,3 +324,79 @@ def test_config_c_scale_properties(pkg):
                & (tick.ys <= tick.qyb[k]))
         assert np.array_equal(res.of(k), np.sort(tick.ids[hit]))
     eng.close()
+
+
+def test_table_join_objects_on_query_edges(pkg):
+    """Objects on a lattice whose coordinates coincide with query edges, many
+    subqueries per leaf (the bucket-table join path) — every ambiguous bit goes
+    through the exact fp64 test; equal to the oracle and to brute force."""
+    rng = np.random.default_rng(41)
+    g = np.arange(0.0, 64.0, 0.25)
+    gx, gy = np.meshgrid(g, g)
+    xs = np.concatenate([gx.ravel(), rng.uniform(0, 64, 4000)])
+    ys = np.concatenate([gy.ravel(), rng.uniform(0, 64, 4000)])
+    n = len(xs)
+    m = 6000
+    a = rng.choice(g, m)
+    b = rng.choice(g, m)
+    wx = rng.choice(np.arange(0.25, 6.0, 0.25), m)
+    wy = rng.choice(np.arange(0.25, 6.0, 0.25), m)
+    qxa, qya, qxb, qyb = a, b, a + wx, b + wy
+    ids = np.arange(n, dtype=np.int64)
+    qids = np.arange(m, dtype=np.int64)
+    for th in (256, 384):
+        eng = _engine(pkg, th=th)
+        res, st = eng.process_columns(ids, xs, ys, qids, qxa, qya, qxb, qyb)
+        ref = qo.run_tick(ids, xs, ys, qids, qxa, qya, qxb, qyb, th_quad=th, keep_tasks=True)
+        _check_vs_oracle(res, ref)
+        off, res_b = qo.brute_force(ids, xs, ys, qxa, qya, qxb, qyb)
+        assert np.array_equal(res.offsets, off) and np.array_equal(res.ids, res_b)
+        bm = eng.native.bitmaps()  # per-task words in the reference's row order (bitmap.py:70-119)
+        assert np.array_equal(bm["words"], np.concatenate([t[3] for t in ref.tasks]))
+        assert np.array_equal(bm["counts"], np.concatenate([t[4] for t in ref.tasks]))
+        assert int(bm["nisq"].max()) >= 12  # the table path ran
+        eng.close()
+
+
+def test_graph_replay_equals_direct_launch(pkg, monkeypatch):
+    """The tick's captured CUDA graphs replay to the same results as direct
+    launches, across ticks with different inputs of the same shape."""
+    rng = np.random.default_rng(43)
+    ticks = []
+    for _ in range(3):
+        xs, ys, a, b, c, d = _rand_tick(rng, 40_000, 20_000, side=(5.0, 40.0))
+        ticks.append((np.arange(40_000, dtype=np.int64), xs, ys, np.arange(20_000, dtype=np.int64), a, b, c, d))
+    eng = _engine(pkg, th=64)
+    graphed = [eng.process_columns(*t)[0] for t in ticks + ticks]
+    eng.close()
+    monkeypatch.setenv("TJ_NO_GRAPH", "1")
+    eng = _engine(pkg, th=64)
+    direct = [eng.process_columns(*t)[0] for t in ticks]
+    eng.close()
+    for k, r in enumerate(graphed):
+        assert np.array_equal(r.offsets, direct[k % 3].offsets) and np.array_equal(r.ids, direct[k % 3].ids)
+
+
+def test_extreme_hotspot_big_leaves(pkg):
+    """Config-E shape, scaled down: uniform background + one extreme hotspot;
+    leaves pinned at l_max hold thousands of objects (multi-tile join units,
+    the decode's large-leaf path)."""
+    rng = np.random.default_rng(47)
+    nu, nh = 200_000, 120_000
+    xs = np.concatenate([rng.uniform(0, 22500, nu), rng.normal(11250, 3.0, nh)])
+    ys = np.concatenate([rng.uniform(0, 22500, nu), rng.normal(11250, 3.0, nh)])
+    n = nu + nh
+    m = 30_000
+    k = rng.integers(0, n, m)
+    side = rng.choice([1.0, 2.0, 8.0], m)
+    qxa, qya = xs[k] - side / 2, ys[k] - side / 2
+    qxb, qyb = qxa + side, qya + side
+    ids = np.arange(n, dtype=np.int64)
+    qids = np.arange(m, dtype=np.int64)
+    eng = _engine(pkg)
+    res, st = eng.process_columns(ids, xs, ys, qids, qxa, qya, qxb, qyb)
+    ref = qo.run_tick(ids, xs, ys, qids, qxa, qya, qxb, qyb)
+    _check_vs_oracle(res, ref)
+    occ = ref.directory.o_end - ref.directory.o_start
+    assert occ.max() > 384  # some leaves span several 384-object join tiles
+    eng.close()

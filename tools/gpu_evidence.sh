@@ -1,0 +1,8 @@
+# Round evidence: GPU tests, full bench line, ncu launch list, ncu --set full of the top kernels
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?; tail -2 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench.log | cut -c1-400
+timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?; tail -1 gpurun_out/bench_ref.log | cut -c1-300
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1; echo launches=$?
+timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:k_decode_query|k_join|k_query_fill|k_query_count|k_radix_downsweep|k_gather|k_codes|k_mbr" --launch-skip 30 -c 9 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/prof_full.log 2>&1; echo ncu=$?
