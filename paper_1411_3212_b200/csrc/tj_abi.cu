@@ -389,7 +389,7 @@ int launch_stage(tj_ctx* c, int stage) {
       scan_launch(sp, ArrIn<int32_t>{d.sq_count}, ExclOut<int64_t>{d.slot_off}, &h->S, h, &h->R, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
       k_close_offsets<<<1, 1, 0, st>>>(d);
-      k_decode_query<<<Gbig, kDQThreads, 0, st>>>(d);
+      k_decode_query<<<c->num_sms * 10, kDQThreads, 0, st>>>(d);  // 10 CTAs of 4 warps fill an SM (48 regs)
       return 8;
     default:  // ---- lists that need a sort by id ----------------------------
       k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
