@@ -46,11 +46,27 @@ WORKLOADS = {
     "B": dict(n_objects=1_000_000, query_rate=1.0, query_side=50.0, distribution="gaussian", n_hotspots=25,
               seed=2),
     "A": dict(n_objects=100_000, query_rate=0.1, query_side=(200.0, 800.0), distribution="uniform", seed=1),
+    # config C at its other query sides
+    "C2": dict(n_objects=10_000_000, query_rate=1.0, query_side=2.0, distribution="gaussian", n_hotspots=25,
+               seed=3),
+    "C10": dict(n_objects=10_000_000, query_rate=1.0, query_side=10.0, distribution="gaussian", n_hotspots=25,
+                seed=3),
+    "C20": dict(n_objects=10_000_000, query_rate=1.0, query_side=20.0, distribution="gaussian", n_hotspots=25,
+                seed=3),
+    # config E: 40M uniform (seed 5) + 10M in one extreme hotspot (sigma 100u, seed 6), ids of the
+    # second part offset by 40M, 1u queries at 100% rate, each part moved by its own generator
+    "E": [dict(n_objects=40_000_000, query_rate=1.0, query_side=1.0, distribution="uniform", seed=5),
+          dict(n_objects=10_000_000, query_rate=1.0, query_side=1.0, distribution="gaussian", n_hotspots=1,
+               sigma=100.0, seed=6)],
 }
 DESCR = {
     "C5": "skewed 10M objects (gaussian, 25 hotspots, sigma 225u), 100% query rate, 5u squares, seed 3",
     "B": "gaussian 1M objects, 100% query rate, 50u squares, seed 2",
     "A": "uniform 100K objects, 10% query rate, sides U[200,800]u, seed 1",
+    "C2": "skewed 10M objects (gaussian, 25 hotspots, sigma 225u), 100% query rate, 2u squares, seed 3",
+    "C10": "skewed 10M objects (gaussian, 25 hotspots, sigma 225u), 100% query rate, 10u squares, seed 3",
+    "C20": "skewed 10M objects (gaussian, 25 hotspots, sigma 225u), 100% query rate, 20u squares, seed 3",
+    "E": "50M objects: 40M uniform (seed 5) + 10M extreme hotspot (1 hotspot, sigma 100u, seed 6), 100% rate, 1u",
 }
 
 
@@ -135,12 +151,31 @@ class ClockSampler:
 
 
 def gen_ticks(name: str, count: int, seed_offset: int = 0):
-    from paper_1411_3212_b200.workload import WorkloadConfig, iter_ticks
+    import numpy as np
 
-    kw = dict(WORKLOADS[name])
-    kw["seed"] = kw["seed"] + seed_offset
-    cfg = WorkloadConfig(n_ticks=count, **kw)
-    return list(iter_ticks(cfg))
+    from paper_1411_3212_b200.workload import ColumnarTick, WorkloadConfig, iter_ticks
+
+    spec = WORKLOADS[name]
+    parts = spec if isinstance(spec, list) else [spec]
+    streams = []
+    for kw in parts:
+        kw = dict(kw)
+        kw["seed"] = kw["seed"] + seed_offset
+        streams.append(list(iter_ticks(WorkloadConfig(n_ticks=count, **kw))))
+    if len(streams) == 1:
+        return streams[0]
+    ticks = []
+    for k in range(count):
+        ts, off = [s_[k] for s_ in streams], 0
+        cols = {c: [] for c in ("ids", "xs", "ys", "qids", "qxa", "qya", "qxb", "qyb")}
+        for t in ts:
+            cols["ids"].append(t.ids + off)
+            cols["qids"].append(t.qids + off)
+            for c in ("xs", "ys", "qxa", "qya", "qxb", "qyb"):
+                cols[c].append(getattr(t, c))
+            off += t.n_objects
+        ticks.append(ColumnarTick(k, **{c: np.concatenate(v) for c, v in cols.items()}))
+    return ticks
 
 
 def cpu_reference_sample(n_objects: int, seed: int = 3):

@@ -1045,6 +1045,51 @@ constexpr int kDQWarps = kDQThreads / 32;
 constexpr int kDQStage = 1024;   // results staged per warp window
 constexpr int kLaneRuns = 4;     // lane-per-query k-way merge up to this many runs
 
+constexpr int kRankRuns = 32;  // lists of 5..32 runs: warp rank merge; more runs: k_merge_big
+
+// Warp-cooperative merge of one list whose k <= 32 sorted runs lie
+// concatenated in src[0, cnt) (shared or global memory; values distinct
+// across runs): element i lands at its rank = its index in its own run + the
+// number of smaller values in each other run (binary searches).
+template <typename T, typename Emit>
+__device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, const int32_t* counts, Emit emit) {
+  const int lane = lane_id();
+  const int c = lane < k ? counts[lane] : 0;
+  const int inc = warp_incl_scan(c);
+  const int st = inc - c;  // lane j < k: start of run j
+  for (int i0 = 0; i0 < cnt; i0 += 32) {
+    const int i = i0 + lane;
+    const bool ok = i < cnt;
+    const T v = ok ? src[i] : T(0);
+    int j = 0;  // own run: the last run starting at or before i
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int sj = __shfl_sync(0xffffffffu, st, (j + step) & 31);
+      if (j + step < k && sj <= i) j += step;
+    }
+    int rank = i - __shfl_sync(0xffffffffu, st, j);
+    for (int jj = 0; jj < k; ++jj) {
+      const int a0 = __shfl_sync(0xffffffffu, st, jj);
+      const int nx = __shfl_sync(0xffffffffu, st, (jj + 1) & 31);
+      const int a1 = jj + 1 < k ? nx : cnt;
+      if (ok && jj != j) {
+        int first = a0, len = a1 - a0;  // lower_bound(v) in run jj
+        while (len > 0) {
+          const int half = len >> 1;
+          if (src[first + half] < v) {
+            first += half + 1;
+            len -= half + 1;
+          } else {
+            len = half;
+          }
+        }
+        rank += first - a0;
+      }
+    }
+    if (ok) emit(rank, v);
+  }
+}
+
 // Per-query decode + merge (Alg. 4 and merge_results, decode.py:40-123).
 // A warp owns 32 consecutive queries; their lists are adjacent in the output
 // (and so are their subquery slots), so it cuts them into windows of at most
@@ -1098,6 +1143,8 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
         const int kq = __shfl_sync(0xffffffffu, k, l0);
         const int32_t sq0 = __shfl_sync(0xffffffffu, s0, l0);
         const int64_t cq = __shfl_sync(0xffffffffu, cnt, l0);
+        const bool rmerge = mono && kq > 1 && kq <= kRankRuns && cq < (int64_t(1) << 30);
+        int64_t* cat = rmerge ? d.scratch : d.out_ids;  // runs concatenated here
         int64_t pos = base;
         for (int j = 0; j < kq; ++j) {
           const int32_t s = sq0 + j;
@@ -1122,14 +1169,19 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
             while (w) {
               const int bit = __ffs(w) - 1;
               w &= w - 1;
-              d.out_ids[p++] = idof(sidx[obase + (b << 5) + bit]);
+              cat[p++] = idof(sidx[obase + (b << 5) + bit]);
             }
             got += __shfl_sync(0xffffffffu, inc, 31);
           }
           bad |= (lane == 0) && (got != cj);  // CountMismatch (bitmap.py:131-132)
           pos += cj;
         }
-        if (lane == 0 && cq > 1 && (kq > 1 || !mono)) {
+        if (rmerge) {
+          __syncwarp();
+          int64_t* out = d.out_ids + base;
+          warp_rank_merge(d.scratch + base, (int)cq, kq, d.sq_count + sq0,
+                          [&](int r, int64_t v) { out[r] = v; });
+        } else if (lane == 0 && cq > 1 && (kq > 1 || !mono)) {
           const int idx = atomicAdd(&h->n_big, 1);
           d.big_list[idx] = (int32_t)(q0 + l0);
         }
@@ -1223,12 +1275,12 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
       // ---- D: per query with 2..4 runs, merge the runs by head over the stored concatenation
       if (act && cnt > 1) {
         const int qs = (int)(qo - base);
-        if (!mono || k > kLaneRuns) {
+        if (!mono || k > kRankRuns) {
           if (k > 1 || !mono) {
             const int idx = atomicAdd(&h->n_big, 1);
             d.big_list[idx] = (int32_t)ql;
           }
-        } else if (k > 1) {
+        } else if (k > 1 && k <= kLaneRuns) {
           int pos[kLaneRuns], end[kLaneRuns];
           int32_t head[kLaneRuns];
           int acc = qs;
@@ -1259,6 +1311,19 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
               }
           }
         }
+      }
+      // lists of 5..32 runs: the warp merges them one at a time by rank
+      unsigned rq = __ballot_sync(0xffffffffu, act && cnt > 1 && mono && k > kLaneRuns && k <= kRankRuns);
+      while (rq) {
+        const int src = __ffs(rq) - 1;
+        rq &= rq - 1;
+        const int kq = __shfl_sync(0xffffffffu, k, src);
+        const int32_t sq0 = __shfl_sync(0xffffffffu, s0, src);
+        const int64_t qoq = __shfl_sync(0xffffffffu, qo, src);
+        const int cq = (int)__shfl_sync(0xffffffffu, cnt, src);
+        int64_t* out = d.out_ids + qoq;
+        warp_rank_merge(sa + (qoq - base), cq, kq, d.sq_count + sq0,
+                        [&](int r, int32_t v) { out[r] = idof(v); });
       }
       __syncwarp();
       l0 = l1;
