@@ -17,7 +17,7 @@ import numpy as np
 from . import errors
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libtickjoin_b200.so")
+LIB_PATH = os.environ.get("TJ_LIB_PATH") or os.path.join(LIB_DIR, "libtickjoin_b200.so")  # override: experiments
 
 TJ_MEM_HOST = 0
 TJ_MEM_DEVICE = 1

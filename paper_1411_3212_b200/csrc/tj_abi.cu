@@ -42,6 +42,7 @@ struct tj_ctx {
   tj_config cfg{};
   int device = 0;
   int num_sms = 148;
+  int join_blocks = 4;  // resident k_join CTAs per SM (occupancy API)
   cudaStream_t st = nullptr;
   cudaEvent_t ev[7] = {};
   DevHdr* d_hdr = nullptr;
@@ -347,13 +348,14 @@ int launch_stage(tj_ctx* c, int stage) {
       k_cell_level<<<Gbig, 256, 0, st>>>(d);
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
-      radix_sort(c, ObjKey{d.code, d.zmap, h}, d.okey, d.oval, &h->n, c->obj_passes);
+      k_obj_keys<<<Gn, 256, 0, st>>>(d);
+      radix_sort(c, ArrKey{d.okey[0]}, d.okey, d.oval, &h->n, c->obj_passes);
       scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
                   st);
       k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
       k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
       // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-      return 14 + F + (D > 0 ? D + 2 : 0) + 5 * c->obj_passes;
+      return 15 + F + (D > 0 ? D + 2 : 0) + 5 * c->obj_passes;
     case 1:  // ---- K2: query -> leaf scatter, subquery directory ----------
       k_query_count<<<Gm, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
@@ -381,7 +383,7 @@ int launch_stage(tj_ctx* c, int stage) {
       return 9 + extra;
     }
     case 3:  // ---- K3: join ---------------------------------------------
-      k_join<<<c->num_sms * 5, kJT, sizeof(JoinSmem), st>>>(d);
+      k_join<<<c->num_sms * c->join_blocks, kJT, sizeof(JoinSmem), st>>>(d);
       return 1;
     case 4:  // ---- K4: offsets, decode + canonical lists ------------------
       k_cov_counts<<<Gbig, 256, 0, st>>>(d);
@@ -555,6 +557,8 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->join_blocks, k_join, kJT, sizeof(JoinSmem));
+  if (c->join_blocks < 1) c->join_blocks = 1;
 
   int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);

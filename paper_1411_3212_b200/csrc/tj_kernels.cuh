@@ -386,8 +386,16 @@ struct ZOut {
   }
 };
 
-// object -> leaf rank (quadtree.py:161-165): the first radix pass computes
-// it on the fly from the l_max code and the zmap (the value is the input row)
+// object -> leaf rank (quadtree.py:161-165) as the radix key; the value of
+// the first radix pass is the input row itself (implicit)
+__global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const int64_t n = h->n;
+  const int sh = 2 * (h->l_max - h->l_deep);
+  TJ_GRID_STRIDE(i, n) d.okey[0][i] = d.zmap[d.code[i] >> sh] & kPayloadMask;
+}
+
 struct ObjKey {
   const uint32_t* code;
   const uint32_t* zmap;
@@ -732,7 +740,10 @@ constexpr int kJT = 256;                      // join CTA threads
 constexpr int kJW = kJT / 32;
 constexpr int kTileBlocks = 12;               // object tile: 12 blocks = 384 objects (th_quad)
 constexpr int kTileObj = kTileBlocks * 32;
-constexpr int kNK = 256;                      // buckets per axis
+#ifndef TJ_NK
+#define TJ_NK 128
+#endif
+constexpr int kNK = TJ_NK;                    // buckets per axis
 constexpr int kRows = kNK + 2;                // prefix rows k = 0 .. kNK + 1
 constexpr int kQC = 512;                      // subqueries per chunk
 constexpr int kTableMinQ = 12;                // table path from this many subqueries
