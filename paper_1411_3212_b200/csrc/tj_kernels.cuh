@@ -736,7 +736,10 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
 // from eight table loads, and only the few objects that share a bucket with
 // a bound (A = (Pre_kb+1 & ~Pre_ka)_x & (...)_y & ~D) get the exact fp64
 // test.  Bit-identical to the direct test by construction.
-constexpr int kJT = 256;                      // join CTA threads
+#ifndef TJ_JT
+#define TJ_JT 128
+#endif
+constexpr int kJT = TJ_JT;                    // join CTA threads
 constexpr int kJW = kJT / 32;
 constexpr int kTileBlocks = 12;               // object tile: 12 blocks = 384 objects (th_quad)
 constexpr int kTileObj = kTileBlocks * 32;
