@@ -371,27 +371,68 @@ def run_ours(args):
                                      *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST), \
                     sum(x.numel() * x.element_size() for x in a)
 
-        tick_host(0)
-        torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        h2d = d2h = eq = 0
-        for k in range(e_steps):
-            (out, st), hb = tick_host(k)
-            h2d += hb
-            d2h += 8 * (out.n_q + 1) + 8 * out.n_results
-            eq += int(st.n_queries)
-        e1.record(stream)
-        torch.cuda.synchronize()
-        e_ms = e0.elapsed_time(e1)
+        if sharded or args.e2e_contexts <= 1:
+            tick_host(0)
+            torch.cuda.synchronize()
+            if world > 1:
+                torch.distributed.barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            h2d = d2h = eq = 0
+            for k in range(e_steps):
+                (out, st), hb = tick_host(k)
+                h2d += hb
+                d2h += 8 * (out.n_q + 1) + 8 * out.n_results
+                eq += int(st.n_queries)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_ms = e0.elapsed_time(e1)
+        else:
+            # P contexts (each its own stream and pinned result buffers), one host thread each,
+            # ticks dealt round-robin: one tick's upload, another's compute and a third's result
+            # download overlap (PCIe is full duplex).  ctypes releases the GIL during tj_tick.
+            import threading
+
+            ctxs = [ctx] + [_native.NativeContext(384, 12, True, 0, local) for _ in range(args.e2e_contexts - 1)]
+
+            def host_tick(cx, k):
+                a = hticks[k % pool]
+                out, st = cx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
+                                       *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST)
+                return out, st, sum(x.numel() * x.element_size() for x in a)
+
+            for cx in ctxs:
+                host_tick(cx, 0)
+            torch.cuda.synchronize()
+            acc = [[0, 0, 0] for _ in ctxs]
+
+            def worker(j):
+                for k in range(j, e_steps, len(ctxs)):
+                    out, st, hb = host_tick(ctxs[j], k)
+                    acc[j][0] += hb
+                    acc[j][1] += 8 * (out.n_q + 1) + 8 * out.n_results
+                    acc[j][2] += int(st.n_queries)
+
+            ths = [threading.Thread(target=worker, args=(j,)) for j in range(len(ctxs))]
+            t0 = time.perf_counter()
+            for th in ths:
+                th.start()
+            for th in ths:
+                th.join()
+            torch.cuda.synchronize()
+            e_ms = (time.perf_counter() - t0) * 1e3
+            h2d, d2h, eq = (sum(a_[i] for a_ in acc) for i in range(3))
+            for cx in ctxs[1:]:
+                cx.close()
         if world > 1:
             t = torch.tensor([e_ms], device=dev)
             torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
             e_ms = float(t.item())
         e2e = {"value": eq / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d // e_steps,
                "d2h_bytes_per_step": d2h // e_steps, "steps": e_steps,
+               "timing": ("wall clock over all steps" if (not sharded and args.e2e_contexts > 1)
+                          else "CUDA events on the library stream"),
+               "contexts": 1 if sharded else args.e2e_contexts,
                "api": ("tj_tick (C ABI): pinned host inputs -> device, results CSR -> pinned host"
                        + ("; per rank: H2D of its 1/G slice, NCCL all-gather, D2H of its leaf-range CSR"
                           if sharded else ""))}
@@ -452,7 +493,10 @@ def main(argv=None):
     ap.add_argument("--pool", type=int, default=3, help="distinct ticks generated and cycled")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--ref-sample", type=int, default=500_000)
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-contexts", type=int, default=2,
+                    help="tj_tick contexts driven from this many host threads in the e2e leg (overlap of "
+                         "uploads, compute and downloads across ticks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sharded", action="store_true",
