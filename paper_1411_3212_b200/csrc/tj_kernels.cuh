@@ -1060,6 +1060,7 @@ constexpr int kDQStage = 1024;   // results staged per warp window
 constexpr int kLaneRuns = 4;     // lane-per-query k-way merge up to this many runs
 
 constexpr int kRankRuns = 32;  // lists of 5..32 runs: warp rank merge; more runs: k_merge_big
+constexpr int kLaneList = 128; // longer lists are merged by the whole warp (rank merge), not one lane
 
 // Warp-cooperative merge of one list whose k <= 32 sorted runs lie
 // concatenated in src[0, cnt) (shared or global memory; values distinct
@@ -1294,7 +1295,7 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
             const int idx = atomicAdd(&h->n_big, 1);
             d.big_list[idx] = (int32_t)ql;
           }
-        } else if (k > 1 && k <= kLaneRuns) {
+        } else if (k > 1 && k <= kLaneRuns && cnt <= kLaneList) {
           int pos[kLaneRuns], end[kLaneRuns];
           int32_t head[kLaneRuns];
           int acc = qs;
@@ -1327,7 +1328,8 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
         }
       }
       // lists of 5..32 runs: the warp merges them one at a time by rank
-      unsigned rq = __ballot_sync(0xffffffffu, act && cnt > 1 && mono && k > kLaneRuns && k <= kRankRuns);
+      unsigned rq = __ballot_sync(0xffffffffu, act && cnt > 1 && mono && k > 1 && k <= kRankRuns &&
+                                                   (k > kLaneRuns || cnt > kLaneList));
       while (rq) {
         const int src = __ffs(rq) - 1;
         rq &= rq - 1;
