@@ -145,11 +145,14 @@ struct ExclOut {
 // ballots (stable: warp w / round k / lane order), stages the tile by digit in
 // shared memory and writes digit runs coalesced.
 // ---------------------------------------------------------------------------
-constexpr int kRadixBits = 8;                       // 2 passes cover 16-bit keys (leaf ranks)
+#ifndef TJ_RADIX_BITS
+#define TJ_RADIX_BITS 8
+#endif
+constexpr int kRadixBits = TJ_RADIX_BITS;           // 8: 2 passes cover 16-bit keys (leaf ranks)
 constexpr int kRadixDigits = 1 << kRadixBits;       // 512
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
-constexpr int kRadixDPT = kRadixDigits / kRadixThreads;  // digits per thread (1)
+constexpr int kRadixDPT = kRadixDigits > kRadixThreads ? kRadixDigits / kRadixThreads : 1;  // digits per thread
 constexpr int kRadixIPT = 16;                       // items per thread per tile
 constexpr int kRadixTile = kRadixThreads * kRadixIPT;  // 4096
 
@@ -182,10 +185,12 @@ k_radix_upsweep(KeySrc keys, const int64_t* n_ptr, const DevHdr* h, int shift,
 #pragma unroll
   for (int j = 0; j < kRadixDPT; ++j) {
     const int dgt = threadIdx.x + j * kRadixThreads;
-    uint32_t s = 0;
+    if (dgt < kRadixDigits) {
+      uint32_t s = 0;
 #pragma unroll
-    for (int ww = 0; ww < kRadixWarps; ++ww) s += cnt[ww][dgt];
-    hist[(int64_t)dgt * G + blockIdx.x] = s;
+      for (int ww = 0; ww < kRadixWarps; ++ww) s += cnt[ww][dgt];
+      hist[(int64_t)dgt * G + blockIdx.x] = s;
+    }
   }
 }
 
@@ -209,7 +214,8 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
   const int t = threadIdx.x, w = t >> 5, lane = t & 31;
 #pragma unroll
   for (int j = 0; j < kRadixDPT; ++j)
-    base[t + j * kRadixThreads] = (uint32_t)offs[(int64_t)(t + j * kRadixThreads) * G + blockIdx.x];
+    if (t + j * kRadixThreads < kRadixDigits)
+      base[t + j * kRadixThreads] = (uint32_t)offs[(int64_t)(t + j * kRadixThreads) * G + blockIdx.x];
   const uint32_t lt = (1u << lane) - 1u;
   // keys/values of the current tile are loaded one tile ahead (all IPT loads in flight)
   uint32_t key[kRadixIPT];
@@ -260,16 +266,18 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
     for (int j = 0; j < kRadixDPT; ++j) {
       const int dgt = t + j * kRadixThreads;
       uint32_t acc = 0;
+      if (dgt < kRadixDigits) {
 #pragma unroll
-      for (int ww = 0; ww < kRadixWarps; ++ww) {
-        const uint32_t c = wcnt[ww][dgt];
-        wcnt[ww][dgt] = acc;
-        acc += c;
+        for (int ww = 0; ww < kRadixWarps; ++ww) {
+          const uint32_t c = wcnt[ww][dgt];
+          wcnt[ww][dgt] = acc;
+          acc += c;
+        }
       }
       run[j] = acc;
       int64_t tot;
       const int64_t ex = block_excl_scan((int64_t)acc, shs, &tot);
-      tprefix[dgt] = (uint32_t)(ex + carry);
+      if (dgt < kRadixDigits) tprefix[dgt] = (uint32_t)(ex + carry);
       carry += tot;
     }
     __syncthreads();
@@ -293,7 +301,8 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < kRadixDPT; ++j) base[t + j * kRadixThreads] += run[j];
+    for (int j = 0; j < kRadixDPT; ++j)
+      if (t + j * kRadixThreads < kRadixDigits) base[t + j * kRadixThreads] += run[j];
     __syncthreads();
   }
 }
