@@ -413,7 +413,18 @@ __global__ void __launch_bounds__(256) k_gather(const Dev d, const T* __restrict
   DevHdr* h = d.h;
   if (h->abort) return;
   const int64_t n = h->n;
-  TJ_GRID_STRIDE(p, n) dst[p] = src[d.sidx[p]];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
+    int32_t r[4];  // four independent gathers in flight per thread
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = p0 + u * stride < n ? d.sidx[p0 + u * stride] : 0;
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = p0 + u * stride < n ? __ldcg(src + r[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (p0 + u * stride < n) __stcs(dst + p0 + u * stride, v[u]);
+  }
 }
 
 // checks after a size became known: abort bits make the rest of the tick a no-op
@@ -1247,7 +1258,7 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
             const uint32_t jt = __shfl_sync(0xffffffffu, tail, j);
             const int wb = t - jx;
             w[u] = 0;
-            if (t < TW) w[u] = jw >= 0 ? d.bitmap[jw + wb] : (wb == jn - 1 ? jt : 0xffffffffu);
+            if (t < TW) w[u] = jw >= 0 ? __ldcs(d.bitmap + jw + wb) : (wb == jn - 1 ? jt : 0xffffffffu);  // read once: evict first
             wo[u] = jo + (wb << 5);
           }
 #pragma unroll
