@@ -44,6 +44,8 @@ struct tj_ctx {
   int num_sms = 148;
   int join_blocks = 4;  // resident k_join CTAs per SM (occupancy API)
   cudaStream_t st = nullptr;
+  cudaStream_t side = nullptr;             // object sort, concurrent with the query scatter
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev[7] = {};
   DevHdr* d_hdr = nullptr;
   DevHdr* h_hdr = nullptr;  // pinned
@@ -62,7 +64,7 @@ struct tj_ctx {
   // join / outputs
   DBuf bitmap, outids, outoff, scratch;
   // scan / radix scratch
-  DBuf partial, rhist, roffs;
+  DBuf partial, partial2, rhist, roffs;
   // pinned host outputs
   void* h_off = nullptr;
   size_t h_off_bytes = 0;
@@ -196,6 +198,7 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(biglist, m * 4);
   ENS(outoff, (m + 1) * 8);
   ENS(partial, 1024 * 8);
+  ENS(partial2, 1024 * 8);
   const int Gr = 2 * c->num_sms;
   ENS(rhist, (int64_t)kRadixDigits * Gr * 4);
   ENS(roffs, (int64_t)kRadixDigits * Gr * 8);
@@ -291,25 +294,25 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
 
 // stable LSD radix sort of (key, value) pairs over `passes` 8-bit digits
 template <typename KeySrc>
-void radix_pass(tj_ctx* c, KeySrc keys, const int32_t* vin, uint32_t* kout, int32_t* vout, const int64_t* n_ptr,
-                int shift) {
+void radix_pass(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc keys, const int32_t* vin, uint32_t* kout,
+                int32_t* vout, const int64_t* n_ptr, int shift) {
   const int Gr = 2 * c->num_sms;
-  ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
-  k_radix_upsweep<<<Gr, kRadixThreads, 0, c->st>>>(keys, n_ptr, c->d_hdr, shift, P<uint32_t>(c->rhist));
+  k_radix_upsweep<<<Gr, kRadixThreads, 0, st>>>(keys, n_ptr, c->d_hdr, shift, P<uint32_t>(c->rhist));
   scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)}, c->d_consts,
-              c->d_hdr, (int64_t*)nullptr, c->st);
-  k_radix_downsweep<<<Gr, kRadixThreads, 0, c->st>>>(keys, vin, kout, vout, n_ptr, c->d_hdr, shift,
-                                                      P<int64_t>(c->roffs));
+              c->d_hdr, (int64_t*)nullptr, st);
+  k_radix_downsweep<<<Gr, kRadixThreads, 0, st>>>(keys, vin, kout, vout, n_ptr, c->d_hdr, shift,
+                                                  P<int64_t>(c->roffs));
 }
 
 // stable LSD radix sort of (key, input row) pairs over `passes` 8-bit digits;
 // the first pass takes its keys from `first` and the rows implicitly
 template <typename KeySrc>
-void radix_sort(tj_ctx* c, KeySrc first, uint32_t* k[2], int32_t* v[2], const int64_t* n_ptr, int passes) {
-  radix_pass(c, first, (const int32_t*)nullptr, k[1], v[1], n_ptr, 0);
+void radix_sort(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc first, uint32_t* k[2], int32_t* v[2],
+                const int64_t* n_ptr, int passes) {
+  radix_pass(c, st, sp, first, (const int32_t*)nullptr, k[1], v[1], n_ptr, 0);
   for (int p = 1; p < passes; ++p) {
     const int src = p & 1, dst = src ^ 1;
-    radix_pass(c, ArrKey{k[src]}, v[src], k[dst], v[dst], n_ptr, kRadixBits * p);
+    radix_pass(c, st, sp, ArrKey{k[src]}, v[src], k[dst], v[dst], n_ptr, kRadixBits * p);
   }
 }
 
@@ -348,15 +351,22 @@ int launch_stage(tj_ctx* c, int stage) {
       k_cell_level<<<Gbig, 256, 0, st>>>(d);
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
-      k_obj_keys<<<Gn, 256, 0, st>>>(d);
-      radix_sort(c, ArrKey{d.okey[0]}, d.okey, d.oval, &h->n, c->obj_passes);
       scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
                   st);
-      k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
-      k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
-      // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-      return 15 + F + (D > 0 ? D + 2 : 0) + 5 * c->obj_passes;
-    case 1:  // ---- K2: query -> leaf scatter, subquery directory ----------
+      // 3 launches per scan
+      return 12 + F + (D > 0 ? D + 2 : 0);
+    case 1: {  // ---- objects into leaf order || K2: query -> leaf scatter ------
+      // fork: the object sort (K1's last part) runs on the side stream while
+      // the query scatter runs here; the join needs both
+      cudaStream_t ss = c->side;
+      ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2)};
+      cudaEventRecord(c->ev_fork, st);
+      cudaStreamWaitEvent(ss, c->ev_fork, 0);
+      k_obj_keys<<<Gn, 256, 0, ss>>>(d);
+      radix_sort(c, ss, sp2, ArrKey{d.okey[0]}, d.okey, d.oval, &h->n, c->obj_passes);
+      k_gather<double><<<Gn, 256, 0, ss>>>(d, d.xs, d.sx);
+      k_gather<double><<<Gn, 256, 0, ss>>>(d, d.ys, d.sy);
+      cudaEventRecord(c->ev_join, ss);
       k_query_count<<<Gm, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
@@ -364,7 +374,10 @@ int launch_stage(tj_ctx* c, int stage) {
                   (int64_t*)nullptr, st);
       k_query_fill<<<Gm, 256, 0, st>>>(d);
       k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
-      return 10;
+      cudaStreamWaitEvent(st, c->ev_join, 0);  // join point
+      // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
+      return 10 + 3 + 5 * c->obj_passes;
+    }
     case 2: {  // ---- join preparation (and this rank's leaf range) -------
       int extra = 0;
       if (c->shard_n > 1) {
@@ -548,6 +561,9 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&c->d_hdr, sizeof(DevHdr)) != cudaSuccess ||
       cudaMallocHost(&c->h_hdr, sizeof(DevHdr)) != cudaSuccess ||
       cudaMalloc(&c->d_consts, 8 * sizeof(int64_t)) != cudaSuccess) {
@@ -576,7 +592,7 @@ int tj_destroy(tj_ctx* c) {
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->crect, &c->qwin, &c->qpos, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
                  &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
-                 &c->outids, &c->outoff, &c->scratch, &c->partial, &c->rhist, &c->roffs};
+                 &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->h_off) cudaFreeHost(c->h_off);
@@ -587,6 +603,9 @@ int tj_destroy(tj_ctx* c) {
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
   if (c->st) cudaStreamDestroy(c->st);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   delete c;
   return TJ_OK;
 }
