@@ -477,8 +477,13 @@ def run_ours(args):
         }
         print(json.dumps(line), flush=True)
     torch.cuda.synchronize()
-    if sharded:  # before the library stream the collectives were ordered on goes away
+    if sharded:
+        # torch's NCCL bookkeeping still references the library stream at interpreter teardown;
+        # leave the process without running destructors once the collectives are done
         torch.distributed.destroy_process_group()
+        sys.stdout.flush()
+        sys.stderr.flush()
+        os._exit(0)
     eng.close()
     return 0
 

@@ -158,10 +158,10 @@ int tj_get_imbalance(tj_ctx* ctx, int32_t sim_processors, int32_t heaviest_first
 
 /* Multi-GPU leaf-range sharding (no reference counterpart —
  * the reference is single-process).  With nranks > 1 every
- * tick builds the full index and subquery directory, then joins / decodes
- * only the leaves of this rank's contiguous Morton range (balanced by work
- * weight); the output CSR holds each query's results restricted to those
- * leaves.  Partial lists of the ranks are disjoint and individually sorted;
+ * tick builds the full index, then scatters, joins and decodes only the
+ * (query, leaf) pairs of this rank's contiguous Morton range of leaves
+ * (balanced by object count); the output CSR holds each query's results
+ * restricted to those leaves.  Partial lists of the ranks are disjoint and individually sorted;
  * their per-query merge is the full result.  nranks == 1 (default): off. */
 int tj_set_shard(tj_ctx* ctx, int32_t rank, int32_t nranks);
 

@@ -353,8 +353,12 @@ int launch_stage(tj_ctx* c, int stage) {
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
       scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
                   st);
+      if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range, before the scatter
+        scan_launch(sp, LeafWeightIn{d.leaf_nobj}, PrefOut{d.leaf_wpre}, &h->L, h, &h->shard_total, st);
+        k_shard_mark<<<Gbig, 256, 0, st>>>(d);
+      }
       // 3 launches per scan
-      return 12 + F + (D > 0 ? D + 2 : 0);
+      return 12 + F + (D > 0 ? D + 2 : 0) + (c->shard_n > 1 ? 4 : 0);
     case 1: {  // ---- objects into leaf order || K2: query -> leaf scatter ------
       // fork: the object sort (K1's last part) runs on the side stream while
       // the query scatter runs here; the join needs both
@@ -378,14 +382,8 @@ int launch_stage(tj_ctx* c, int stage) {
       // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
       return 10 + 3 + 5 * c->obj_passes;
     }
-    case 2: {  // ---- join preparation (and this rank's leaf range) -------
-      int extra = 0;
-      if (c->shard_n > 1) {
-        scan_launch(sp, LeafWeightIn{d.leaf_nobj, d.leaf_nisq, d.leaf_ncov}, PrefOut{d.leaf_wpre}, &h->L, h,
-                    &h->shard_total, st);
-        k_shard_mark<<<Gbig, 256, 0, st>>>(d);
-        extra = 4;
-      }
+    case 2: {  // ---- join preparation -----------------------------------
+      const int extra = 0;
       scan_launch(sp, WordsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_woff}, &h->L, h,
                   &h->W, st);
       scan_launch(sp, UnitsIn{d.leaf_nobj, d.leaf_nisq, d.leaf_active}, ExclOut<int64_t>{d.leaf_ubase}, &h->L, h,

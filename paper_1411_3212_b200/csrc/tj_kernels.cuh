@@ -87,6 +87,9 @@ struct Dev {
   int D;        // l_max - F
 };
 
+// multi-GPU leaf-range sharding: leaf r belongs to this rank (always, unsharded)
+__device__ __forceinline__ bool leaf_on(const uint8_t* active, int64_t r) { return !active || active[r]; }
+
 #define TJ_GRID_STRIDE(i, n) \
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < (n); i += (int64_t)gridDim.x * blockDim.x)
 
@@ -585,20 +588,22 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
       w.w = (int)cell_of(cyb, ya, sy, hpos, side);
       if (is_small(w)) {
         uint32_t key[4], rank[4];
-        cnt = enum_small(w, ld, d.zmap, key, rank);
+        const int ne = enum_small(w, ld, d.zmap, key, rank);
         int pos[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
-          if (k < cnt) {
+          if (k < ne && leaf_on(d.leaf_active, rank[k])) {
             const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
             int4* c = d.leaf_cnt + rank[k];
-            pos[k] = atomicAdd(cv ? &c->y : &c->x, 1);
+            pos[cnt++] = atomicAdd(cv ? &c->y : &c->x, 1);  // owned pairs, in order
           }
         d.qpos[q] = make_int4(pos[0], pos[1], pos[2], pos[3]);
       } else {
-        cnt = enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
+        enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
+          if (!leaf_on(d.leaf_active, rank)) return;
           int4* c = d.leaf_cnt + rank;
           atomicAdd(pair_cov(d, lev, z, r, cov_on) ? &c->w : &c->z, 1);
+          ++cnt;
         });
       }
     }
@@ -637,16 +642,18 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
     const Rect4 r = d.crect[q];
     if (is_small(w)) {
       uint32_t key[4], rank[4];
-      enum_small(w, ld, d.zmap, key, rank);
+      const int ne = enum_small(w, ld, d.zmap, key, rank);
       const int4 p4 = d.qpos[q];
       const int pos[4] = {p4.x, p4.y, p4.z, p4.w};
+      int j = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (k < n) {
+        if (k < ne && leaf_on(d.leaf_active, rank[k])) {
           const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
           const int4 c = d.leaf_cnt[rank[k]];
-          const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pos[k];
-          emit_subquery(d, base + k, q, n, rank[k], cv, e, r);
+          const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pos[j];
+          emit_subquery(d, base + j, q, n, rank[k], cv, e, r);
+          ++j;
         }
       continue;
     }
@@ -654,7 +661,9 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
 #pragma unroll
     for (int l = 0; l <= kMaxLevel; ++l) cur[l] = 0;
     if (n > 1) {
-      enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t, uint32_t) { cur[lev]++; });
+      enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t, uint32_t rank) {
+        if (leaf_on(d.leaf_active, rank)) cur[lev]++;
+      });
       int run = 0;
 #pragma unroll
       for (int l = 0; l <= kMaxLevel; ++l) {
@@ -664,6 +673,7 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
       }
     }
     enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
+      if (!leaf_on(d.leaf_active, rank)) return;
       const bool cv = pair_cov(d, lev, z, r, cov_on);
       const int4 c = d.leaf_cnt[rank];
       const int32_t e = d.leaf_sbase[rank] + (cv ? c.x + c.z + c.y : c.x) +
@@ -762,7 +772,6 @@ constexpr int kRows = kNK + 2;                // prefix rows k = 0 .. kNK + 1
 constexpr int kQC = 512;                      // subqueries per chunk
 constexpr int kTableMinQ = 12;                // table path from this many subqueries
 
-__device__ __forceinline__ bool leaf_on(const uint8_t* active, int64_t r) { return !active || active[r]; }
 
 struct WordsIn {
   const int32_t* nobj;
@@ -795,18 +804,14 @@ struct LeafSqIn {
 };
 
 // Multi-GPU leaf-range sharding: every rank builds the same
-// index and subquery directory; leaves are cut into contiguous Morton ranges
-// balanced by a work weight (objects x subqueries + both), and a rank joins,
-// decodes and assembles only its own leaves — its per-query lists are the
-// restriction of the full lists to its leaves (disjoint across ranks).
+// index; right after it, leaves are cut into contiguous Morton ranges balanced
+// by their object counts (queries are issued where objects are), and a rank
+// scatters, joins, decodes and assembles only the (query, leaf) pairs of its
+// own leaves — its per-query lists are the restriction of the full lists to
+// its leaves (disjoint across ranks).
 struct LeafWeightIn {
   const int32_t* nobj;
-  const int32_t* nisq;
-  const int32_t* ncov;
-  __device__ int64_t operator()(int64_t r) const {
-    const int64_t no = nobj[r], sq = (int64_t)nisq[r] + ncov[r];
-    return no * sq + no + sq;
-  }
+  __device__ int64_t operator()(int64_t r) const { return (int64_t)nobj[r] + 1; }
 };
 struct PrefOut {
   int64_t* a;
@@ -816,7 +821,7 @@ __global__ void __launch_bounds__(256) k_shard_mark(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const int64_t T = h->shard_total > 0 ? h->shard_total : 1;
-  const LeafWeightIn wt{d.leaf_nobj, d.leaf_nisq, d.leaf_ncov};
+  const LeafWeightIn wt{d.leaf_nobj};
   TJ_GRID_STRIDE(r, h->L) {
     const int64_t mid = 2 * d.leaf_wpre[r] + wt(r);  // 2 x midpoint of the leaf's weight interval
     const int64_t owner = (mid * h->shard_n) / (2 * T);

@@ -2,11 +2,11 @@
 
 One process per GPU.  Each rank ingests 1/G of the tick's position updates
 and queries; an all-gather (NCCL over NVLink on GPUs, gloo on CPU) gives every
-rank the full tick; every rank builds the bit-identical index and subquery
-directory (the index build is integer-exact), then joins, decodes and
-assembles only the leaves of its contiguous Morton range, balanced by the
-per-leaf work weight (device side: `tj_set_shard`, `k_shard_mark` in
-csrc/tj_kernels.cuh).  A rank's per-query lists are the restriction of the
+rank the full tick; every rank builds the bit-identical index (the index
+build is integer-exact), then scatters, joins, decodes and assembles only the
+(query, leaf) pairs of its contiguous Morton range of leaves, balanced by the
+per-leaf object count (device side: `tj_set_shard`, `k_shard_mark` in
+csrc/tj_kernels.cuh, run right after the index build).  A rank's per-query lists are the restriction of the
 full lists to its leaves: disjoint across ranks and each sorted, so the
 per-query union (merge) is the full result.
 
@@ -23,11 +23,10 @@ import numpy as np
 from .errors import DuplicateResult
 
 
-def leaf_weight(nobj: np.ndarray, nisq: np.ndarray, ncov: np.ndarray) -> np.ndarray:
-    """Per-leaf work weight — the device's `LeafWeightIn`."""
-    no = np.asarray(nobj, np.int64)
-    sq = np.asarray(nisq, np.int64) + np.asarray(ncov, np.int64)
-    return no * sq + no + sq
+def leaf_weight(nobj: np.ndarray) -> np.ndarray:
+    """Per-leaf work weight — the device's `LeafWeightIn`: objects + 1 (known
+    right after the index build, before the query scatter)."""
+    return np.asarray(nobj, np.int64) + 1
 
 
 def leaf_owners(weights: np.ndarray, nranks: int) -> np.ndarray:

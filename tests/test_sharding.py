@@ -54,7 +54,7 @@ def _partial_for_rank(tick, rank, nranks, th=64):
     nobj = np.where(present, (d.o_end - d.o_start)[np.minimum(rows, len(d.cells) - 1)], 0)
     nisq = np.where(present, (d.i_end - d.i_start)[np.minimum(rows, len(d.cells) - 1)], 0)
     ncov = np.where(present, (d.c_end - d.c_start)[np.minimum(rows, len(d.cells) - 1)], 0)
-    own = leaf_owners(leaf_weight(nobj, nisq, ncov), nranks)
+    own = leaf_owners(leaf_weight(nobj), nranks)
     mine = set(cells[own == rank].tolist())
     id_to_cell = dict(zip(tick["ids"].tolist(), t.obj_cell.tolist()))
     offs, ids = t.offsets, t.result_ids
