@@ -35,6 +35,8 @@ struct TickGraph {
   Dev dv;
   int64_t n = 0, m = 0;
   int obj_passes = 0, shard_n = 0, launches[6] = {};
+  const void* scan_state[2] = {nullptr, nullptr};  // host-side buffers baked into the graph
+  int64_t scan_words = 0;
   cudaGraphExec_t exec[6] = {};
 };
 
@@ -64,7 +66,9 @@ struct tj_ctx {
   // join / outputs
   DBuf bitmap, outids, outoff, scratch;
   // scan / radix scratch
-  DBuf partial, partial2, rhist, roffs;
+  DBuf partial, partial2, rhist, roffs, sstate, sstate2;
+  int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
+  bool lb_scan = false;    // single-pass look-back scan (measured slower here than reduce-then-scan)
   // pinned host outputs
   void* h_off = nullptr;
   size_t h_off_bytes = 0;
@@ -223,6 +227,14 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sinv, c->cap_S * 4);
   ENS(slotoff, (c->cap_S + 1) * 8);
   ENS(bitmap, c->cap_W * 4);
+  {  // look-back scan state: enough tiles for the longest scanned array
+    const int64_t Zmax = int64_t(1) << (2 * c->cfg.l_max);
+    const int64_t longest = std::max({c->cap_S + 1, c->m + 1, c->n + 1, Zmax, c->cap_L,
+                                      (int64_t)kRadixDigits * 2 * c->num_sms});
+    c->scan_words = (longest + kScanTile - 1) / kScanTile + 2;
+    ENS(sstate, c->scan_words * 8);
+    ENS(sstate2, c->scan_words * 8);
+  }
   ENS(unitleaf, c->cap_U * 4);
   ENS(scratch, c->cap_R * 8);
   ENS(outids, c->cap_R * 8);
@@ -331,7 +343,8 @@ int launch_stage(tj_ctx* c, int stage) {
   const int64_t n = c->n, m = c->m;
   const int Gn = grid_for(c, n), Gm = grid_for(c, m);
   const int Gbig = c->num_sms * 8;
-  ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial)};
+  ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial),
+              c->lb_scan ? P<unsigned long long>(c->sstate) : nullptr, c->scan_words};
   switch (stage) {
     case 0:  // ---- K0 / K1: index build ------------------------------------
       cudaMemsetAsync(d.pyr + pyr_off(F), 0, (pyr_off(F + 1) - pyr_off(F)) * 4, st);  // the histogram level
@@ -363,7 +376,8 @@ int launch_stage(tj_ctx* c, int stage) {
       // fork: the object sort (K1's last part) runs on the side stream while
       // the query scatter runs here; the join needs both
       cudaStream_t ss = c->side;
-      ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2)};
+      ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
+                   c->lb_scan ? P<unsigned long long>(c->sstate2) : nullptr, c->scan_words};
       cudaEventRecord(c->ev_fork, st);
       cudaStreamWaitEvent(ss, c->ev_fork, 0);
       k_obj_keys<<<Gn, 256, 0, ss>>>(d);
@@ -447,6 +461,7 @@ int check_launch(tj_ctx* c) {
 
 bool same_shape(const TickGraph& g, const tj_ctx* c) {
   return g.n == c->n && g.m == c->m && g.obj_passes == c->obj_passes && g.shard_n == c->shard_n &&
+         g.scan_state[0] == c->sstate.p && g.scan_state[1] == c->sstate2.p && g.scan_words == c->scan_words &&
          std::memcmp(&g.dv, &c->dv, sizeof(Dev)) == 0;
 }
 
@@ -486,6 +501,9 @@ int run_tick(tj_ctx* c, int64_t* launches) {
       ng.m = c->m;
       ng.obj_passes = c->obj_passes;
       ng.shard_n = c->shard_n;
+      ng.scan_state[0] = c->sstate.p;
+      ng.scan_state[1] = c->sstate2.p;
+      ng.scan_words = c->scan_words;
       if (capture_tick(c, ng)) {
         if (c->graphs.size() >= 4) {
           for (auto& e : c->graphs.front().exec)
@@ -556,6 +574,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   c->cfg = *cfg;
   c->device = cfg->device;
   if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
+  if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
@@ -590,7 +609,7 @@ int tj_destroy(tj_ctx* c) {
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->crect, &c->qwin, &c->qpos, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
                  &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
-                 &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs};
+                 &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->h_off) cudaFreeHost(c->h_off);

@@ -595,7 +595,10 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
           if (k < ne && leaf_on(d.leaf_active, rank[k])) {
             const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
             int4* c = d.leaf_cnt + rank[k];
-            pos[cnt++] = atomicAdd(cv ? &c->y : &c->x, 1);  // owned pairs, in order
+            const int v = atomicAdd(cv ? &c->y : &c->x, 1);  // owned pairs, in order
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pos[j] = (j == cnt) ? v : pos[j];  // (no local-memory indexing)
+            ++cnt;
           }
         d.qpos[q] = make_int4(pos[0], pos[1], pos[2], pos[3]);
       } else {
@@ -651,7 +654,8 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
         if (k < ne && leaf_on(d.leaf_active, rank[k])) {
           const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
           const int4 c = d.leaf_cnt[rank[k]];
-          const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pos[j];
+          const int pj = j == 0 ? pos[0] : j == 1 ? pos[1] : j == 2 ? pos[2] : pos[3];
+          const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pj;
           emit_subquery(d, base + j, q, n, rank[k], cv, e, r);
           ++j;
         }

@@ -113,14 +113,105 @@ k_scan_down(In in, Out out, const int64_t* n_ptr, const DevHdr* h, const int64_t
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-pass exclusive scan with decoupled look-back: tiles are claimed in
+// order from an atomic counter; a tile publishes its aggregate, walks back
+// over its predecessors' published aggregates / inclusive prefixes to get its
+// exclusive prefix, publishes its inclusive prefix, and writes its outputs.
+// Reads the input once (the three-kernel scan reads it twice).  state[0] is
+// the tile counter, state[1 + t] tile t's (flag << 62 | value); the state is
+// cleared (one memset) before every scan.
+// ---------------------------------------------------------------------------
+constexpr unsigned long long kLbAgg = 1ull << 62, kLbInc = 2ull << 62, kLbVal = (1ull << 62) - 1;
+
+template <typename In, typename Out>
+__global__ void __launch_bounds__(kScanThreads)
+k_scan_lb(In in, Out out, const int64_t* n_ptr, DevHdr* h, int64_t* total_out, unsigned long long* state) {
+  if (h->abort) return;
+  __shared__ int64_t sh[33];
+  __shared__ int64_t tile[kScanTile];
+  __shared__ int64_t s_tile, s_excl;
+  const int64_t n = *n_ptr;
+  const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+  if (ntiles == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0 && total_out) *total_out = 0;
+    return;
+  }
+  const int t = threadIdx.x;
+  unsigned long long* st = state + 1;
+  for (;;) {
+    if (t == 0) s_tile = (int64_t)atomicAdd(&state[0], 1ull);
+    __syncthreads();
+    const int64_t tl = s_tile;
+    if (tl >= ntiles) break;
+    const int64_t base = tl * kScanTile;
+    int64_t v[kScanItems];
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + t;
+      v[k] = i < n ? in(i) : 0;
+      tile[k * kScanThreads + t] = v[k];
+    }
+    __syncthreads();
+    int64_t blk[kScanItems];
+    int64_t loc = 0;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      blk[k] = tile[t * kScanItems + k];
+      loc += blk[k];
+    }
+    int64_t tot;
+    int64_t ex = block_excl_scan(loc, sh, &tot);  // (contains __syncthreads)
+    if (t == 0) {
+      int64_t excl = 0;
+      if (tl == 0) {
+        atomicExch(&st[0], kLbInc | (unsigned long long)tot);
+      } else {
+        atomicExch(&st[tl], kLbAgg | (unsigned long long)tot);
+        for (int64_t pp = tl - 1;;) {
+          const unsigned long long sv = *(volatile unsigned long long*)&st[pp];
+          if (sv == 0) continue;  // predecessor not published yet
+          excl += (int64_t)(sv & kLbVal);
+          if (sv & kLbInc) break;
+          --pp;
+        }
+        atomicExch(&st[tl], kLbInc | (unsigned long long)(excl + tot));
+      }
+      s_excl = excl;
+      if (tl == ntiles - 1 && total_out) *total_out = excl + tot;
+    }
+    __syncthreads();
+    ex += s_excl;
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      tile[t * kScanItems + k] = ex;
+      ex += blk[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kScanItems; ++k) {
+      const int64_t i = base + k * kScanThreads + t;
+      if (i < n) out(i, tile[k * kScanThreads + t], v[k]);
+    }
+    __syncthreads();
+  }
+}
+
 struct ScanPlan {
   int G;
-  int64_t* partial;  // G entries
+  int64_t* partial;             // G entries (three-kernel scan)
+  unsigned long long* state;    // look-back scan: counter + tile states
+  int64_t state_words;
 };
 
 template <typename In, typename Out>
 inline void scan_launch(const ScanPlan& p, In in, Out out, const int64_t* n_ptr, DevHdr* h,
                         int64_t* total_out, cudaStream_t st) {
+  if (p.state) {
+    cudaMemsetAsync(p.state, 0, (size_t)p.state_words * 8, st);
+    k_scan_lb<In, Out><<<p.G, kScanThreads, 0, st>>>(in, out, n_ptr, h, total_out, p.state);
+    return;
+  }
   k_scan_reduce<In><<<p.G, kScanThreads, 0, st>>>(in, n_ptr, h, p.partial);
   k_scan_partials<<<1, 1024, 0, st>>>(p.partial, p.G, total_out, h);
   k_scan_down<In, Out><<<p.G, kScanThreads, 0, st>>>(in, out, n_ptr, h, p.partial);
