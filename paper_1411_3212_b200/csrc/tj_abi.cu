@@ -60,7 +60,7 @@ struct tj_ctx {
   // index
   DBuf linfo, pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf crect, qwin, qpos, nsub, qsbase, biglist, leafcnt;
+  DBuf qpos, nsub, qsbase, biglist, leafcnt;
   // subqueries
   DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, leafcur, unitleaf;
   // join / outputs
@@ -193,8 +193,6 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(leafcur, c->cap_L * 2 * 4);
   ENS(lactive, c->cap_L);
   ENS(lwpre, c->cap_L * 8);
-  ENS(crect, m * sizeof(Rect4));
-  ENS(qwin, m * sizeof(int4));
   ENS(qpos, m * sizeof(int4));
   ENS(leafcnt, c->cap_L * sizeof(int4));
   ENS(nsub, m * 4);
@@ -275,8 +273,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.leaf_sbase = P<int32_t>(c->lsbase);
   d.leaf_woff = P<int64_t>(c->lwoff);
   d.leaf_ubase = P<int64_t>(c->lubase);
-  d.crect = P<Rect4>(c->crect);
-  d.qwin = P<int4>(c->qwin);
   d.nsub = P<int32_t>(c->nsub);
   d.qsbase = P<int32_t>(c->qsbase);
   d.sq_leaf = P<int32_t>(c->sqleaf);
@@ -607,7 +603,7 @@ int tj_destroy(tj_ctx* c) {
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->crect, &c->qwin, &c->qpos, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
+                 &c->lubase, &c->qpos, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
                  &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)

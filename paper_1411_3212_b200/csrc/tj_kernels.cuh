@@ -56,8 +56,6 @@ struct Dev {
   int64_t* leaf_woff;
   int64_t* leaf_ubase;
   // queries
-  Rect4* crect;
-  int4* qwin;
   int32_t* nsub;
   int32_t* qsbase;
   // subqueries
@@ -544,6 +542,28 @@ __device__ __forceinline__ bool covers(const Rect4& q, int lev, uint32_t z, cons
   return (q.xa <= lxa) && (q.xb >= ux) && (q.ya <= lya) && (q.yb >= uy);
 }
 
+// Clip (geometry.py:80-88: max/min against the index MBR) and the deepest-
+// cell window of the clipped rect (quadtree.py:182-183).  Both scatter passes
+// recompute it from the input rect (cheaper than storing and re-reading it).
+// Returns false for a query disjoint from the MBR.
+__device__ __forceinline__ bool clip_window(const Dev& d, int64_t q, double xa, double ya, double xb, double yb,
+                                            double sx, double sy, int wpos, int hpos, uint32_t side, Rect4& r,
+                                            int4& w) {
+  double cxa = d.qxa[q], cya = d.qya[q], cxb = d.qxb[q], cyb = d.qyb[q];
+  cxa = cxa < xa ? xa : cxa;  // max(q.xa, mbr.xa)
+  cya = cya < ya ? ya : cya;
+  cxb = cxb > xb ? xb : cxb;  // min(q.xb, mbr.xb)
+  cyb = cyb > yb ? yb : cyb;
+  r.xa = cxa; r.ya = cya; r.xb = cxb; r.yb = cyb;
+  w = make_int4(-1, -1, -1, -1);
+  if (cxa > cxb || cya > cyb) return false;
+  w.x = (int)cell_of(cxa, xa, sx, wpos, side);
+  w.y = (int)cell_of(cxb, xa, sx, wpos, side);
+  w.z = (int)cell_of(cya, ya, sy, hpos, side);
+  w.w = (int)cell_of(cyb, ya, sy, hpos, side);
+  return true;
+}
+
 // Counting sort of the (query, leaf) pairs into per-leaf directory blocks
 // (directory.py:119-158), two passes over the queries:
 //  count: every pair bumps its leaf's intersecting or covering counter.  A
@@ -571,21 +591,10 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
   const uint32_t side = 1u << ld;
   const int cov_on = h->covering;
   TJ_GRID_STRIDE(q, m) {
-    double cxa = d.qxa[q], cya = d.qya[q], cxb = d.qxb[q], cyb = d.qyb[q];
-    cxa = cxa < xa ? xa : cxa;  // max(q.xa, mbr.xa)
-    cya = cya < ya ? ya : cya;
-    cxb = cxb > xb ? xb : cxb;  // min(q.xb, mbr.xb)
-    cyb = cyb > yb ? yb : cyb;
     Rect4 r;
-    r.xa = cxa; r.ya = cya; r.xb = cxb; r.yb = cyb;
-    d.crect[q] = r;
+    int4 w;
     int cnt = 0;
-    int4 w = make_int4(-1, -1, -1, -1);
-    if (!(cxa > cxb || cya > cyb)) {
-      w.x = (int)cell_of(cxa, xa, sx, wpos, side);
-      w.y = (int)cell_of(cxb, xa, sx, wpos, side);
-      w.z = (int)cell_of(cya, ya, sy, hpos, side);
-      w.w = (int)cell_of(cyb, ya, sy, hpos, side);
+    if (clip_window(d, q, xa, ya, xb, yb, sx, sy, wpos, hpos, side, r, w)) {
       if (is_small(w)) {
         uint32_t key[4], rank[4];
         const int ne = enum_small(w, ld, d.zmap, key, rank);
@@ -610,7 +619,6 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
         });
       }
     }
-    d.qwin[q] = w;
     d.nsub[q] = cnt;
   }
 }
@@ -637,12 +645,17 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   const int64_t m = h->m;
   const int ld = h->l_deep;
   const int cov_on = h->covering;
+  const double xa = h->xa, ya = h->ya, xb = h->xb, yb = h->yb;
+  const double sx = h->sx_deep, sy = h->sy_deep;
+  const int wpos = h->wpos, hpos = h->hpos;
+  const uint32_t side = 1u << ld;
   TJ_GRID_STRIDE(q, m) {
     const int n = d.nsub[q];
     if (n == 0) continue;
-    const int4 w = d.qwin[q];
+    Rect4 r;
+    int4 w;
+    clip_window(d, q, xa, ya, xb, yb, sx, sy, wpos, hpos, side, r, w);
     const int32_t base = d.qsbase[q];
-    const Rect4 r = d.crect[q];
     if (is_small(w)) {
       uint32_t key[4], rank[4];
       const int ne = enum_small(w, ld, d.zmap, key, rank);
