@@ -108,6 +108,7 @@ typedef struct tj_stats {
   int64_t kernel_launches;     /* kernels this call launched (all attempts)    */
   double t_build_ms;           /* index build alone (K0 + K1: MBR .. leaf directory of objects) */
   double t_scatter_ms;         /* query -> leaf scatter + subquery directory (K2) */
+  double t_sort_ms;            /* objects into leaf order (K1's last part, concurrent with K2) */
 } tj_stats;
 
 /* Reference-order index view (QuadIndex, quadtree.py:41-67). */

@@ -34,10 +34,10 @@ struct DBuf {
 struct TickGraph {
   Dev dv;
   int64_t n = 0, m = 0;
-  int obj_passes = 0, shard_n = 0, launches[6] = {};
+  int obj_passes = 0, shard_n = 0, launches[7] = {};
   const void* scan_state[2] = {nullptr, nullptr};  // host-side buffers baked into the graph
   int64_t scan_words = 0;
-  cudaGraphExec_t exec[6] = {};
+  cudaGraphExec_t exec[7] = {};
 };
 
 struct tj_ctx {
@@ -48,7 +48,7 @@ struct tj_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t side = nullptr;             // object sort, concurrent with the query scatter
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev[7] = {};
+  cudaEvent_t ev[9] = {};
   DevHdr* d_hdr = nullptr;
   DevHdr* h_hdr = nullptr;  // pinned
   int64_t* d_consts = nullptr;
@@ -68,7 +68,8 @@ struct tj_ctx {
   // scan / radix scratch
   DBuf partial, partial2, rhist, roffs, sstate, sstate2;
   int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
-  bool lb_scan = false;    // single-pass look-back scan (measured slower here than reduce-then-scan)
+  bool lb_scan = false;
+  bool serial_sort = false;  // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)    // single-pass look-back scan (measured slower here than reduce-then-scan)
   // pinned host outputs
   void* h_off = nullptr;
   size_t h_off_bytes = 0;
@@ -328,6 +329,7 @@ void radix_sort(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc first, ui
 // preparation, join, decode, merge); no host synchronisation inside.  Stage
 // boundaries carry the timing events.  Returns the kernels launched.
 constexpr int kStages = 6;
+constexpr int kSortStage = 6;  // the object sort: its own graph, on the side stream
 
 int launch_stage(tj_ctx* c, int stage) {
   cudaStream_t st = c->st;
@@ -368,19 +370,18 @@ int launch_stage(tj_ctx* c, int stage) {
       }
       // 3 launches per scan
       return 12 + F + (D > 0 ? D + 2 : 0) + (c->shard_n > 1 ? 4 : 0);
-    case 1: {  // ---- objects into leaf order || K2: query -> leaf scatter ------
-      // fork: the object sort (K1's last part) runs on the side stream while
-      // the query scatter runs here; the join needs both
-      cudaStream_t ss = c->side;
+    case kSortStage: {  // ---- K1's last part: objects into leaf order (side stream) ----
+      cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
                    c->lb_scan ? P<unsigned long long>(c->sstate2) : nullptr, c->scan_words};
-      cudaEventRecord(c->ev_fork, st);
-      cudaStreamWaitEvent(ss, c->ev_fork, 0);
       k_obj_keys<<<Gn, 256, 0, ss>>>(d);
       radix_sort(c, ss, sp2, ArrKey{d.okey[0]}, d.okey, d.oval, &h->n, c->obj_passes);
       k_gather<double><<<Gn, 256, 0, ss>>>(d, d.xs, d.sx);
       k_gather<double><<<Gn, 256, 0, ss>>>(d, d.ys, d.sy);
-      cudaEventRecord(c->ev_join, ss);
+      // 5 launches per radix pass (upsweep + 3-kernel scan + downsweep)
+      return 3 + 5 * c->obj_passes;
+    }
+    case 1: {  // ---- K2: query -> leaf scatter (concurrent with the object sort) ----
       k_query_count<<<Gm, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
@@ -388,9 +389,7 @@ int launch_stage(tj_ctx* c, int stage) {
                   (int64_t*)nullptr, st);
       k_query_fill<<<Gm, 256, 0, st>>>(d);
       k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
-      cudaStreamWaitEvent(st, c->ev_join, 0);  // join point
-      // 3 launches per scan, 5 per radix pass (upsweep + scan + downsweep)
-      return 10 + 3 + 5 * c->obj_passes;
+      return 10;
     }
     case 2: {  // ---- join preparation -----------------------------------
       const int extra = 0;
@@ -471,11 +470,12 @@ void drop_graphs(tj_ctx* c) {
 // Capture every stage of the launch sequence as its own CUDA graph (the
 // timing events sit between the stage graphs, on the stream).
 bool capture_tick(tj_ctx* c, TickGraph& g) {
-  for (int s = 0; s < kStages; ++s) {
+  for (int s = 0; s <= kSortStage; ++s) {
+    cudaStream_t cs = (s == kSortStage && !c->serial_sort) ? c->side : c->st;
     cudaGraph_t graph = nullptr;
-    if (cudaStreamBeginCapture(c->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
+    if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
     g.launches[s] = launch_stage(c, s);
-    cudaError_t e = cudaStreamEndCapture(c->st, &graph);
+    cudaError_t e = cudaStreamEndCapture(cs, &graph);
     if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec[s], graph, 0);
     if (graph) cudaGraphDestroy(graph);
     if (e != cudaSuccess) return false;
@@ -516,15 +516,28 @@ int run_tick(tj_ctx* c, int64_t* launches) {
       }
     }
   }
-  cudaEventRecord(c->ev[0], c->st);
-  for (int s = 0; s < kStages; ++s) {
+  auto stage = [&](int s, cudaStream_t cs) -> int {
     if (g) {
       *launches += g->launches[s];
-      cudaError_t e = cudaGraphLaunch(g->exec[s], c->st);
+      cudaError_t e = cudaGraphLaunch(g->exec[s], cs);
       if (e != cudaSuccess) return fail(c, TJ_E_CUDA, std::string("cudaGraphLaunch: ") + cudaGetErrorString(e));
     } else {
       *launches += launch_stage(c, s);
     }
+    return TJ_OK;
+  };
+  int rc;
+  cudaEventRecord(c->ev[0], c->st);
+  for (int s = 0; s < kStages; ++s) {
+    if (s == 1) {  // fork: the object sort on the side stream, concurrent with the query scatter
+      cudaStream_t ss = c->serial_sort ? c->st : c->side;
+      cudaStreamWaitEvent(ss, c->ev[kStageEvent[0]], 0);
+      cudaEventRecord(c->ev[7], ss);
+      if ((rc = stage(kSortStage, ss))) return rc;
+      cudaEventRecord(c->ev[8], ss);
+    }
+    if (s == 2) cudaStreamWaitEvent(c->st, c->ev[8], 0);  // join: the join needs both
+    if ((rc = stage(s, c->st))) return rc;
     cudaEventRecord(c->ev[kStageEvent[s]], c->st);
   }
   return check_launch(c);
@@ -571,6 +584,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   c->device = cfg->device;
   if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
   if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
+  if (const char* ss = std::getenv("TJ_SERIAL_SORT")) c->serial_sort = std::atoi(ss) != 0;
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
@@ -727,6 +741,9 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     cudaEventElapsedTime(&kb, c->ev[0], c->ev[6]);
     S.t_build_ms = kb;
     S.t_scatter_ms = ms[0] - kb;
+    float ks = 0;
+    cudaEventElapsedTime(&ks, c->ev[7], c->ev[8]);
+    S.t_sort_ms = ks;
     S.t_total_ms = tot;
     S.task_objects = (int64_t)H.task_obj;
     S.task_subqueries = (int64_t)H.task_isq;
