@@ -1099,6 +1099,73 @@ constexpr int kLaneList = 128; // longer lists are merged by the whole warp (ran
 // concatenated in src[0, cnt) (shared or global memory; values distinct
 // across runs): element i lands at its rank = its index in its own run + the
 // number of smaller values in each other run (binary searches).
+// In-place pairwise merging of a list of k sorted runs (values distinct)
+// held in shared memory a[0, cnt), cnt <= 256: each round merges runs
+// (0,1), (2,3), ... — every element moves to (its index in its run) + (the
+// number of smaller values in the partner run), one binary search each — so
+// k runs take ceil(log2 k) rounds instead of k - 1 searches per element.
+// Elements ride in registers (8 per lane) between a round's reads and writes.
+constexpr int kPairMax = 256;
+__device__ __forceinline__ void warp_pair_merge(int32_t* a, int cnt, int k, const int32_t* counts) {
+  const int lane = lane_id();
+  const int c = lane < k ? counts[lane] : 0;
+  const int inc = warp_incl_scan(c);
+  int st = inc - c;  // lane j < k: start of run j (lanes >= k: cnt)
+  if (lane >= k) st = cnt;
+  for (int nr = k; nr > 1; nr = (nr + 1) >> 1) {
+    int32_t v[kPairMax / 32];
+    int np[kPairMax / 32];
+#pragma unroll
+    for (int u = 0; u < kPairMax / 32; ++u) {
+      const int i = u * 32 + lane;
+      int j = 0;  // own run: the last run starting at or before i (every lane shuffles)
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const int sj = __shfl_sync(0xffffffffu, st, (j + step) & 31);
+        if (j + step < nr && sj <= i) j += step;
+      }
+      v[u] = i < cnt ? a[i] : 0;
+      np[u] = i < cnt ? j : -1;  // temporarily the run index
+    }
+    // partner runs and searches (shuffles need every lane: done outside the predicate)
+#pragma unroll
+    for (int u = 0; u < kPairMax / 32; ++u) {
+      const int i = u * 32 + lane;
+      const int j = np[u] < 0 ? 0 : np[u];
+      const int pj = j ^ 1;
+      const int s_j = __shfl_sync(0xffffffffu, st, j & 31);
+      const int s_p = __shfl_sync(0xffffffffu, st, pj & 31);
+      const int e_p = __shfl_sync(0xffffffffu, st, (pj + 1) & 31);
+      const int s_pair = __shfl_sync(0xffffffffu, st, (j & ~1) & 31);
+      if (np[u] >= 0) {
+        int rank = i - s_j;
+        if (pj < nr) {
+          int first = s_p, len = (pj + 1 < nr ? e_p : cnt) - s_p;  // lower_bound(v) in the partner run
+          while (len > 0) {
+            const int half = len >> 1;
+            if (a[first + half] < v[u]) {
+              first += half + 1;
+              len -= half + 1;
+            } else {
+              len = half;
+            }
+          }
+          rank += first - s_p;
+        }
+        np[u] = s_pair + rank;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int u = 0; u < kPairMax / 32; ++u)
+      if (np[u] >= 0) a[np[u]] = v[u];
+    __syncwarp();
+    // merged run r' = old runs 2r', 2r'+1: start = old start of 2r'
+    const int ns = __shfl_sync(0xffffffffu, st, (2 * lane) & 31);
+    st = (2 * lane < nr && lane < 16) ? ns : cnt;
+  }
+}
+
 template <typename T, typename Emit>
 __device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, const int32_t* counts, Emit emit) {
   const int lane = lane_id();
@@ -1371,8 +1438,14 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
         const int64_t qoq = __shfl_sync(0xffffffffu, qo, src);
         const int cq = (int)__shfl_sync(0xffffffffu, cnt, src);
         int64_t* out = d.out_ids + qoq;
-        warp_rank_merge(sa + (qoq - base), cq, kq, d.sq_count + sq0,
-                        [&](int r, int32_t v) { out[r] = idof(v); });
+        if (cq <= kPairMax && kq >= 3) {  // log2(k) rounds of pairwise merges in place, then store
+          int32_t* lst = sa + (qoq - base);
+          warp_pair_merge(lst, cq, kq, d.sq_count + sq0);
+          for (int i = lane; i < cq; i += 32) out[i] = idof(lst[i]);
+        } else {
+          warp_rank_merge(sa + (qoq - base), cq, kq, d.sq_count + sq0,
+                          [&](int r, int32_t v) { out[r] = idof(v); });
+        }
       }
       __syncwarp();
       l0 = l1;
