@@ -875,11 +875,14 @@ struct JoinSmem {
 // keep it monotone (fl(v - base), the product, the clamps and the
 // truncation are all non-decreasing in v); the leaf's own extent makes the
 // buckets even.  Objects and bounds use the same map.
-__device__ __forceinline__ int bucket(double v, double base, double scale) {
-  double t = __dmul_rn(__dsub_rn(v, base), scale);
-  t = t > 0.0 ? t : 0.0;
-  t = t < (double)(kNK - 1) ? t : (double)(kNK - 1);
-  return 1 + __double2int_rz(t);
+// (evaluated in fp32: rounding to float, subtracting a constant and scaling by
+// a positive constant are each monotone, and monotonicity is all the bucket
+// tables need — the exact fp64 test settles every bit they cannot prove)
+__device__ __forceinline__ int bucket(double v, float base, float scale) {
+  float t = __fmul_rn(__fsub_rn(__double2float_rn(v), base), scale);
+  t = fmaxf(t, 0.0f);
+  t = fminf(t, (float)(kNK - 1));
+  return 1 + __float2int_rz(t);
 }
 
 __device__ __forceinline__ bool in_rect(double x, double y, const Rect4& R) {
@@ -920,7 +923,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       S.ox[i] = x;
       S.oy[i] = y;
     }
-    double bx = 0.0, by = 0.0, scx = 0.0, scy = 0.0;
+    float bx = 0.0f, by = 0.0f, scx = 0.0f, scy = 0.0f;
     if (table) {
       const uint32_t code = d.leaf_code[r];
       const int lev = (int)(code >> kLevelShift);
@@ -932,7 +935,8 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       const double f = (double)kNK / (double)(1u << (lmax - lev));
       scx = sxm * f;
       scy = sym * f;
-      for (int i = tid; i < 2 * kRows * nbt; i += kJT) S.tab[i] = 0u;
+      static_assert((2 * kRows) % 4 == 0, "table rows must allow 16-byte zeroing");
+      for (int i = tid; i < 2 * kRows * nbt / 4; i += kJT) reinterpret_cast<uint4*>(S.tab)[i] = make_uint4(0u, 0u, 0u, 0u);
       __syncthreads();
       // bucket scatter: Bk[axis][k][b] |= bit of each object
       for (int i = tid; i < P; i += kJT) {
