@@ -60,7 +60,7 @@ struct tj_ctx {
   // index
   DBuf linfo, pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf qpos, nsub, qsbase, biglist, leafcnt;
+  DBuf qpos, qwin, crect, nsub, qsbase, biglist, leafcnt;
   // subqueries
   DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, leafcur, unitleaf;
   // join / outputs
@@ -195,6 +195,8 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(lactive, c->cap_L);
   ENS(lwpre, c->cap_L * 8);
   ENS(qpos, m * sizeof(int4));
+  ENS(qwin, m * sizeof(int4));
+  ENS(crect, m * sizeof(Rect4));
   ENS(leafcnt, c->cap_L * sizeof(int4));
   ENS(nsub, m * 4);
   ENS(qsbase, m * 4);
@@ -294,6 +296,8 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.leaf_cur = P<int32_t>(c->leafcur);
   d.leaf_cnt = P<int4>(c->leafcnt);
   d.qpos = P<int4>(c->qpos);
+  d.qwin = P<int4>(c->qwin);
+  d.crect = P<Rect4>(c->crect);
   d.unit_leaf = P<int32_t>(c->unitleaf);
   d.big_list = P<int32_t>(c->biglist);
   d.leaf_active = c->shard_n > 1 ? P<uint8_t>(c->lactive) : nullptr;
@@ -617,7 +621,7 @@ int tj_destroy(tj_ctx* c) {
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->qpos, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
+                 &c->lubase, &c->qpos, &c->qwin, &c->crect, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
                  &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)

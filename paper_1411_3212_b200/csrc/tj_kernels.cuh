@@ -71,6 +71,8 @@ struct Dev {
   int32_t* leaf_cur;       // per leaf x {intersecting, covering}: fill cursor of large-window pairs
   int4* leaf_cnt;          // per leaf: intersecting / covering pairs of small windows, of large windows
   int4* qpos;              // per small-window query: each pair's place in its leaf block
+  int4* qwin;              // per query: deepest-cell window of its clipped rect (count pass -> fill pass)
+  Rect4* crect;            // per query: clipped rect (count pass -> fill pass)
   int32_t* unit_leaf;      // join work unit -> leaf
   uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
   int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
@@ -620,6 +622,8 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
       }
     }
     d.nsub[q] = cnt;
+    d.qwin[q] = w;
+    d.crect[q] = r;
   }
 }
 
@@ -652,9 +656,8 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   TJ_GRID_STRIDE(q, m) {
     const int n = d.nsub[q];
     if (n == 0) continue;
-    Rect4 r;
-    int4 w;
-    clip_window(d, q, xa, ya, xb, yb, sx, sy, wpos, hpos, side, r, w);
+    const Rect4 r = d.crect[q];  // clip and window from the count pass (one 32-byte and one 16-byte load)
+    const int4 w = d.qwin[q];
     const int32_t base = d.qsbase[q];
     if (is_small(w)) {
       uint32_t key[4], rank[4];
