@@ -62,7 +62,7 @@ struct tj_ctx {
   // queries
   DBuf qpos, qwin, crect, nsub, qsbase, biglist, leafcnt;
   // subqueries
-  DBuf sqleaf, sqq, sqcov, sqcount, ecount, erect, sinv, slotoff, leafcur, unitleaf;
+  DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf;
   // join / outputs
   DBuf bitmap, outids, outoff, scratch;
   // scan / radix scratch
@@ -219,13 +219,10 @@ int prepare_dynamic(tj_ctx* c) {
   int rc;
 #define ENS(buf, bytes) \
   if ((rc = ensure(c, c->buf, (size_t)(bytes))) != TJ_OK) return rc
-  ENS(sqleaf, c->cap_S * 4);
-  ENS(sqq, c->cap_S * 4);
-  ENS(sqcov, c->cap_S);
+  ENS(sqle, c->cap_S * 8);
   ENS(sqcount, c->cap_S * 4);
   ENS(erect, c->cap_S * sizeof(Rect4));
   ENS(ecount, c->cap_S * 4);
-  ENS(sinv, c->cap_S * 4);
   ENS(slotoff, (c->cap_S + 1) * 8);
   ENS(bitmap, c->cap_W * 4);
   {  // look-back scan state: enough tiles for the longest scanned array
@@ -278,13 +275,10 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.leaf_ubase = P<int64_t>(c->lubase);
   d.nsub = P<int32_t>(c->nsub);
   d.qsbase = P<int32_t>(c->qsbase);
-  d.sq_leaf = P<int32_t>(c->sqleaf);
-  d.sq_q = P<int32_t>(c->sqq);
-  d.sq_cov = P<uint8_t>(c->sqcov);
+  d.sq_le = P<int2>(c->sqle);
   d.sq_count = P<int32_t>(c->sqcount);
   d.erect = P<Rect4>(c->erect);
   d.ecount = P<int32_t>(c->ecount);
-  d.sinv = P<int32_t>(c->sinv);
   d.linfo = P<int4>(c->linfo);
   d.slot_off = P<int64_t>(c->slotoff);
   d.bitmap = P<uint32_t>(c->bitmap);
@@ -621,8 +615,8 @@ int tj_destroy(tj_ctx* c) {
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->heavy, &c->sub, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->qpos, &c->qwin, &c->crect, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqleaf, &c->sqq, &c->sqcov,
-                 &c->sqcount, &c->ecount, &c->erect, &c->sinv, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
+                 &c->lubase, &c->qpos, &c->qwin, &c->crect, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqle,
+                 &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
@@ -839,13 +833,13 @@ int load_leaves(tj_ctx* c, LeafView& lv) {
 
 // Directory entries of leaf r's block [e0, e0 + cnt) in the reference's
 // order (ascending slot = query input order, directory.py:131): the device
-// keeps fill order inside a block; entry -> slot is the inverse of sinv.
+// keeps fill order inside a block; entry -> slot inverts the slots' entries.
 int entry_slots(tj_ctx* c, std::vector<int32_t>& eslot) {
-  std::vector<int32_t> sinv;
+  std::vector<int2> le;
   int rc;
-  if ((rc = d2h(c, sinv, c->sinv.p, c->last.S))) return rc;
-  eslot.assign(sinv.size(), -1);
-  for (size_t s = 0; s < sinv.size(); ++s) eslot[sinv[s]] = (int32_t)s;
+  if ((rc = d2h(c, le, c->sqle.p, c->last.S))) return rc;
+  eslot.assign(le.size(), -1);
+  for (size_t s = 0; s < le.size(); ++s) eslot[le[s].y] = (int32_t)s;
   return TJ_OK;
 }
 std::vector<int32_t> block_in_ref_order(const std::vector<int32_t>& eslot, int64_t e0, int64_t cnt) {
@@ -921,15 +915,17 @@ int tj_get_subqueries(tj_ctx* c, int64_t* count, int64_t* q_row, int64_t* cell, 
   if (cap < S) return fail(c, TJ_E_INVALID_ARG, "subquery buffers too small");
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
-  std::vector<int32_t> leaf, q;
-  std::vector<uint8_t> cv;
-  if ((rc = d2h(c, leaf, c->sqleaf.p, S)) || (rc = d2h(c, q, c->sqq.p, S)) || (rc = d2h(c, cv, c->sqcov.p, S)))
-    return rc;
-  for (int64_t s = 0; s < S; ++s) {
-    if (q_row) q_row[s] = q[s];
-    if (cell) cell[s] = lv.packed[leaf[s]];
-    if (covering) covering[s] = cv[s] & 1;
-  }
+  std::vector<int2> le;
+  std::vector<int32_t> nsub;
+  if ((rc = d2h(c, le, c->sqle.p, S)) || (rc = d2h(c, nsub, c->nsub.p, c->m))) return rc;
+  int64_t s = 0;  // slots are grouped per query in input order (nsub each)
+  for (int64_t q = 0; q < c->m; ++q)
+    for (int32_t j = 0; j < nsub[q]; ++j, ++s) {
+      const int32_t leaf = le[s].x;
+      if (q_row) q_row[s] = q;
+      if (cell) cell[s] = lv.packed[leaf];
+      if (covering) covering[s] = (uint8_t)(le[s].y - lv.sbase[leaf] >= lv.nisq[leaf]);
+    }
   return TJ_OK;
 }
 

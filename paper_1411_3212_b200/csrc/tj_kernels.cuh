@@ -59,13 +59,11 @@ struct Dev {
   int32_t* nsub;
   int32_t* qsbase;
   // subqueries
-  int32_t* sq_leaf;
-  int32_t* sq_q;
-  uint8_t* sq_cov;
+  int2* sq_le;              // per subquery slot: (leaf rank, directory entry); query and covering flag are
+                            // implied (slot ranges per query; entry row >= the leaf's intersecting count)
   int32_t* sq_count;        // result count per subquery slot (popcount, or block size if covering)
   int32_t* ecount;          // result count per directory entry (entry order)
   Rect4* erect;             // clipped rect per directory entry (entry order, the join's input)
-  int32_t* sinv;            // per slot: its directory entry
   int4* linfo;              // per leaf: object base, object count, entry base, intersecting count
   int64_t* slot_off;        // per slot (S + 1): start of its run in the output CSR
   int32_t* leaf_cur;       // per leaf x {intersecting, covering}: fill cursor of large-window pairs
@@ -627,16 +625,9 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
   }
 }
 
-// Subquery flags: bit 0 covering, bit 1 the query has a single subquery
-// (its list needs no merge and is decoded straight into the output).
-constexpr uint8_t kFlagCov = 1, kFlagSingle = 2;
 
-__device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, int64_t q, int n, uint32_t rank, bool cv,
-                                              int32_t e, const Rect4& r) {
-  d.sq_leaf[slot] = (int32_t)rank;
-  d.sq_q[slot] = (int32_t)q;
-  d.sq_cov[slot] = (uint8_t)((cv ? kFlagCov : 0) | (n == 1 ? kFlagSingle : 0));
-  d.sinv[slot] = e;
+__device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, uint32_t rank, int32_t e, const Rect4& r) {
+  d.sq_le[slot] = make_int2((int32_t)rank, e);  // one 8-byte store
   d.erect[e] = r;  // the join's input, in entry order
 }
 
@@ -649,10 +640,6 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   const int64_t m = h->m;
   const int ld = h->l_deep;
   const int cov_on = h->covering;
-  const double xa = h->xa, ya = h->ya, xb = h->xb, yb = h->yb;
-  const double sx = h->sx_deep, sy = h->sy_deep;
-  const int wpos = h->wpos, hpos = h->hpos;
-  const uint32_t side = 1u << ld;
   TJ_GRID_STRIDE(q, m) {
     const int n = d.nsub[q];
     if (n == 0) continue;
@@ -672,7 +659,7 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
           const int4 c = d.leaf_cnt[rank[k]];
           const int pj = j == 0 ? pos[0] : j == 1 ? pos[1] : j == 2 ? pos[2] : pos[3];
           const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pj;
-          emit_subquery(d, base + j, q, n, rank[k], cv, e, r);
+          emit_subquery(d, base + j, rank[k], e, r);
           ++j;
         }
       continue;
@@ -698,7 +685,7 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
       const int4 c = d.leaf_cnt[rank];
       const int32_t e = d.leaf_sbase[rank] + (cv ? c.x + c.z + c.y : c.x) +
                         atomicAdd(&d.leaf_cur[2 * rank + (cv ? 1 : 0)], 1);
-      emit_subquery(d, base + cur[lev]++, q, n, rank, cv, e, r);
+      emit_subquery(d, base + cur[lev]++, rank, e, r);
     });
   }
 }
@@ -1082,7 +1069,7 @@ __global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
 __global__ void __launch_bounds__(256) k_slot_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  TJ_GRID_STRIDE(s, h->S) d.sq_count[s] = d.ecount[d.sinv[s]];
+  TJ_GRID_STRIDE(s, h->S) d.sq_count[s] = d.ecount[d.sq_le[s].y];
 }
 
 __global__ void k_close_offsets(const Dev d) {
@@ -1272,12 +1259,13 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
           const int32_t s = sq0 + j;
           const int64_t cj = d.sq_count[s];
           if (cj == 0) continue;
-          const int32_t leaf = d.sq_leaf[s];
+          const int2 le = d.sq_le[s];
+          const int32_t leaf = le.x;
           const int4 li = d.linfo[leaf];
           const int nobj = li.y;
           const int32_t obase = li.x;
           const int nbw = (nobj + 31) >> 5;
-          const int row = d.sinv[s] - li.z;
+          const int row = le.y - li.z;
           const bool cov = row >= li.w;
           const uint32_t* wpt = cov ? nullptr : d.bitmap + d.leaf_woff[leaf] + (int64_t)row * nbw;
           const uint32_t tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
@@ -1321,10 +1309,11 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
         int64_t wof = -1;
         uint32_t tail = 0;
         if (s < shi && d.sq_count[s] > 0) {
-          const int32_t leaf = d.sq_leaf[s];
+          const int2 le = d.sq_le[s];
+          const int32_t leaf = le.x;
           const int4 li = d.linfo[leaf];
           const int nobj = li.y;
-          const int row = d.sinv[s] - li.z;
+          const int row = le.y - li.z;
           obase = li.x;
           nbw = (nobj + 31) >> 5;
           tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
