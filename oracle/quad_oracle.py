@@ -192,6 +192,30 @@ def map_objects(xs, ys, index: OracleIndex) -> np.ndarray:
     return index.zmap[morton(i, j)]
 
 
+def leaf_occupancy(xs, ys, index: OracleIndex) -> np.ndarray:
+    """Object count per leaf, aligned with index.leaves (quadtree.py:243-247)."""
+    cells = map_objects(xs, ys, index)
+    rows = np.searchsorted(index.leaves, cells)
+    return np.bincount(rows, minlength=len(index.leaves)).astype(np.int64)
+
+
+def needs_rebuild(xs, ys, index: OracleIndex, overfull_factor: float = 2.0, overfull_fraction: float = 0.05,
+                  hard_factor: float = 8.0) -> bool:
+    """quadtree.py:250-270: objects escaped the old MBR, any leaf over
+    hard_factor * th_quad, or more than overfull_fraction of the leaves over
+    overfull_factor * th_quad."""
+    try:
+        counts = leaf_occupancy(xs, ys, index)
+    except OracleError as e:
+        if e.kind == "OutOfBounds":
+            return True
+        raise
+    if np.any(counts > hard_factor * index.th_quad):
+        return True
+    frac = float(np.mean(counts > overfull_factor * index.th_quad))
+    return frac > overfull_fraction
+
+
 def clip_rects(qxa, qya, qxb, qyb, mbr):
     """Intersect query rects with the index MBR; keep-mask of non-disjoint ones.
 

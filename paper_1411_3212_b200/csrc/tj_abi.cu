@@ -35,6 +35,7 @@ struct TickGraph {
   Dev dv;
   int64_t n = 0, m = 0;
   int obj_passes = 0, shard_n = 0, launches[7] = {};
+  bool reuse = false;
   const void* scan_state[2] = {nullptr, nullptr};  // host-side buffers baked into the graph
   int64_t scan_words = 0;
   cudaGraphExec_t exec[7] = {};
@@ -69,7 +70,12 @@ struct tj_ctx {
   DBuf partial, partial2, rhist, roffs, sstate, sstate2;
   int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
   bool lb_scan = false;
-  bool serial_sort = false;  // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)    // single-pass look-back scan (measured slower here than reduce-then-scan)
+  bool serial_sort = false;
+  // adaptive rebuild: the last built index (header fields + the buffers it lives in)
+  bool have_index = false;
+  bool reuse = false;  // this tick reuses it
+  DevHdr idx{};
+  const void* idx_bufs[3] = {nullptr, nullptr, nullptr};  // zmap, leaf codes, leaf counts  // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)    // single-pass look-back scan (measured slower here than reduce-then-scan)
   // pinned host outputs
   void* h_off = nullptr;
   size_t h_off_bytes = 0;
@@ -343,9 +349,18 @@ int launch_stage(tj_ctx* c, int stage) {
               c->lb_scan ? P<unsigned long long>(c->sstate) : nullptr, c->scan_words};
   switch (stage) {
     case 0:  // ---- K0 / K1: index build ------------------------------------
-      cudaMemsetAsync(d.pyr + pyr_off(F), 0, (pyr_off(F + 1) - pyr_off(F)) * 4, st);  // the histogram level
       cudaMemsetAsync(d.leaf_cur, 0, c->cap_L * 2 * 4, st);
       cudaMemsetAsync(d.leaf_cnt, 0, c->cap_L * sizeof(int4), st);
+      if (c->reuse) {  // adaptive: the old tree, leaf counts recounted by the check pass
+        scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
+                    st);
+        if (c->shard_n > 1) {
+          scan_launch(sp, LeafWeightIn{d.leaf_nobj}, PrefOut{d.leaf_wpre}, &h->L, h, &h->shard_total, st);
+          k_shard_mark<<<Gbig, 256, 0, st>>>(d);
+        }
+        return 3 + (c->shard_n > 1 ? 4 : 0);
+      }
+      cudaMemsetAsync(d.pyr + pyr_off(F), 0, (pyr_off(F + 1) - pyr_off(F)) * 4, st);  // the histogram level
       k_mbr<<<Gn, 256, 0, st>>>(d);
       k_finalize_mbr<<<1, 1, 0, st>>>(h);
       k_codes<<<Gn, 256, 0, st>>>(d);
@@ -440,6 +455,21 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.l_deep = 1;
   H.shard_rank = c->shard_rank;
   H.shard_n = c->shard_n;
+  if (c->reuse) {  // adaptive reuse: the index's MBR, scales, depth and leaves
+    const DevHdr& I = c->idx;
+    H.xa = I.xa; H.ya = I.ya; H.xb = I.xb; H.yb = I.yb;
+    H.width = I.width; H.height = I.height;
+    H.wpos = I.wpos; H.hpos = I.hpos;
+    H.sx_max = I.sx_max; H.sy_max = I.sy_max; H.sx_deep = I.sx_deep; H.sy_deep = I.sy_deep;
+    for (int l = 0; l <= kMaxLevel; ++l) {
+      H.lw[l] = I.lw[l];
+      H.lh[l] = I.lh[l];
+    }
+    H.l_deep = I.l_deep;
+    H.Z = I.Z;
+    H.L = I.L;
+    H.reuse_index = 1;
+  }
   const char* dbg = std::getenv("TJ_DEBUG");
   H.dbg = dbg ? std::atoi(dbg) : 0;
 }
@@ -454,6 +484,7 @@ int check_launch(tj_ctx* c) {
 
 bool same_shape(const TickGraph& g, const tj_ctx* c) {
   return g.n == c->n && g.m == c->m && g.obj_passes == c->obj_passes && g.shard_n == c->shard_n &&
+         g.reuse == c->reuse &&
          g.scan_state[0] == c->sstate.p && g.scan_state[1] == c->sstate2.p && g.scan_words == c->scan_words &&
          std::memcmp(&g.dv, &c->dv, sizeof(Dev)) == 0;
 }
@@ -495,6 +526,7 @@ int run_tick(tj_ctx* c, int64_t* launches) {
       ng.m = c->m;
       ng.obj_passes = c->obj_passes;
       ng.shard_n = c->shard_n;
+      ng.reuse = c->reuse;
       ng.scan_state[0] = c->sstate.p;
       ng.scan_state[1] = c->sstate2.p;
       ng.scan_words = c->scan_words;
@@ -689,6 +721,34 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     if ((rc = prepare_static(c, n, m))) return rc;
     if (c->last_L == 0) c->last_L = c->cap_L;
     c->obj_passes = passes_for(std::max<int64_t>(c->last_L, 1) - 1);  // grows (tick replay) if L crosses a digit
+    // adaptive rebuild (engine.py:163-174): check the previous index against this tick's objects
+    c->reuse = false;
+    if (c->cfg.rebuild == TJ_REBUILD_ADAPTIVE && c->have_index && c->idx_bufs[0] == c->zmap.p &&
+        c->idx_bufs[1] == c->lcode.p && c->idx_bufs[2] == c->lnobj.p) {
+      if ((rc = prepare_dynamic(c))) return rc;
+      fill_dev(c, ids, xs, ys, qxa, qya, qxb, qyb);
+      c->reuse = true;
+      init_hdr(c, n, m);
+      TJ_CUDA(cudaMemcpyAsync(c->d_hdr, c->h_hdr, sizeof(DevHdr), cudaMemcpyHostToDevice, c->st));
+      const int lmax = c->cfg.l_max, F = std::min(lmax, kDenseTop);
+      const int Gn = grid_for(c, n);
+      Dev& d = c->dv;
+      cudaMemsetAsync(d.pyr + pyr_off(F), 0, (pyr_off(F + 1) - pyr_off(F)) * 4, c->st);
+      k_mbr<<<Gn, 256, 0, c->st>>>(d);
+      k_reuse_oob<<<1, 1, 0, c->st>>>(c->d_hdr);
+      k_codes<<<Gn, 256, 0, c->st>>>(d);  // at the old index's scale
+      for (int l = F - 1; l >= 0; --l)
+        k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, c->st>>>(d, l);
+      k_leaf_recount<<<c->num_sms * 8, 256, 0, c->st>>>(d);
+      S.kernel_launches += 4 + F;
+      if ((rc = check_launch(c))) return rc;
+      TJ_CUDA(cudaMemcpyAsync(c->h_hdr, c->d_hdr, sizeof(DevHdr), cudaMemcpyDeviceToHost, c->st));
+      TJ_CUDA(cudaStreamSynchronize(c->st));
+      const DevHdr& H = *c->h_hdr;
+      // needs_rebuild (quadtree.py:250-270): escaped objects, a leaf over 8 x th, or > 5% over 2 x th
+      const bool rebuild = H.oob || H.overfull8 > 0 || (double)H.overfull2 / (double)std::max<int64_t>(H.L, 1) > 0.05;
+      c->reuse = !rebuild;
+    }
     bool done = false;
     for (int attempt = 0; attempt < 8 && !done; ++attempt) {
       if ((rc = prepare_dynamic(c))) return rc;
@@ -719,6 +779,13 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     const DevHdr& H = *c->h_hdr;
     c->last = H;
     c->last_L = H.L;
+    if (!c->reuse) {  // this tick built the index: keep it for the adaptive policy
+      c->idx = H;
+      c->have_index = true;
+      c->idx_bufs[0] = c->zmap.p;
+      c->idx_bufs[1] = c->lcode.p;
+      c->idx_bufs[2] = c->lnobj.p;
+    }
     if (H.dup) return fail(c, TJ_E_DUPLICATE_RESULT, "a (query, object) pair was produced twice");
     if (H.count_mismatch) return fail(c, TJ_E_COUNT_MISMATCH, "decoded counts disagree with popcounts");
     R = H.R;
@@ -760,7 +827,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     S.bitmap_words = H.W;
     S.n_subqueries = H.S;
     S.work_units = H.U;
-    S.rebuilt = 1;
+    S.rebuilt = c->reuse ? 0 : 1;
     S.mbr[0] = H.xa;
     S.mbr[1] = H.ya;
     S.mbr[2] = H.xb;

@@ -106,6 +106,8 @@ __device__ __forceinline__ uint32_t cell_of(double v, double lo, double scale, i
   double t = __dmul_rn(__dsub_rn(v, lo), scale);
   double lim = (double)(side - 1u);
   t = (t < lim) ? t : lim;  // np.minimum (no NaNs on this path)
+  t = (t > 0.0) ? t : 0.0;  // a no-op for points inside the MBR; keeps the adaptive check's
+                            // out-of-MBR points (discarded by the rebuild) inside the grid
   return (uint32_t)__double2int_rz(t);
 }
 

@@ -360,6 +360,37 @@ __global__ void __launch_bounds__(256) k_cell_level(const Dev d) {
   }
 }
 
+// ---- adaptive rebuild (rebuild="adaptive": quadtree.py:243-270, engine.py:163-174)
+// The previous tick's index is reused unless needs_rebuild: an object outside
+// the old MBR (OutOfBounds, morton.py:98-99), any leaf holding more than
+// 8 x th_quad objects, or more than 5% of the leaves holding more than
+// 2 x th_quad.  The check recounts the old leaves from the dense pyramid of
+// this tick's codes, taken at the old index's scale.
+__global__ void k_reuse_oob(DevHdr* h) {
+  const bool out = dunkey(h->kmin_x) < h->xa || dunkey(h->kmax_x) > h->xb || dunkey(h->kmin_y) < h->ya ||
+                   dunkey(h->kmax_y) > h->yb;
+  if (out) h->oob = 1;
+}
+
+__global__ void __launch_bounds__(256) k_leaf_recount(const Dev d) {
+  DevHdr* h = d.h;
+  const uint32_t th = (uint32_t)h->th;
+  unsigned long long o2 = 0, o8 = 0;
+  TJ_GRID_STRIDE(r, h->L) {
+    const uint32_t code = d.leaf_code[r];
+    const uint32_t cnt = node_count(d, h->F, (int)(code >> kLevelShift), code & kPayloadMask);
+    d.leaf_nobj[r] = (int32_t)cnt;
+    o2 += cnt > 2u * th;
+    o8 += cnt > 8u * th;
+  }
+  o2 = warp_sum(o2);
+  o8 = warp_sum(o8);
+  if (lane_id() == 0) {
+    if (o2) atomicAdd(&h->overfull2, o2);
+    if (o8) atomicAdd(&h->overfull8, o8);
+  }
+}
+
 struct ZFlagIn {
   const uint8_t* clev;
   const DevHdr* h;

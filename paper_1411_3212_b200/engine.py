@@ -116,6 +116,7 @@ class TickStats:
     # B200 additions
     n_leaves: int = 0
     l_deep: int = 0
+    rebuilt: bool = True  # rebuild="adaptive": False when the previous tick's index was reused
     device_ms: dict = field(default_factory=dict)
 
 
@@ -142,6 +143,7 @@ def _fill_stats(stats: TickStats, st: "_native.TjStats") -> None:
     stats.results_total = int(st.results_total)
     stats.n_leaves = int(st.n_leaves)
     stats.l_deep = int(st.l_deep)
+    stats.rebuilt = bool(st.rebuilt)
     if stats.results_total:
         stats.covering_result_fraction = stats.covering_results / stats.results_total
     a = int(st.active_cells)

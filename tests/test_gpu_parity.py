@@ -400,3 +400,31 @@ def test_extreme_hotspot_big_leaves(pkg):
     occ = ref.directory.o_end - ref.directory.o_start
     assert occ.max() > 384  # some leaves span several 384-object join tiles
     eng.close()
+
+
+def _adaptive_runs():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "adaptive.json")) as fp:
+        return json.load(fp)["runs"]
+
+
+@pytest.mark.parametrize("name", sorted(_adaptive_runs()))
+def test_adaptive_rebuild_matches_reference(pkg, name):
+    """rebuild="adaptive" (engine.py:163-174, quadtree.py:243-270): per tick the
+    device reuses or rebuilds its index exactly when the reference engine does,
+    with the same leaves / depth, and returns the reference's results."""
+    run = _adaptive_runs()[name]
+    cfg = dict(run["config"])
+    th = cfg.pop("th_quad")
+    if isinstance(cfg.get("query_side"), list):
+        cfg["query_side"] = tuple(cfg["query_side"])
+    eng = _engine(pkg, th=th, rebuild="adaptive")
+    for t, tick in enumerate(pkg.iter_ticks(pkg.WorkloadConfig(**cfg))):
+        want = run["ticks"][t]
+        res, st = eng.process_tick_columnar(tick)
+        assert st.rebuilt == want["rebuilt"], t
+        assert st.n_leaves == want["n_leaves"] and st.l_deep == want["l_deep"], t
+        assert qo.result_digest(tick.qids, res.offsets, res.ids) == want["digest"], t
+    eng.close()

@@ -201,3 +201,38 @@ def test_oracle_digest_config_a_first_ticks(digests):
 @pytest.mark.parametrize("k", [0, 1, 2, 5, 10, 19])
 def test_oracle_digest_c1(digests, k):
     _digest_run(digests[f"C1_{k}"])
+
+
+# ------------------------------------------------------- adaptive rebuild --
+
+def _adaptive_runs():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "adaptive.json")) as fp:
+        return json.load(fp)["runs"]
+
+
+@pytest.mark.parametrize("name", sorted(_adaptive_runs()))
+def test_oracle_adaptive_rebuild_matches_reference(name):
+    """needs_rebuild (quadtree.py:243-270) + index reuse (engine.py:163-174):
+    the oracle's per-tick rebuild decisions, index shape and results equal
+    the reference engine's (tests/golden/make_adaptive_golden.py)."""
+    from paper_1411_3212_b200.workload import WorkloadConfig, iter_ticks
+
+    run = _adaptive_runs()[name]
+    cfg = dict(run["config"])
+    th = cfg.pop("th_quad")
+    if isinstance(cfg.get("query_side"), list):
+        cfg["query_side"] = tuple(cfg["query_side"])
+    index = None
+    for tick, want in zip(iter_ticks(WorkloadConfig(**cfg)), run["ticks"]):
+        rebuilt = index is None or qo.needs_rebuild(tick.xs, tick.ys, index)
+        if rebuilt:
+            index = qo.build_index(tick.xs, tick.ys, qo.mbr_of(tick.xs, tick.ys), th, qo.L_MAX)
+        assert rebuilt == want["rebuilt"]
+        assert len(index.leaves) == want["n_leaves"] and index.l_deep == want["l_deep"]
+        assert list(index.mbr) == want["mbr"]
+        t = qo.run_tick(tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb, th_quad=th,
+                        index=index)
+        assert qo.result_digest(tick.qids, t.offsets, t.result_ids) == want["digest"]
