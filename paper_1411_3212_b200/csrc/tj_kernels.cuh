@@ -1423,8 +1423,11 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
             d.big_list[idx] = (int32_t)ql;
           }
         } else if (k > 1 && k <= kLaneRuns && cnt <= kLaneList) {
+          // heads packed as (row << 2 | run) (rows < 2^28): the minimum names its run
+          static_assert(kLaneRuns == 4, "the packed-head minimum below is written for four runs");
+          constexpr uint32_t kEnd = 0x7ffffffcu;
           int pos[kLaneRuns], end[kLaneRuns];
-          int32_t head[kLaneRuns];
+          uint32_t hk[kLaneRuns];
           int acc = qs;
 #pragma unroll
           for (int j = 0; j < kLaneRuns; ++j) {
@@ -1432,25 +1435,27 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
             pos[j] = acc;
             end[j] = acc + c;
             acc += c;
-            head[j] = c > 0 ? sa[pos[j]] : kRowEnd;
+            hk[j] = (c > 0 ? ((uint32_t)sa[pos[j]] << 2) : kEnd) | (uint32_t)j;
           }
           int64_t* dst = d.out_ids + qo;
           for (int o = 0; o < (int)cnt; ++o) {
-            int bj = 0;
-            int32_t bv = head[0];
+            const uint32_t mn = min(min(hk[0], hk[1]), min(hk[2], hk[3]));
+            const int bj = (int)(mn & 3u);
+            dst[o] = idof((int32_t)(mn >> 2));
+            // advance the winning run: select its cursor, one shared-memory load, select back
+            int np = pos[0], ne = end[0];
 #pragma unroll
-            for (int j = 1; j < kLaneRuns; ++j)
-              if (head[j] < bv) {
-                bv = head[j];
-                bj = j;
-              }
-            dst[o] = idof(bv);
+            for (int j = 1; j < kLaneRuns; ++j) {
+              np = j == bj ? pos[j] : np;
+              ne = j == bj ? end[j] : ne;
+            }
+            ++np;
+            const uint32_t nk = (np < ne ? ((uint32_t)sa[np] << 2) : kEnd) | (uint32_t)bj;
 #pragma unroll
-            for (int j = 0; j < kLaneRuns; ++j)
-              if (j == bj) {
-                ++pos[j];
-                head[j] = pos[j] < end[j] ? sa[pos[j]] : kRowEnd;
-              }
+            for (int j = 0; j < kLaneRuns; ++j) {
+              pos[j] = j == bj ? np : pos[j];
+              hk[j] = j == bj ? nk : hk[j];
+            }
           }
         }
       }
