@@ -59,7 +59,7 @@ struct tj_ctx {
   // objects
   DBuf code, okey0, okey1, oval0, oval1, sx, sy;
   // index
-  DBuf linfo, pyr, heavy, sub, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
+  DBuf linfo, pyr, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
   DBuf qpos, qwin, crect, nsub, qsbase, biglist, leafcnt;
   // subqueries
@@ -82,7 +82,7 @@ struct tj_ctx {
   void* h_ids = nullptr;
   size_t h_ids_bytes = 0;
   // capacities of the dynamically sized arenas
-  int64_t cap_S = 0, cap_W = 0, cap_R = 0, cap_L = 0, cap_heavy = 0, cap_U = 0;
+  int64_t cap_S = 0, cap_W = 0, cap_R = 0, cap_L = 0, cap_U = 0;
   int64_t last_L = 0;
   // last tick, for introspection
   bool have = false;
@@ -166,7 +166,6 @@ inline int grid_for(tj_ctx* c, int64_t items, int per_sm = 8) {
 int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   const int lmax = c->cfg.l_max;
   const int F = std::min(lmax, kDenseTop);
-  const int D = lmax - F;
   const int64_t th = c->cfg.th_quad;
   int rc;
 #define ENS(buf, bytes) \
@@ -175,7 +174,6 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   const int64_t Zmax = int64_t(1) << (2 * lmax);
   int64_t lcap = 4 + 3 * (int64_t)(lmax > 1 ? lmax - 1 : 0) * (n / (th + 1) + 1);
   c->cap_L = std::min(lcap, Zmax);
-  c->cap_heavy = D > 0 ? std::min<int64_t>(n / (th + 1) + 1, int64_t(1) << (2 * F)) : 0;
   ENS(code, n * 4);
   ENS(okey0, n * 4);
   ENS(okey1, n * 4);
@@ -184,8 +182,6 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(sx, n * 8);
   ENS(sy, n * 8);
   ENS(pyr, pyr_off(F + 1) * 4);
-  ENS(heavy, (int64_t(1) << (2 * F)) * 4);
-  ENS(sub, std::max<int64_t>(1, c->cap_heavy * sub_size(D)) * 4);
   ENS(clev, Zmax);
   ENS(zmap, Zmax * 4);
   ENS(lcode, c->cap_L * 4);
@@ -267,8 +263,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.sx = P<double>(c->sx);
   d.sy = P<double>(c->sy);
   d.pyr = P<uint32_t>(c->pyr);
-  d.heavy_map = P<int32_t>(c->heavy);
-  d.sub = P<uint32_t>(c->sub);
   d.clev = P<uint8_t>(c->clev);
   d.zmap = P<uint32_t>(c->zmap);
   d.leaf_code = P<uint32_t>(c->lcode);
@@ -290,8 +284,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.bitmap = P<uint32_t>(c->bitmap);
   d.out_ids = P<int64_t>(c->outids);
   d.out_off = P<int64_t>(c->outoff);
-  d.D = lmax - F;
-  d.SUB = sub_size(d.D);
   d.sidx = d.oval[c->obj_passes & 1];
   d.leaf_cur = P<int32_t>(c->leafcur);
   d.leaf_cnt = P<int4>(c->leafcnt);
@@ -341,7 +333,6 @@ int launch_stage(tj_ctx* c, int stage) {
   DevHdr* h = c->d_hdr;
   const int lmax = c->cfg.l_max;
   const int F = std::min(lmax, kDenseTop);
-  const int D = lmax - F;
   const int64_t n = c->n, m = c->m;
   const int Gn = grid_for(c, n), Gm = grid_for(c, m);
   const int Gbig = c->num_sms * 8;
@@ -365,12 +356,6 @@ int launch_stage(tj_ctx* c, int stage) {
       k_finalize_mbr<<<1, 1, 0, st>>>(h);
       k_codes<<<Gn, 256, 0, st>>>(d);
       for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
-      if (D > 0) {
-        k_heavy<<<grid_for(c, int64_t(1) << (2 * F)), 256, 0, st>>>(d);
-        k_zero_sub<<<Gbig, 256, 0, st>>>(d);
-        k_sub_hist<<<Gn, 256, 0, st>>>(d);
-        for (int r = D - 1; r >= 1; --r) k_sub_level<<<Gbig, 256, 0, st>>>(d, r);
-      }
       k_finalize_index<<<1, 1, 0, st>>>(h);
       k_cell_level<<<Gbig, 256, 0, st>>>(d);
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
@@ -382,7 +367,7 @@ int launch_stage(tj_ctx* c, int stage) {
         k_shard_mark<<<Gbig, 256, 0, st>>>(d);
       }
       // 3 launches per scan
-      return 12 + F + (D > 0 ? D + 2 : 0) + (c->shard_n > 1 ? 4 : 0);
+      return 12 + F + (c->shard_n > 1 ? 4 : 0);
     case kSortStage: {  // ---- K1's last part: objects into leaf order (side stream) ----
       cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
@@ -449,7 +434,6 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.cap_R = c->cap_R;
   H.cap_U = c->cap_U;
   H.cap_L = c->cap_L;
-  H.cap_heavy = c->cap_heavy;
   H.kmin_x = H.kmin_y = ~0ull;
   H.kmax_x = H.kmax_y = 0ull;
   H.l_deep = 1;
@@ -645,7 +629,7 @@ int tj_destroy(tj_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   drop_graphs(c);
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
-                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->heavy, &c->sub, &c->clev,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->qpos, &c->qwin, &c->crect, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
@@ -764,7 +748,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
         break;
       }
       S.retries++;
-      if (H.abort & (8 | 16)) return fail(c, TJ_E_CUDA, "internal capacity bound violated (heavy/leaves)");
+      if (H.abort & (8 | 16)) return fail(c, TJ_E_CUDA, "internal capacity bound violated (leaves)");
       if (H.abort & 32) {
         c->obj_passes = passes_for(H.L - 1);
       }

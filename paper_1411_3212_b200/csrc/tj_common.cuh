@@ -14,10 +14,11 @@ namespace tj {
 
 constexpr int kWarp = 32;
 constexpr int kMaxLevel = 12;        // morton.py:20 L_MAX
-constexpr int kDenseTop = 12;        // dense pyramid levels 0..min(l_max, 12): the histogram is taken
-                                     // at l_max (fine bins: little atomic contention in hotspots)
+constexpr int kDenseTop = 12;        // dense pyramid levels 0..l_max (l_max <= 12): the histogram is
+                                     // taken at l_max (fine bins: little atomic contention in hotspots)
 constexpr int kLevelShift = 24;      // zmap / leaf code: (level << 24) | payload
 constexpr uint32_t kPayloadMask = (1u << kLevelShift) - 1u;
+static_assert(kDenseTop >= kMaxLevel, "node_count reads every level from the dense pyramid");
 
 // Per-tick device header: sizes that only the device knows, reduction
 // targets, and the abort flag that makes every later kernel a no-op when a
@@ -26,7 +27,7 @@ struct DevHdr {
   // host-written each tick
   int64_t n, m;
   int32_t th, l_max, F, covering;
-  int64_t cap_S, cap_W, cap_R, cap_U, cap_L, cap_heavy;
+  int64_t cap_S, cap_W, cap_R, cap_U, cap_L;
   // MBR reduction (order-preserving keys) and derived scalars
   unsigned long long kmin_x, kmin_y, kmax_x, kmax_y;
   double xa, ya, xb, yb, width, height;
@@ -34,7 +35,7 @@ struct DevHdr {
   double lw[13], lh[13];    // leaf extent per level: width / 2^level, height / 2^level (quadtree.py:219-231)
   int32_t wpos, hpos;       // width > 0, height > 0
   int32_t l_deep;
-  int32_t n_heavy;
+  int32_t pad0;
   int32_t reuse_index;      // adaptive policy: this tick reuses the previous index
   int64_t Z, L;             // deepest cells, leaves
   int64_t S, S_i, S_c;      // subqueries: all / intersecting / covering
@@ -45,7 +46,7 @@ struct DevHdr {
   unsigned long long tests, cov_results, active_cells, occ_sum, occ_sumsq, sum_isq, sum_cov;
   unsigned long long task_obj, task_isq;  // P_a, S_a: objects / subqueries inside join tasks
   // flags
-  int32_t abort;            // bit0 S, bit1 W/U, bit2 R, bit3 heavy, bit4 L
+  int32_t abort;            // bit0 S, bit1 W/U, bit2 R, bit4 L
   int32_t not_monotone;     // object ids not strictly increasing in input order
   int32_t not_identity;     // some object id differs from its input row
   int32_t pad1;
@@ -64,9 +65,6 @@ struct DevHdr {
 __host__ __device__ inline int64_t pyr_off(int l) {
   return l == 0 ? 0 : ((int64_t(1) << (2 * l)) - 4) / 3 + 4;
 }
-// relative sub-pyramid offsets below a heavy level-F node: level F+r at (4^r-4)/3
-__host__ __device__ inline int64_t sub_off(int r) { return ((int64_t(1) << (2 * r)) - 4) / 3; }
-__host__ __device__ inline int64_t sub_size(int D) { return D > 0 ? sub_off(D + 1) : 0; }
 
 // order-preserving map double -> uint64 (for atomic min/max)
 __device__ __forceinline__ unsigned long long dkey(double v) {

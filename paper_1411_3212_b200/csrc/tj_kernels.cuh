@@ -2,7 +2,7 @@
 // tick; every size after the index build lives in DevHdr on the device.
 //
 //   K0  mbr / finalize           geometry.py:72-77, morton.py:100-104
-//   K1  codes + level-F histogram, dense pyramid, heavy-node sub-pyramids,
+//   K1  codes + level-l_max histogram, dense count pyramid,
 //       leaf level per deepest cell, zmap + leaf table (scan), object keys,
 //       stable radix sort of objects by leaf, payload gather
 //                                 quadtree.py:74-165, directory.py:128
@@ -43,8 +43,6 @@ struct Dev {
   double* sy;
   // index
   uint32_t* pyr;
-  int32_t* heavy_map;
-  uint32_t* sub;
   uint8_t* clev;
   uint32_t* zmap;
   uint32_t* leaf_code;
@@ -80,9 +78,6 @@ struct Dev {
   uint32_t* bitmap;
   int64_t* out_ids;
   int64_t* out_off;
-  // config
-  int64_t SUB;  // sub-pyramid entries per heavy node
-  int D;        // l_max - F
 };
 
 // multi-GPU leaf-range sharding: leaf r belongs to this rank (always, unsharded)
@@ -244,82 +239,6 @@ __global__ void __launch_bounds__(256) k_pyr_level(const Dev d, int l) {
   }
 }
 
-// level-F nodes over the threshold get a dense sub-pyramid slot
-__global__ void __launch_bounds__(256) k_heavy(const Dev d) {
-  DevHdr* h = d.h;
-  const int F = h->F;
-  const int64_t cnt = int64_t(1) << (2 * F);
-  const uint32_t* hist = d.pyr + pyr_off(F);
-  const uint32_t th = (uint32_t)h->th;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < cnt; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t z = b + threadIdx.x;
-    bool split = false;
-    if (z < cnt) {
-      split = hist[z] > th;  // F < l_max here
-      int slot = -1;
-      if (split) {
-        slot = atomicAdd(&h->n_heavy, 1);
-        if (slot >= h->cap_heavy) {
-          atomicOr(&h->abort, 8);
-          slot = -1;
-        }
-      }
-      d.heavy_map[z] = slot;
-    }
-    note_split(h, split, F + 1);
-  }
-}
-
-__global__ void __launch_bounds__(256) k_zero_sub(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  const int64_t cnt = (int64_t)h->n_heavy * d.SUB;
-  TJ_GRID_STRIDE(i, cnt) d.sub[i] = 0u;
-}
-
-__global__ void __launch_bounds__(256) k_sub_hist(const Dev d) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  const int64_t n = h->n;
-  const int D = d.D;
-  const uint32_t lowmask = (1u << (2 * D)) - 1u;
-  const int64_t off = sub_off(D);
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < n; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t i = b + threadIdx.x;
-    int64_t bin = -1;
-    if (i < n) {
-      const uint32_t z = d.code[i];
-      const int slot = d.heavy_map[z >> (2 * D)];
-      if (slot >= 0) bin = (int64_t)slot * d.SUB + off + (z & lowmask);
-    }
-    if (bin >= 0) atomicAdd(&d.sub[bin], 1u);
-  }
-}
-
-// relative level r (absolute F + r) from r + 1 inside each heavy node
-__global__ void __launch_bounds__(256) k_sub_level(const Dev d, int r) {
-  DevHdr* h = d.h;
-  if (h->abort) return;
-  const int64_t per = int64_t(1) << (2 * r);
-  const int64_t cnt = (int64_t)h->n_heavy * per;
-  const uint32_t th = (uint32_t)h->th;
-  const int l = h->F + r;
-  const bool can_split = l < h->l_max;
-  for (int64_t b = (int64_t)blockIdx.x * blockDim.x; b < cnt; b += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = b + threadIdx.x;
-    bool split = false;
-    if (e < cnt) {
-      const int64_t slot = e >> (2 * r), loc = e & (per - 1);
-      uint32_t* base = d.sub + slot * d.SUB;
-      const uint4 c = *reinterpret_cast<const uint4*>(base + sub_off(r + 1) + 4 * loc);
-      const uint32_t s = c.x + c.y + c.z + c.w;
-      base[sub_off(r) + loc] = s;
-      split = can_split && s > th;
-    }
-    note_split(h, split, l + 1);
-  }
-}
-
 __global__ void k_finalize_index(DevHdr* h) {
   if (h->abort) return;
   h->Z = int64_t(1) << (2 * h->l_deep);
@@ -330,11 +249,8 @@ __global__ void k_finalize_index(DevHdr* h) {
 
 // object count of node (l, z); l >= 1
 __device__ __forceinline__ uint32_t node_count(const Dev& d, int F, int l, uint32_t z) {
-  if (l <= F) return d.pyr[pyr_off(l) + z];
-  const int r = l - F;
-  const int slot = d.heavy_map[z >> (2 * r)];
-  if (slot < 0) return 0u;
-  return d.sub[(int64_t)slot * d.SUB + sub_off(r) + (z & ((1u << (2 * r)) - 1u))];
+  (void)F;  // F == l_max: the dense pyramid covers every level
+  return d.pyr[pyr_off(l) + z];
 }
 
 // Level of the leaf containing deepest cell c: the first level whose ancestor
@@ -807,8 +723,14 @@ constexpr int kTileObj = kTileBlocks * 32;
 #endif
 constexpr int kNK = TJ_NK;                    // buckets per axis
 constexpr int kRows = kNK + 2;                // prefix rows k = 0 .. kNK + 1
-constexpr int kQC = 512;                      // subqueries per chunk
-constexpr int kTableMinQ = 12;                // table path from this many subqueries
+#ifndef TJ_QC
+#define TJ_QC 512
+#endif
+constexpr int kQC = TJ_QC;                    // subqueries per chunk
+#ifndef TJ_TMQ
+#define TJ_TMQ 12
+#endif
+constexpr int kTableMinQ = TJ_TMQ;            // table path from this many subqueries
 
 
 struct WordsIn {
