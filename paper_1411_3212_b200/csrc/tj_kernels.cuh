@@ -1034,89 +1034,94 @@ __global__ void k_close_offsets(const Dev d) {
 
 constexpr int32_t kRowEnd = 0x7fffffff;
 
+#ifndef TJ_DQ_MINB
+#define TJ_DQ_MINB 10  // resident decode CTAs per SM the register budget is cut for
+#endif
 constexpr int kDQThreads = 128;
 constexpr int kDQWarps = kDQThreads / 32;
 constexpr int kDQStage = 1024;   // results staged per warp window
 constexpr int kLaneRuns = 4;     // lane-per-query k-way merge up to this many runs
 
-constexpr int kRankRuns = 32;  // lists of 5..32 runs: warp rank merge; more runs: k_merge_big
-constexpr int kLaneList = 128; // longer lists are merged by the whole warp (rank merge), not one lane
+constexpr int kRankRuns = 32;  // oversized lists (> one window) of 2..32 runs: warp rank merge; more: k_merge_big
+constexpr int kLaneList = 128; // longer lists are sorted by the whole warp (warp_bitonic), not one lane
 
-// Warp-cooperative merge of one list whose k <= 32 sorted runs lie
-// concatenated in src[0, cnt) (shared or global memory; values distinct
-// across runs): element i lands at its rank = its index in its own run + the
-// number of smaller values in each other run (binary searches).
-// In-place pairwise merging of a list of k sorted runs (values distinct)
-// held in shared memory a[0, cnt), cnt <= 256: each round merges runs
-// (0,1), (2,3), ... — every element moves to (its index in its run) + (the
-// number of smaller values in the partner run), one binary search each — so
-// k runs take ceil(log2 k) rounds instead of k - 1 searches per element.
-// Elements ride in registers (8 per lane) between a round's reads and writes.
-constexpr int kPairMax = 256;
-__device__ __forceinline__ void warp_pair_merge(int32_t* a, int cnt, int k, const int32_t* counts) {
+// Warp bitonic sort of one list a[0, cnt) in shared memory, cnt <= 32 * E,
+// back in place (values distinct int32 input rows; padding INT_MAX).
+// Lane-major layout — lane L holds elements L*E .. L*E+E-1 — so the stages
+// with partner distance j < E are register compare-exchanges and only those
+// with j >= E cross lanes (one shuffle per element).  For lists of many runs
+// this costs O(n log^2 n / 32) register ops per lane with no dependent
+// shared-memory searches, against k binary searches per element for the
+// rank merge.
+template <int E>
+__device__ __forceinline__ void warp_bitonic(int32_t* a, int cnt) {
+  constexpr int P = 32 * E;
   const int lane = lane_id();
-  const int c = lane < k ? counts[lane] : 0;
-  const int inc = warp_incl_scan(c);
-  int st = inc - c;  // lane j < k: start of run j (lanes >= k: cnt)
-  if (lane >= k) st = cnt;
-  for (int nr = k; nr > 1; nr = (nr + 1) >> 1) {
-    int32_t v[kPairMax / 32];
-    int np[kPairMax / 32];
+  int32_t v[E];
 #pragma unroll
-    for (int u = 0; u < kPairMax / 32; ++u) {
-      const int i = u * 32 + lane;
-      int j = 0;  // own run: the last run starting at or before i (every lane shuffles)
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const int sj = __shfl_sync(0xffffffffu, st, (j + step) & 31);
-        if (j + step < nr && sj <= i) j += step;
-      }
-      v[u] = i < cnt ? a[i] : 0;
-      np[u] = i < cnt ? j : -1;  // temporarily the run index
-    }
-    // partner runs and searches (shuffles need every lane: done outside the predicate)
-#pragma unroll
-    for (int u = 0; u < kPairMax / 32; ++u) {
-      const int i = u * 32 + lane;
-      const int j = np[u] < 0 ? 0 : np[u];
-      const int pj = j ^ 1;
-      const int s_j = __shfl_sync(0xffffffffu, st, j & 31);
-      const int s_p = __shfl_sync(0xffffffffu, st, pj & 31);
-      const int e_p = __shfl_sync(0xffffffffu, st, (pj + 1) & 31);
-      const int s_pair = __shfl_sync(0xffffffffu, st, (j & ~1) & 31);
-      if (np[u] >= 0) {
-        int rank = i - s_j;
-        if (pj < nr) {
-          int first = s_p, len = (pj + 1 < nr ? e_p : cnt) - s_p;  // lower_bound(v) in the partner run
-          while (len > 0) {
-            const int half = len >> 1;
-            if (a[first + half] < v[u]) {
-              first += half + 1;
-              len -= half + 1;
-            } else {
-              len = half;
-            }
-          }
-          rank += first - s_p;
-        }
-        np[u] = s_pair + rank;
-      }
-    }
-    __syncwarp();
-#pragma unroll
-    for (int u = 0; u < kPairMax / 32; ++u)
-      if (np[u] >= 0) a[np[u]] = v[u];
-    __syncwarp();
-    // merged run r' = old runs 2r', 2r'+1: start = old start of 2r'
-    const int ns = __shfl_sync(0xffffffffu, st, (2 * lane) & 31);
-    st = (2 * lane < nr && lane < 16) ? ns : cnt;
+  for (int u = 0; u < E; ++u) {
+    const int i = lane * E + u;
+    v[u] = i < cnt ? a[i] : 0x7fffffff;
   }
+  // phases k < E: directions per slot (compile-time); the whole lane's block is one run
+#pragma unroll
+  for (int k = 2; k < E; k <<= 1) {
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+#pragma unroll
+      for (int u = 0; u < E; ++u) {
+        if ((u & j) == 0) {
+          const int32_t x = v[u], y = v[u + j];
+          v[u] = (u & k) == 0 ? min(x, y) : max(x, y);
+          v[u + j] = (u & k) == 0 ? max(x, y) : min(x, y);
+        }
+      }
+    }
+  }
+  // phases k >= E: the direction is per lane.  Descending lanes hold ~v
+  // (order-reversing on int32), so every exchange below is ascending.
+  int32_t flip = 0;
+#pragma unroll
+  for (int k = E; k <= P; k <<= 1) {
+    const int32_t nf = ((lane * E) & k) ? -1 : 0;
+#pragma unroll
+    for (int u = 0; u < E; ++u) v[u] ^= flip ^ nf;
+    flip = nf;
+#pragma unroll
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j >= E) {
+        const int lj = j / E;
+        const bool upper = (lane & lj) != 0;  // the upper partner keeps the max
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+          const int32_t y = __shfl_xor_sync(0xffffffffu, v[u], lj);
+          v[u] = ((v[u] < y) != upper) ? v[u] : y;
+        }
+      } else {
+#pragma unroll
+        for (int u = 0; u < E; ++u) {
+          if ((u & j) == 0) {
+            const int32_t x = v[u], y = v[u + j];
+            v[u] = min(x, y);
+            v[u + j] = max(x, y);
+          }
+        }
+      }
+    }
+  }
+  // the last phase (k = P) is ascending everywhere: flip == 0
+  __syncwarp();
+#pragma unroll
+  for (int u = 0; u < E; ++u) {
+    const int i = lane * E + u;
+    if (i < cnt) a[i] = v[u];
+  }
+  __syncwarp();
 }
 
 template <typename T, typename Emit>
-__device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, const int32_t* counts, Emit emit) {
+__device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, int c, Emit emit) {
   const int lane = lane_id();
-  const int c = lane < k ? counts[lane] : 0;
   const int inc = warp_incl_scan(c);
   const int st = inc - c;  // lane j < k: start of run j
   for (int i0 = 0; i0 < cnt; i0 += 32) {
@@ -1162,13 +1167,18 @@ __device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, co
 //     output position of every bit — runs are concatenated in slot order,
 //     which is output order;
 //  B. turns leaf positions into input rows with batched independent loads;
-//  C. per query (lane), merges its 2..4 runs by head (object ids increase
-//     with the input row) or copies its single run into a second buffer;
-//  D. stores the window with coalesced writes, ids looked up there.
+//  C. stores the window (runs concatenated) with coalesced writes, ids
+//     looked up there;
+//  D. re-sorts the lists of several runs (object ids increase with the input
+//     row): one lane per query merges 2..4 runs of <= 128 results by head;
+//     longer lists or more runs are sorted by the whole warp, one list at a
+//     time, in registers (warp_bitonic; > 512 results: two sorted halves and
+//     one rank merge).
 // Lists of one query larger than a window are concatenated in global memory
-// by the whole warp; lists that need a sort by id (ids not monotone, or more
-// than 4 runs) go to the CTA-wide k_merge_big.
-__global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
+// by the whole warp and rank-merged there (<= 32 runs); lists that need a
+// sort by id (ids not monotone) or oversized lists of more than 32 runs go to
+// the CTA-wide k_merge_big.
+__global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   __shared__ int32_t sbuf[kDQWarps][kDQStage];
@@ -1242,7 +1252,7 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
         if (rmerge) {
           __syncwarp();
           int64_t* out = d.out_ids + base;
-          warp_rank_merge(d.scratch + base, (int)cq, kq, d.sq_count + sq0,
+          warp_rank_merge(d.scratch + base, (int)cq, kq, lane < kq ? d.sq_count[sq0 + lane] : 0,
                           [&](int r, int64_t v) { out[r] = v; });
         } else if (lane == 0 && cq > 1 && (kq > 1 || !mono)) {
           const int idx = atomicAdd(&h->n_big, 1);
@@ -1336,14 +1346,12 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
       // ---- C: store the window (runs concatenated; ids looked up here)
       for (int i = lane; i < (int)T; i += 32) d.out_ids[base + i] = idof(sa[i]);
       __syncwarp();
-      // ---- D: per query with 2..4 runs, merge the runs by head over the stored concatenation
+      // ---- D: per query with 2..4 runs and <= 128 results, merge the runs by head (one lane per query)
       if (act && cnt > 1) {
         const int qs = (int)(qo - base);
-        if (!mono || k > kRankRuns) {
-          if (k > 1 || !mono) {
-            const int idx = atomicAdd(&h->n_big, 1);
-            d.big_list[idx] = (int32_t)ql;
-          }
+        if (!mono) {  // ids not increasing with the input row: sorted by id in k_merge_big
+          const int idx = atomicAdd(&h->n_big, 1);
+          d.big_list[idx] = (int32_t)ql;
         } else if (k > 1 && k <= kLaneRuns && cnt <= kLaneList) {
           // heads packed as (row << 2 | run) (rows < 2^28): the minimum names its run
           static_assert(kLaneRuns == 4, "the packed-head minimum below is written for four runs");
@@ -1381,24 +1389,25 @@ __global__ void __launch_bounds__(kDQThreads, 10) k_decode_query(const Dev d) {
           }
         }
       }
-      // lists of 5..32 runs: the warp merges them one at a time by rank
-      unsigned rq = __ballot_sync(0xffffffffu, act && cnt > 1 && mono && k > 1 && k <= kRankRuns &&
-                                                   (k > kLaneRuns || cnt > kLaneList));
+      // other multi-run lists: the warp sorts them one at a time
+      unsigned rq = __ballot_sync(0xffffffffu, act && cnt > 1 && mono && k > 1 && (k > kLaneRuns || cnt > kLaneList));
       while (rq) {
         const int src = __ffs(rq) - 1;
         rq &= rq - 1;
-        const int kq = __shfl_sync(0xffffffffu, k, src);
-        const int32_t sq0 = __shfl_sync(0xffffffffu, s0, src);
         const int64_t qoq = __shfl_sync(0xffffffffu, qo, src);
         const int cq = (int)__shfl_sync(0xffffffffu, cnt, src);
         int64_t* out = d.out_ids + qoq;
-        if (cq <= kPairMax && kq >= 3) {  // log2(k) rounds of pairwise merges in place, then store
-          int32_t* lst = sa + (qoq - base);
-          warp_pair_merge(lst, cq, kq, d.sq_count + sq0);
+        int32_t* lst = sa + (qoq - base);
+        if (cq <= 512) {  // sort in registers, then store
+          if (cq <= 64) warp_bitonic<2>(lst, cq);
+          else if (cq <= 128) warp_bitonic<4>(lst, cq);
+          else if (cq <= 256) warp_bitonic<8>(lst, cq);
+          else warp_bitonic<16>(lst, cq);
           for (int i = lane; i < cq; i += 32) out[i] = idof(lst[i]);
-        } else {
-          warp_rank_merge(sa + (qoq - base), cq, kq, d.sq_count + sq0,
-                          [&](int r, int32_t v) { out[r] = idof(v); });
+        } else {  // two sorted halves, then one rank merge of the pair
+          warp_bitonic<16>(lst, 512);
+          warp_bitonic<16>(lst + 512, cq - 512);
+          warp_rank_merge(lst, cq, 2, lane == 0 ? 512 : cq - 512, [&](int r, int32_t v) { out[r] = idof(v); });
         }
       }
       __syncwarp();

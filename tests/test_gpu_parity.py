@@ -229,6 +229,29 @@ def test_huge_queries_many_subqueries(pkg):
         eng.close()
 
 
+@pytest.mark.parametrize("th", [16, 64])
+def test_decode_merge_paths_all_list_shapes(pkg, th):
+    """Every per-query merge path of the decode kernel: single runs, the lane
+    merge (2..4 runs, <= 128 results), the warp bitonic sort (>= 3 runs, up to
+    512 results), the warp rank merge (513..1024 results), the oversized-list
+    path (> 1024 results, concatenated in global memory) and the CTA sort of
+    lists of more than 32 runs."""
+    rng = np.random.default_rng(17 + th)
+    n, m = 200_000, 4000
+    xs, ys, a, b, c, d = _rand_tick(rng, n, m, side=(1.0, 110.0))
+    ids = np.arange(n, dtype=np.int64)
+    qids = np.arange(m, dtype=np.int64)
+    eng = _engine(pkg, th=th)
+    res, _ = eng.process_columns(ids, xs, ys, qids, a, b, c, d)
+    ref = qo.run_tick(ids, xs, ys, qids, a, b, c, d, th_quad=th)
+    _check_vs_oracle(res, ref)
+    cnt = np.diff(ref.offsets)
+    runs = np.bincount(eng.native.subqueries()[0], minlength=m)
+    assert ((runs >= 3) & (cnt > 256) & (cnt <= 512)).any() and ((runs >= 3) & (cnt <= 64) & (cnt > 1)).any()
+    assert (cnt > 1024).any() and (runs > 32).any()
+    eng.close()
+
+
 def test_covering_toggle_preserves_results(pkg):
     """test_engine.py:100-111 / acceptance C4 semantics."""
     cfg = pkg.WorkloadConfig(n_objects=4000, n_ticks=1, distribution="gaussian", n_hotspots=4, seed=8,
