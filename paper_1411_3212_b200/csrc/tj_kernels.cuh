@@ -1032,6 +1032,9 @@ __global__ void k_close_offsets(const Dev d) {
   d.out_off[h->m] = h->R;
 }
 
+// result ids are written once and never re-read on the device: streaming stores
+__device__ __forceinline__ void st_out(int64_t* p, int64_t v) { __stcs(reinterpret_cast<long long*>(p), (long long)v); }
+
 constexpr int32_t kRowEnd = 0x7fffffff;
 
 #ifndef TJ_DQ_MINB
@@ -1344,7 +1347,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
       }
       __syncwarp();
       // ---- C: store the window (runs concatenated; ids looked up here)
-      for (int i = lane; i < (int)T; i += 32) d.out_ids[base + i] = idof(sa[i]);
+      for (int i = lane; i < (int)T; i += 32) st_out(d.out_ids + base + i, idof(sa[i]));
       __syncwarp();
       // ---- D: per query with 2..4 runs and <= 128 results, merge the runs by head (one lane per query)
       if (act && cnt > 1) {
@@ -1371,7 +1374,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
           for (int o = 0; o < (int)cnt; ++o) {
             const uint32_t mn = min(min(hk[0], hk[1]), min(hk[2], hk[3]));
             const int bj = (int)(mn & 3u);
-            dst[o] = idof((int32_t)(mn >> 2));
+            st_out(dst + o, idof((int32_t)(mn >> 2)));
             // advance the winning run: select its cursor, one shared-memory load, select back
             int np = pos[0], ne = end[0];
 #pragma unroll
@@ -1403,11 +1406,11 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
           else if (cq <= 128) warp_bitonic<4>(lst, cq);
           else if (cq <= 256) warp_bitonic<8>(lst, cq);
           else warp_bitonic<16>(lst, cq);
-          for (int i = lane; i < cq; i += 32) out[i] = idof(lst[i]);
+          for (int i = lane; i < cq; i += 32) st_out(out + i, idof(lst[i]));
         } else {  // two sorted halves, then one rank merge of the pair
           warp_bitonic<16>(lst, 512);
           warp_bitonic<16>(lst + 512, cq - 512);
-          warp_rank_merge(lst, cq, 2, lane == 0 ? 512 : cq - 512, [&](int r, int32_t v) { out[r] = idof(v); });
+          warp_rank_merge(lst, cq, 2, lane == 0 ? 512 : cq - 512, [&](int r, int32_t v) { st_out(out + r, idof(v)); });
         }
       }
       __syncwarp();
