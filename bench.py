@@ -364,6 +364,8 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         e_steps = max(1, min(args.steps, args.e2e_steps))
+        out_flag = 0 if args.e2e_ids64 else _native.TJ_OUT_IDS32
+        idb, idbs = 8, set()
         if sharded:
             hsh = [Shard(t, rank, world, dev, pinned=True) for t in ticks]
             dsl = [[torch.empty_like(x, device=dev) for x in hsh[0].mine] for _ in range(1)][0]
@@ -376,7 +378,7 @@ def run_ours(args):
                     sh.gather(dsl)
                 a = sh.full
                 return ctx.tick_ptrs(sh.n, *(x.data_ptr() for x in a[:3]), sh.m, *(x.data_ptr() for x in a[3:]),
-                                     _native.TJ_MEM_DEVICE, _native.TJ_MEM_HOST), \
+                                     _native.TJ_MEM_DEVICE, _native.TJ_MEM_HOST | out_flag), \
                     sum(x.numel() * x.element_size() for x in sh.mine)
         else:
             hticks = [[torch.from_numpy(a).pin_memory() for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb,
@@ -385,7 +387,7 @@ def run_ours(args):
             def tick_host(k):
                 a = hticks[k % pool]
                 return ctx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
-                                     *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST), \
+                                     *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST | out_flag), \
                     sum(x.numel() * x.element_size() for x in a)
 
         if sharded or args.e2e_contexts <= 1:
@@ -399,7 +401,8 @@ def run_ours(args):
             for k in range(e_steps):
                 (out, st), hb = tick_host(k)
                 h2d += hb
-                d2h += 8 * (out.n_q + 1) + 8 * out.n_results
+                d2h += 8 * (out.n_q + 1) + out.id_bytes * out.n_results
+                idb = out.id_bytes
                 eq += int(st.n_queries)
             e1.record(stream)
             torch.cuda.synchronize()
@@ -415,7 +418,8 @@ def run_ours(args):
             def host_tick(cx, k):
                 a = hticks[k % pool]
                 out, st = cx.tick_ptrs(a[0].numel(), *(x.data_ptr() for x in a[:3]), a[3].numel(),
-                                       *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST, _native.TJ_MEM_HOST)
+                                       *(x.data_ptr() for x in a[3:]), _native.TJ_MEM_HOST,
+                                       _native.TJ_MEM_HOST | out_flag)
                 return out, st, sum(x.numel() * x.element_size() for x in a)
 
             for cx in ctxs:
@@ -427,7 +431,8 @@ def run_ours(args):
                 for k in range(j, e_steps, len(ctxs)):
                     out, st, hb = host_tick(ctxs[j], k)
                     acc[j][0] += hb
-                    acc[j][1] += 8 * (out.n_q + 1) + 8 * out.n_results
+                    acc[j][1] += 8 * (out.n_q + 1) + out.id_bytes * out.n_results
+                    idbs.add(out.id_bytes)
                     acc[j][2] += int(st.n_queries)
 
             ths = [threading.Thread(target=worker, args=(j,)) for j in range(len(ctxs))]
@@ -439,6 +444,7 @@ def run_ours(args):
             torch.cuda.synchronize()
             e_ms = (time.perf_counter() - t0) * 1e3
             h2d, d2h, eq = (sum(a_[i] for a_ in acc) for i in range(3))
+            idb = max(idbs) if idbs else 8
             for cx in ctxs[1:]:
                 cx.close()
         if world > 1:
@@ -450,7 +456,9 @@ def run_ours(args):
                "timing": ("wall clock over all steps" if (not sharded and args.e2e_contexts > 1)
                           else "CUDA events on the library stream"),
                "contexts": 1 if sharded else args.e2e_contexts,
+               "id_bytes": idb,
                "api": ("tj_tick (C ABI): pinned host inputs -> device, results CSR -> pinned host"
+                       + (" (ids as int32: TJ_OUT_IDS32, every id < 2^31)" if idb == 4 else " (int64 ids)")
                        + ("; per rank: H2D of its 1/G slice, NCCL all-gather, D2H of its leaf-range CSR"
                           if sharded else ""))}
 
@@ -518,11 +526,13 @@ def main(argv=None):
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--ref-sample", type=int, default=500_000)
     ap.add_argument("--e2e-steps", type=int, default=6)
-    ap.add_argument("--e2e-contexts", type=int, default=2,
+    ap.add_argument("--e2e-contexts", type=int, default=3,
                     help="tj_tick contexts driven from this many host threads in the e2e leg (overlap of "
                          "uploads, compute and downloads across ticks)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-ids64", action="store_true",
+                    help="e2e leg downloads int64 result ids instead of asking for int32 (TJ_OUT_IDS32)")
     ap.add_argument("--sharded", action="store_true",
                     help="leaf-range sharded path (NCCL all-gather + tj_set_shard) even at N=1")
     args = ap.parse_args(argv)

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define TJ_ABI_VERSION 1
+#define TJ_ABI_VERSION 2
 
 /* status codes — errors.py:4-45 */
 #define TJ_OK 0
@@ -40,6 +40,11 @@ extern "C" {
 /* memory spaces of caller buffers */
 #define TJ_MEM_HOST 0   /* pageable or pinned host memory                  */
 #define TJ_MEM_DEVICE 1 /* device memory on the context's CUDA device      */
+/* tj_tick_in.out_mem flag: deliver result ids as int32 (tj_tick_out.ids32,
+ * id_bytes = 4) when every result id of the tick fits in int32; otherwise
+ * the tick falls back to int64 ids (id_bytes = 8).  Halves the result bytes
+ * a host caller downloads per tick; the values are the same. */
+#define TJ_OUT_IDS32 0x100
 
 /* rebuild policies — MethodConfig.rebuild, engine.py:70,163-170 */
 #define TJ_REBUILD_EVERY_TICK 0
@@ -71,7 +76,8 @@ typedef struct tj_tick_in {
   const double* q_xb;
   const double* q_yb;
   int32_t mem;     /* TJ_MEM_HOST / TJ_MEM_DEVICE for the inputs        */
-  int32_t out_mem; /* where tj_tick_out buffers should be delivered     */
+  int32_t out_mem; /* where tj_tick_out buffers should be delivered,
+                      optionally | TJ_OUT_IDS32                          */
 } tj_tick_in;
 
 /* Per-query results as CSR in input-query order; ids ascending per query
@@ -81,9 +87,10 @@ typedef struct tj_tick_out {
   int64_t n_q;
   int64_t n_results;
   const int64_t* offsets; /* n_q + 1 */
-  const int64_t* ids;     /* n_results */
+  const int64_t* ids;     /* n_results (id_bytes == 8; else NULL) */
   int32_t mem;
-  int32_t reserved;
+  int32_t id_bytes;       /* 8: ids holds the results; 4: ids32 does  */
+  const int32_t* ids32;   /* n_results (id_bytes == 4; else NULL) */
 } tj_tick_out;
 
 /* TickStats counters (engine.py:99-121) plus device stage times. */

@@ -21,6 +21,7 @@ LIB_PATH = os.environ.get("TJ_LIB_PATH") or os.path.join(LIB_DIR, "libtickjoin_b
 
 TJ_MEM_HOST = 0
 TJ_MEM_DEVICE = 1
+TJ_OUT_IDS32 = 0x100  # out_mem flag: result ids as int32 when they all fit
 TJ_REBUILD_EVERY_TICK = 0
 TJ_REBUILD_ADAPTIVE = 1
 
@@ -52,7 +53,7 @@ class TjTickIn(ctypes.Structure):
 
 class TjTickOut(ctypes.Structure):
     _fields_ = [("n_q", c_int64), ("n_results", c_int64), ("offsets", c_void_p), ("ids", c_void_p),
-                ("mem", c_int32), ("reserved", c_int32)]
+                ("mem", c_int32), ("id_bytes", c_int32), ("ids32", c_void_p)]
 
 
 class TjStats(ctypes.Structure):
@@ -155,25 +156,25 @@ class NativeContext:
             self._raise(rc, self.h)
 
     # -- hot path ---------------------------------------------------------
-    def tick_host(self, ids, xs, ys, qids, qxa, qya, qxb, qyb):
-        """Host arrays in, host CSR out (copied into fresh NumPy arrays)."""
+    def tick_host(self, ids, xs, ys, qids, qxa, qya, qxb, qyb, ids32: bool = False):
+        """Host arrays in, host CSR out (copied into fresh NumPy arrays).  ids32: ask for int32
+        result ids (TJ_OUT_IDS32); the returned array is int32 only if every id fit."""
         arrs = [np.ascontiguousarray(ids, np.int64), np.ascontiguousarray(xs, np.float64),
                 np.ascontiguousarray(ys, np.float64), np.ascontiguousarray(qids, np.int64),
                 np.ascontiguousarray(qxa, np.float64), np.ascontiguousarray(qya, np.float64),
                 np.ascontiguousarray(qxb, np.float64), np.ascontiguousarray(qyb, np.float64)]
         tin = TjTickIn(len(arrs[0]), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[3]),
                        _ptr(arrs[3]), _ptr(arrs[4]), _ptr(arrs[5]), _ptr(arrs[6]), _ptr(arrs[7]),
-                       TJ_MEM_HOST, TJ_MEM_HOST)
+                       TJ_MEM_HOST, TJ_MEM_HOST | (TJ_OUT_IDS32 if ids32 else 0))
         tout = TjTickOut()
         st = TjStats()
         self._check(self.lib.tj_tick(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
         m = tout.n_q
         offs = np.ctypeslib.as_array(ctypes.cast(tout.offsets, POINTER(c_int64)), shape=(m + 1,)).copy()
+        res = np.zeros(0, np.int32 if tout.id_bytes == 4 else np.int64)
         if tout.n_results:
-            res = np.ctypeslib.as_array(ctypes.cast(tout.ids, POINTER(c_int64)),
-                                        shape=(tout.n_results,)).copy()
-        else:
-            res = np.zeros(0, np.int64)
+            src, typ = (tout.ids32, c_int32) if tout.id_bytes == 4 else (tout.ids, c_int64)
+            res = np.ctypeslib.as_array(ctypes.cast(src, POINTER(typ)), shape=(tout.n_results,)).copy()
         return offs, res, st
 
     def tick_ptrs(self, n, ids, xs, ys, m, qids, qxa, qya, qxb, qyb, mem: int, out_mem: int):

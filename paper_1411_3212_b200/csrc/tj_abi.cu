@@ -654,6 +654,10 @@ int tj_destroy(tj_ctx* c) {
 int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) {
   if (!c || !in || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
   const int64_t n = in->n_obj, m = in->n_q;
+  const bool want32 = (in->out_mem & TJ_OUT_IDS32) != 0;
+  const int out_space = in->out_mem & ~TJ_OUT_IDS32;
+  if (out_space != TJ_MEM_HOST && out_space != TJ_MEM_DEVICE)
+    return fail(c, TJ_E_INVALID_ARG, "unknown output memory space");
   if (n < 0 || m < 0) return fail(c, TJ_E_INVALID_ARG, "negative size");
   if (n > INT32_MAX / 2 || m > INT32_MAX / 2) return fail(c, TJ_E_INVALID_ARG, "tick too large for 32-bit rows");
   if (n >= (int64_t(1) << 28)) return fail(c, TJ_E_INVALID_ARG, "more than 2^28 objects per tick is not supported");
@@ -821,18 +825,38 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
   // ---- deliver results ----------------------------------------------------
   out->n_q = m;
   out->n_results = R;
-  if (in->out_mem == TJ_MEM_DEVICE) {
+  // TJ_OUT_IDS32: narrow the ids on the device (into the idle merge scratch) when they all fit
+  bool use32 = false;
+  if (want32) {
+    use32 = true;
+    if (R > 0) {
+      k_narrow_ids<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(c->outids), P<int32_t>(c->scratch), R, c->d_hdr);
+      ++S.kernel_launches;
+      TJ_CUDA(cudaMemcpyAsync(&c->h_hdr->ids_wide, &c->d_hdr->ids_wide, sizeof(int32_t), cudaMemcpyDeviceToHost,
+                              c->st));
+      TJ_CUDA(cudaStreamSynchronize(c->st));
+      use32 = c->h_hdr->ids_wide == 0;
+    }
+  }
+  const int64_t idb = use32 ? 4 : 8;
+  out->id_bytes = (int32_t)idb;
+  out->ids = nullptr;
+  out->ids32 = nullptr;
+  if (out_space == TJ_MEM_DEVICE) {
     out->offsets = P<int64_t>(c->outoff);
-    out->ids = n ? P<int64_t>(c->outids) : nullptr;
+    if (use32) out->ids32 = R ? P<int32_t>(c->scratch) : nullptr;
+    else out->ids = n ? P<int64_t>(c->outids) : nullptr;
     out->mem = TJ_MEM_DEVICE;
   } else {
     if ((rc = ensure_host(c, c->h_off, c->h_off_bytes, (m + 1) * 8))) return rc;
-    if ((rc = ensure_host(c, c->h_ids, c->h_ids_bytes, R * 8))) return rc;
+    if ((rc = ensure_host(c, c->h_ids, c->h_ids_bytes, R * idb))) return rc;
     TJ_CUDA(cudaMemcpyAsync(c->h_off, c->outoff.p, (m + 1) * 8, cudaMemcpyDeviceToHost, c->st));
-    if (R) TJ_CUDA(cudaMemcpyAsync(c->h_ids, c->outids.p, R * 8, cudaMemcpyDeviceToHost, c->st));
+    if (R) TJ_CUDA(cudaMemcpyAsync(c->h_ids, use32 ? c->scratch.p : c->outids.p, R * idb, cudaMemcpyDeviceToHost,
+                                   c->st));
     TJ_CUDA(cudaStreamSynchronize(c->st));
     out->offsets = (const int64_t*)c->h_off;
-    out->ids = (const int64_t*)c->h_ids;
+    if (use32) out->ids32 = (const int32_t*)c->h_ids;
+    else out->ids = (const int64_t*)c->h_ids;
     out->mem = TJ_MEM_HOST;
   }
   if (stats) *stats = S;

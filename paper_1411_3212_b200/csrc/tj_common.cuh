@@ -53,6 +53,7 @@ struct DevHdr {
   int32_t dup;              // DuplicateResult detected
   int32_t oob;              // OutOfBounds (adaptive reuse: object outside old MBR)
   int32_t count_mismatch;   // CountMismatch
+  int32_t ids_wide;         // TJ_OUT_IDS32: some result id does not fit in int32
   int32_t n_big;            // queries queued for k_merge_big
   int32_t dbg;              // experiment switches (TJ_DEBUG env), 0 in production
   unsigned long long overfull2, overfull8;  // needs_rebuild counters

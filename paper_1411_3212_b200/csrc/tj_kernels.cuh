@@ -1420,6 +1420,18 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
   if (__any_sync(0xffffffffu, bad) && lane == 0) h->count_mismatch = 1;
 }
 
+// TJ_OUT_IDS32 delivery: result ids narrowed to int32 (flag if one does not fit)
+__global__ void __launch_bounds__(256) k_narrow_ids(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
+                                                    int64_t R, DevHdr* h) {
+  int wide = 0;
+  TJ_GRID_STRIDE(i, R) {
+    const long long v = __ldcs(reinterpret_cast<const long long*>(src) + i);
+    wide |= v != (long long)(int32_t)v;
+    __stcs(dst + i, (int32_t)v);
+  }
+  if (__any_sync(0xffffffffu, wide) && lane_id() == 0) h->ids_wide = 1;
+}
+
 // ---------------------------------------------------------------------------
 // CTA-wide sort of one segment (used only when object ids are not increasing
 // in input order: then lists must be sorted by id, decode.py:117).

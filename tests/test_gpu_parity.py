@@ -252,6 +252,24 @@ def test_decode_merge_paths_all_list_shapes(pkg, th):
     eng.close()
 
 
+def test_int32_id_delivery(pkg):
+    """TJ_OUT_IDS32: the same CSR with int32 ids; ids beyond int32 fall back to int64."""
+    from paper_1411_3212_b200 import _native
+
+    rng = np.random.default_rng(23)
+    n, m = 50_000, 5000
+    xs, ys, a, b, c, d = _rand_tick(rng, n, m)
+    qids = np.arange(m, dtype=np.int64)
+    ctx = _native.NativeContext(64, 12, True, 0, 0)
+    for ids in (np.arange(n, dtype=np.int64), np.sort(rng.choice(2**31 - 1, n, replace=False)).astype(np.int64),
+                np.arange(n, dtype=np.int64) * 50_000):  # the last: ids up to 2.5e9 > 2^31
+        o64, r64, _ = ctx.tick_host(ids, xs, ys, qids, a, b, c, d)
+        o32, r32, _ = ctx.tick_host(ids, xs, ys, qids, a, b, c, d, ids32=True)
+        assert np.array_equal(o64, o32) and np.array_equal(r64, r32.astype(np.int64))
+        assert r32.dtype == (np.int64 if ids.max() >= 2**31 else np.int32)
+    ctx.close()
+
+
 def test_covering_toggle_preserves_results(pkg):
     """test_engine.py:100-111 / acceptance C4 semantics."""
     cfg = pkg.WorkloadConfig(n_objects=4000, n_ticks=1, distribution="gaussian", n_hotspots=4, seed=8,
