@@ -45,6 +45,7 @@ struct tj_ctx {
   tj_config cfg{};
   int device = 0;
   int num_sms = 148;
+  int scatter_per_sm = 8;
   int join_blocks = 4;  // resident k_join CTAs per SM (occupancy API)
   cudaStream_t st = nullptr;
   cudaStream_t side = nullptr;             // object sort, concurrent with the query scatter
@@ -335,6 +336,7 @@ int launch_stage(tj_ctx* c, int stage) {
   const int F = std::min(lmax, kDenseTop);
   const int64_t n = c->n, m = c->m;
   const int Gn = grid_for(c, n), Gm = grid_for(c, m);
+  const int Gs = grid_for(c, m, c->scatter_per_sm);  // the query scatter shares the GPU with the object sort
   const int Gbig = c->num_sms * 8;
   ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial),
               c->lb_scan ? P<unsigned long long>(c->sstate) : nullptr, c->scan_words};
@@ -380,12 +382,12 @@ int launch_stage(tj_ctx* c, int stage) {
       return 3 + 5 * c->obj_passes;
     }
     case 1: {  // ---- K2: query -> leaf scatter (concurrent with the object sort) ----
-      k_query_count<<<Gm, 256, 0, st>>>(d);
+      k_query_count<<<Gs, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
       scan_launch(sp, LeafSqIn{d.leaf_cnt}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
                   (int64_t*)nullptr, st);
-      k_query_fill<<<Gm, 256, 0, st>>>(d);
+      k_query_fill<<<Gs, 256, 0, st>>>(d);
       k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
       return 10;
     }
@@ -489,7 +491,7 @@ bool capture_tick(tj_ctx* c, TickGraph& g) {
     if (cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal) != cudaSuccess) return false;
     g.launches[s] = launch_stage(c, s);
     cudaError_t e = cudaStreamEndCapture(cs, &graph);
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec[s], graph, 0);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&g.exec[s], graph, cudaGraphInstantiateFlagUseNodePriority);
     if (graph) cudaGraphDestroy(graph);
     if (e != cudaSuccess) return false;
   }
@@ -599,10 +601,17 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
   if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
   if (const char* ss = std::getenv("TJ_SERIAL_SORT")) c->serial_sort = std::atoi(ss) != 0;
+  if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  // side-stream priority (TJ_SIDE_PRIO=1: the object sort's blocks go first) measured no gain:
+  // the sort branch is latency-bound, not starved of SMs; default priority
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  int side_prio = prio_lo;
+  if (const char* sp = std::getenv("TJ_SIDE_PRIO")) side_prio = std::atoi(sp) ? prio_hi : prio_lo;
   if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaMalloc(&c->d_hdr, sizeof(DevHdr)) != cudaSuccess ||

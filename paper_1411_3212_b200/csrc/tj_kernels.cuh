@@ -546,18 +546,26 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
         uint32_t key[4], rank[4];
         const int ne = enum_small(w, ld, d.zmap, key, rank);
         int pos[4] = {0, 0, 0, 0};
+        uint32_t rc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (k < ne && leaf_on(d.leaf_active, rank[k])) {
             const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
             int4* c = d.leaf_cnt + rank[k];
             const int v = atomicAdd(cv ? &c->y : &c->x, 1);  // owned pairs, in order
+            const uint32_t packed = rank[k] | (cv ? 0x80000000u : 0u);
 #pragma unroll
-            for (int j = 0; j < 4; ++j) pos[j] = (j == cnt) ? v : pos[j];  // (no local-memory indexing)
+            for (int j = 0; j < 4; ++j) {  // (no local-memory indexing)
+              pos[j] = (j == cnt) ? v : pos[j];
+              rc[j] = (j == cnt) ? packed : rc[j];
+            }
             ++cnt;
           }
+        // the fill needs no window walk for these: their leaves (covering flag in bit 31) and places
         d.qpos[q] = make_int4(pos[0], pos[1], pos[2], pos[3]);
+        w = make_int4((int)rc[0], (int)rc[1], (int)rc[2], (int)rc[3]);
       } else {
+        d.qpos[q] = make_int4(-1, 0, 0, 0);  // a window the fill walks again
         enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
           if (!leaf_on(d.leaf_active, rank)) return;
           int4* c = d.leaf_cnt + rank;
@@ -590,24 +598,21 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   TJ_GRID_STRIDE(q, m) {
     const int n = d.nsub[q];
     if (n == 0) continue;
-    const Rect4 r = d.crect[q];  // clip and window from the count pass (one 32-byte and one 16-byte load)
-    const int4 w = d.qwin[q];
+    const Rect4 r = d.crect[q];  // clip from the count pass
+    const int4 p4 = d.qpos[q];
+    const int4 w = d.qwin[q];  // small window: its leaves as found by the count pass; else the window
     const int32_t base = d.qsbase[q];
-    if (is_small(w)) {
-      uint32_t key[4], rank[4];
-      const int ne = enum_small(w, ld, d.zmap, key, rank);
-      const int4 p4 = d.qpos[q];
+    if (p4.x >= 0) {
+      const uint32_t rc[4] = {(uint32_t)w.x, (uint32_t)w.y, (uint32_t)w.z, (uint32_t)w.w};
       const int pos[4] = {p4.x, p4.y, p4.z, p4.w};
-      int j = 0;
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (k < ne && leaf_on(d.leaf_active, rank[k])) {
-          const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
-          const int4 c = d.leaf_cnt[rank[k]];
-          const int pj = j == 0 ? pos[0] : j == 1 ? pos[1] : j == 2 ? pos[2] : pos[3];
-          const int32_t e = d.leaf_sbase[rank[k]] + (cv ? c.x + c.z : 0) + pj;
-          emit_subquery(d, base + j, rank[k], e, r);
-          ++j;
+        if (k < n) {
+          const uint32_t rank = rc[k] & 0x7fffffffu;
+          const bool cv = (rc[k] >> 31) != 0;
+          const int4 c = d.leaf_cnt[rank];
+          const int32_t e = d.leaf_sbase[rank] + (cv ? c.x + c.z : 0) + pos[k];
+          emit_subquery(d, base + k, rank, e, r);
         }
       continue;
     }
