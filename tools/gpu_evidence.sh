@@ -5,4 +5,4 @@ python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; 
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo bench=$?; tail -1 gpurun_out/bench.log | cut -c1-400
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo ref=$?; tail -1 gpurun_out/bench_ref.log | cut -c1-300
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/b_ncu.log 2>&1; echo launches=$?
-timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:k_decode_query|k_join|k_query_fill|k_query_count|k_radix_downsweep|k_gather|k_codes|k_mbr" --launch-skip 30 -c 9 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/prof_full.log 2>&1; echo ncu=$?
+timeout 1500 ncu --set full --clock-control none --import-source on -k "regex:k_decode_query|k_join|k_query_fill|k_query_count|k_radix_downsweep|k_gather|k_codes|k_mbr" --launch-skip 30 -c 14 -o gpurun_out/prof_full python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/prof_full.log 2>&1; echo ncu=$?
