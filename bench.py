@@ -530,7 +530,7 @@ def main(argv=None):
     ap.add_argument("--pool", type=int, default=3, help="distinct ticks generated and cycled")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--ref-sample", type=int, default=500_000)
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--e2e-contexts", type=int, default=3,
                     help="tj_tick contexts driven from this many host threads in the e2e leg (overlap of "
                          "uploads, compute and downloads across ticks)")
