@@ -19,6 +19,11 @@ constexpr int kScanThreads = 256;
 // ---------------------------------------------------------------------------
 constexpr int kScanItems = 8;  // items per thread per step: 8 independent loads in flight (ILP)
 constexpr int kScanTile = kScanThreads * kScanItems;
+// 8-byte tile entries padded by one slot per 16: the blocked accesses (thread t,
+// items 8t..8t+7, a 64-byte stride) and the striped ones both hit distinct
+// bank pairs within each half-warp instead of 16-way conflicts
+__device__ __forceinline__ int scan_pad(int i) { return i + (i >> 4); }
+constexpr int kScanTilePadded = kScanTile + kScanTile / 16;
 
 __device__ __forceinline__ void scan_chunk(int64_t n, int64_t G, int64_t blk, int64_t* b, int64_t* e) {
   const int64_t chunk = ((n + G - 1) / G + kScanTile - 1) / kScanTile * kScanTile;
@@ -74,7 +79,7 @@ __global__ void __launch_bounds__(kScanThreads)
 k_scan_down(In in, Out out, const int64_t* n_ptr, const DevHdr* h, const int64_t* partial) {
   if (h->abort) return;
   __shared__ int64_t sh[33];
-  __shared__ int64_t tile[kScanTile];
+  __shared__ int64_t tile[kScanTilePadded];
   int64_t b, e;
   scan_chunk(*n_ptr, gridDim.x, blockIdx.x, &b, &e);
   int64_t carry = partial[blockIdx.x];
@@ -85,28 +90,28 @@ k_scan_down(In in, Out out, const int64_t* n_ptr, const DevHdr* h, const int64_t
     for (int k = 0; k < kScanItems; ++k) {
       const int64_t i = base + k * kScanThreads + t;
       v[k] = i < e ? in(i) : 0;
-      tile[k * kScanThreads + t] = v[k];
+      tile[scan_pad(k * kScanThreads + t)] = v[k];
     }
     __syncthreads();
     int64_t blk[kScanItems];
     int64_t loc = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-      blk[k] = tile[t * kScanItems + k];
+      blk[k] = tile[scan_pad(t * kScanItems + k)];
       loc += blk[k];
     }
     int64_t tot;
     int64_t ex = carry + block_excl_scan(loc, sh, &tot);  // (contains __syncthreads)
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-      tile[t * kScanItems + k] = ex;
+      tile[scan_pad(t * kScanItems + k)] = ex;
       ex += blk[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
       const int64_t i = base + k * kScanThreads + t;
-      if (i < e) out(i, tile[k * kScanThreads + t], v[k]);
+      if (i < e) out(i, tile[scan_pad(k * kScanThreads + t)], v[k]);
     }
     carry += tot;
     __syncthreads();
@@ -129,7 +134,7 @@ __global__ void __launch_bounds__(kScanThreads)
 k_scan_lb(In in, Out out, const int64_t* n_ptr, DevHdr* h, int64_t* total_out, unsigned long long* state) {
   if (h->abort) return;
   __shared__ int64_t sh[33];
-  __shared__ int64_t tile[kScanTile];
+  __shared__ int64_t tile[kScanTilePadded];
   __shared__ int64_t s_tile, s_excl;
   const int64_t n = *n_ptr;
   const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
@@ -150,14 +155,14 @@ k_scan_lb(In in, Out out, const int64_t* n_ptr, DevHdr* h, int64_t* total_out, u
     for (int k = 0; k < kScanItems; ++k) {
       const int64_t i = base + k * kScanThreads + t;
       v[k] = i < n ? in(i) : 0;
-      tile[k * kScanThreads + t] = v[k];
+      tile[scan_pad(k * kScanThreads + t)] = v[k];
     }
     __syncthreads();
     int64_t blk[kScanItems];
     int64_t loc = 0;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-      blk[k] = tile[t * kScanItems + k];
+      blk[k] = tile[scan_pad(t * kScanItems + k)];
       loc += blk[k];
     }
     int64_t tot;
@@ -184,14 +189,14 @@ k_scan_lb(In in, Out out, const int64_t* n_ptr, DevHdr* h, int64_t* total_out, u
     ex += s_excl;
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
-      tile[t * kScanItems + k] = ex;
+      tile[scan_pad(t * kScanItems + k)] = ex;
       ex += blk[k];
     }
     __syncthreads();
 #pragma unroll
     for (int k = 0; k < kScanItems; ++k) {
       const int64_t i = base + k * kScanThreads + t;
-      if (i < n) out(i, tile[k * kScanThreads + t], v[k]);
+      if (i < n) out(i, tile[scan_pad(k * kScanThreads + t)], v[k]);
     }
     __syncthreads();
   }
