@@ -2,7 +2,8 @@
 
 This module restates, in columnar NumPy, the reference algorithm of the
 `tickjoin` package (arXiv 1411.3212 desk-scale reimplementation) for the one
-path this repository accelerates: the QUAD method's per-tick pipeline.  It is
+path this repository accelerates: the QUAD method's per-tick pipeline, and the
+uniform-grid (UG) index that feeds the same join and decode.  It is
 the checker that the CUDA path is compared against; only `tests/`,
 `__graft_entry__.smoke()` and `bench.py`'s CPU-baseline leg may import it.
 The product (`paper_1411_3212_b200`) never imports it and fails loudly when
@@ -403,8 +404,18 @@ def run_tick(ids, xs, ys, qids, qxa, qya, qxb, qyb, th_quad=384, l_max=L_MAX,
                                           index.mbr)
     out.keep = keep
     obj_cell = map_objects(xs, ys, index)
-    out.obj_cell = obj_cell
     sub = split_queries(cxa, cya, cxb, cyb, index)
+    _join_decode(out, ids, xs, ys, m, keep, cxa, cya, cxb, cyb, obj_cell, sub, covering_optimization, keep_tasks)
+    out.counters.update(n_leaves=int(len(index.leaves)), l_deep=int(index.l_deep))
+    return out
+
+
+def _join_decode(out, ids, xs, ys, m, keep, cxa, cya, cxb, cyb, obj_cell, sub, covering_optimization,
+                 keep_tasks):
+    """The index-independent part of a tick: directory, per-cell bitmaps,
+    decode, covering expansion, canonical merge and counters
+    (engine.py:199-259, 269-329).  Shared by the QUAD and UG methods."""
+    out.obj_cell = obj_cell
     if not covering_optimization:  # engine.py:199-208
         sub = OracleSubqueries(sub.qrow, sub.cell, np.zeros(len(sub.cell), bool))
     out.sub = sub
@@ -471,9 +482,112 @@ def run_tick(ids, xs, ys, qids, qxa, qya, qxb, qyb, th_quad=384, l_max=L_MAX,
         results_total=int(len(alli)),
         occupancy_mean=float(occ.mean()) if len(occ) else 0.0,
         occupancy_var=float(occ.var()) if len(occ) else 0.0,
-        n_leaves=int(len(index.leaves)),
-        l_deep=int(index.l_deep),
     )
+
+
+# --------------------------------------------------------------------------
+# UG: the uniform-grid method (grid.py) over the same join / decode
+# --------------------------------------------------------------------------
+
+MAX_SPLIT_FACTOR = 1 << 16  # grid.py:22
+
+
+def grid_axis_cells(values, origin: float, extent: float, n: int) -> np.ndarray:
+    """floor((v - origin) * (n / extent)) clamped to n - 1; 0 when extent == 0.
+    grid.py:42-46 (the scale is one Python float division, as there)."""
+    values = np.asarray(values, np.float64)
+    if extent > 0:
+        return np.minimum((values - origin) * (n / extent), n - 1).astype(np.int64)
+    return np.zeros(values.shape, np.int64)
+
+
+def ug_map_objects(xs, ys, mbr, split_factor: int) -> np.ndarray:
+    """Cell id = Morton(i, j) of the object's grid cell.  grid.py:55-68."""
+    xa, ya, xb, yb = mbr
+    xs = np.asarray(xs, np.float64)
+    ys = np.asarray(ys, np.float64)
+    if len(xs) and (np.any(xs < xa) or np.any(xs > xb) or np.any(ys < ya) or np.any(ys > yb)):
+        raise OracleError("OutOfBounds", "object outside the grid MBR")
+    i = grid_axis_cells(xs, xa, xb - xa, split_factor)
+    j = grid_axis_cells(ys, ya, yb - ya, split_factor)
+    return morton(i, j)
+
+
+def ug_split_queries(cxa, cya, cxb, cyb, mbr, split_factor: int) -> OracleSubqueries:
+    """One subquery per (clipped query, grid cell of its window), cells of a
+    query in row-major order (i fastest), covering flag against the cell's
+    extent inside the MBR.  grid.py:71-112."""
+    xa, ya, xb, yb = mbr
+    width, height = xb - xa, yb - ya
+    cell_w = width / split_factor  # grid.py:39
+    cell_h = height / split_factor
+    i0 = grid_axis_cells(cxa, xa, width, split_factor)
+    j0 = grid_axis_cells(cya, ya, height, split_factor)
+    i1 = grid_axis_cells(cxb, xa, width, split_factor)
+    j1 = grid_axis_cells(cyb, ya, height, split_factor)
+    per = (i1 - i0 + 1) * (j1 - j0 + 1)
+    if per.sum() == 0:
+        return OracleSubqueries(np.zeros(0, np.int64), np.zeros(0, np.int64), np.zeros(0, bool))
+    offs = np.concatenate([[0], np.cumsum(per)[:-1]])
+    qrow = np.repeat(np.arange(len(per)), per)
+    pos = np.arange(int(per.sum())) - offs[qrow]
+    wdt = (i1 - i0 + 1)[qrow]
+    ii = i0[qrow] + pos % wdt
+    jj = j0[qrow] + pos // wdt
+    lxa = xa + ii * cell_w
+    lya = ya + jj * cell_h
+    cov = ((cxa[qrow] <= lxa) & (cxb[qrow] >= np.minimum(lxa + cell_w, xb))
+           & (cya[qrow] <= lya) & (cyb[qrow] >= np.minimum(lya + cell_h, yb)))
+    return OracleSubqueries(qrow.astype(np.int64), morton(ii, jj), cov)
+
+
+def ug_indexing_cost(d: OracleDirectory) -> int:
+    """Containment tests + decoded bitmap bits over the task cells.  grid.py:125-138."""
+    n_obj = d.o_end - d.o_start
+    n_isq = d.i_end - d.i_start
+    mask = (n_obj > 0) & (n_isq > 0)
+    blocks = -(n_obj[mask] // -WORD_BITS)
+    return int((n_isq[mask] * n_obj[mask]).sum()) + int((n_isq[mask] * blocks * WORD_BITS).sum())
+
+
+def ug_sweep_costs(xs, ys, qxa, qya, qxb, qyb, candidates) -> list:
+    """(split factor, cost) per candidate on one tick; the engine keeps the
+    cheapest, ties to the smaller.  grid.py:141-165, engine.py:154-156."""
+    xs = np.asarray(xs, np.float64)
+    ys = np.asarray(ys, np.float64)
+    mbr = mbr_of(xs, ys)
+    keep, cxa, cya, cxb, cyb = clip_rects(np.asarray(qxa, np.float64), np.asarray(qya, np.float64),
+                                          np.asarray(qxb, np.float64), np.asarray(qyb, np.float64), mbr)
+    out = []
+    for sf in candidates:
+        oc = ug_map_objects(xs, ys, mbr, sf)
+        sub = ug_split_queries(cxa, cya, cxb, cyb, mbr, sf)
+        out.append((int(sf), ug_indexing_cost(group_by_cell(oc, sub))))
+    return out
+
+
+def run_tick_ug(ids, xs, ys, qids, qxa, qya, qxb, qyb, split_factor: int, covering_optimization=True,
+                keep_tasks=False) -> OracleTick:
+    """One UG tick end to end (engine.py:178-259 with the ug branch, 152-161)."""
+    if not 1 <= split_factor <= MAX_SPLIT_FACTOR:
+        raise OracleError("BadSplitFactor", str(split_factor))
+    ids = np.asarray(ids, np.int64)
+    xs = np.asarray(xs, np.float64)
+    ys = np.asarray(ys, np.float64)
+    m = len(qids)
+    out = OracleTick()
+    if len(ids) == 0:  # engine.py:188-190
+        out.offsets = np.zeros(m + 1, np.int64)
+        out.result_ids = np.zeros(0, np.int64)
+        return out
+    mbr = mbr_of(xs, ys)
+    keep, cxa, cya, cxb, cyb = clip_rects(np.asarray(qxa, np.float64), np.asarray(qya, np.float64),
+                                          np.asarray(qxb, np.float64), np.asarray(qyb, np.float64), mbr)
+    out.keep = keep
+    obj_cell = ug_map_objects(xs, ys, mbr, split_factor)
+    sub = ug_split_queries(cxa, cya, cxb, cyb, mbr, split_factor)
+    _join_decode(out, ids, xs, ys, m, keep, cxa, cya, cxb, cyb, obj_cell, sub, covering_optimization, keep_tasks)
+    out.counters.update(split_factor=int(split_factor))
     return out
 
 

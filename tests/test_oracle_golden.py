@@ -236,3 +236,66 @@ def test_oracle_adaptive_rebuild_matches_reference(name):
         t = qo.run_tick(tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb, th_quad=th,
                         index=index)
         assert qo.result_digest(tick.qids, t.offsets, t.result_ids) == want["digest"]
+
+
+# ------------------------------------------------------------ uniform grid --
+
+def _ug_runs():
+    import json
+    import os
+
+    with open(os.path.join(os.path.dirname(__file__), "golden", "ug.json")) as fp:
+        return json.load(fp)
+
+
+def _ug_ticks(run):
+    from paper_1411_3212_b200.workload import WorkloadConfig, iter_ticks
+
+    cfg = dict(run["workload"])
+    cfg["query_side"] = tuple(cfg["query_side"])
+    return list(iter_ticks(WorkloadConfig(**cfg)))
+
+
+def _ug_subq_sha(t):
+    import hashlib
+
+    qrow = np.flatnonzero(t.keep)[t.sub.qrow].astype(np.int32)
+    return hashlib.sha256(qrow.tobytes() + t.sub.cell.astype(np.int32).tobytes()
+                          + t.sub.covering.astype(np.uint8).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", sorted(_ug_runs()))
+def test_oracle_ug_matches_reference(name):
+    """UG method (grid.py:35-112 + the shared join/decode): results digest,
+    TickStats counters and the subquery list (row-major per query) equal the
+    reference engine's (tests/golden/make_ug_golden.py), for power-of-two and
+    other split factors."""
+    import os
+
+    run = _ug_runs()[name]
+    subq = np.load(os.path.join(os.path.dirname(__file__), "golden", "ug_subqueries.npz"))
+    for t_idx, (tick, want) in enumerate(zip(_ug_ticks(run), run["ticks"])):
+        for sf, w in want["split"].items():
+            t = qo.run_tick_ug(tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb,
+                               split_factor=int(sf))
+            assert qo.result_digest(tick.qids, t.offsets, t.result_ids) == w["digest"], (t_idx, sf)
+            for k, v in w["stats"].items():
+                assert t.counters[k] == v, (t_idx, sf, k)
+            if "subq_sha256" in w:
+                assert _ug_subq_sha(t) == w["subq_sha256"], (t_idx, sf)
+                key = f"{name}_t{t_idx}_sf{sf}_cell"
+                if key in subq.files:
+                    assert np.array_equal(t.sub.cell, subq[key])
+
+
+@pytest.mark.parametrize("name", sorted(_ug_runs()))
+def test_oracle_ug_sweep_matches_reference(name):
+    """Split-factor sweep (grid.py:125-165, engine.py:154-156): per-candidate
+    cost and the chosen factor on the first tick."""
+    run = _ug_runs()[name]
+    tick = _ug_ticks(run)[0]
+    want = run["ticks"][0]["sweep"]
+    cands = [c for c, _ in want["costs"]]
+    costs = qo.ug_sweep_costs(tick.xs, tick.ys, tick.qxa, tick.qya, tick.qxb, tick.qyb, cands)
+    assert [list(c) for c in costs] == want["costs"]
+    assert min(costs, key=lambda c: (c[1], c[0]))[0] == want["chosen"]
