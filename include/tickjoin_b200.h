@@ -52,14 +52,17 @@ extern "C" {
 
 typedef struct tj_ctx tj_ctx;
 
-/* MethodConfig fields read by the QUAD path (engine.py:57-96). */
+/* MethodConfig fields read by the QUAD and UG paths (engine.py:57-96). */
 typedef struct tj_config {
   int32_t th_quad;               /* occupancy threshold, >= 1 (default 384)  */
   int32_t l_max;                 /* deepest level, 1..12 (default 12)        */
   int32_t covering_optimization; /* 1: covering subqueries skip bitmaps      */
   int32_t rebuild;               /* TJ_REBUILD_*                             */
   int32_t device;                /* CUDA device ordinal                      */
-  int32_t reserved;
+  int32_t split_factor;          /* 0: QUAD (quadtree index).  1..4096: the
+                                    uniform-grid method "ug" with this many
+                                    columns and rows (grid.py:35-40); th_quad,
+                                    l_max and rebuild are then unused         */
 } tj_config;
 
 /* One tick of input as structure-of-arrays (TickBatch, geometry.py:58-64,

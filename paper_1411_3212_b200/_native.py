@@ -42,7 +42,7 @@ _ERRORS = {
 
 class TjConfig(ctypes.Structure):
     _fields_ = [("th_quad", c_int32), ("l_max", c_int32), ("covering_optimization", c_int32),
-                ("rebuild", c_int32), ("device", c_int32), ("reserved", c_int32)]
+                ("rebuild", c_int32), ("device", c_int32), ("split_factor", c_int32)]
 
 
 class TjTickIn(ctypes.Structure):
@@ -125,9 +125,11 @@ def _ptr(a: np.ndarray) -> int:
 class NativeContext:
     """Owns one `tj_ctx` (one CUDA device, one stream)."""
 
-    def __init__(self, th_quad: int, l_max: int, covering: bool, rebuild: int = 0, device: int = 0):
+    def __init__(self, th_quad: int, l_max: int, covering: bool, rebuild: int = 0, device: int = 0,
+                 split_factor: int = 0):
+        """split_factor > 0: the uniform-grid method ("ug") with that many cells per side."""
         self.lib = load_library()
-        cfg = TjConfig(th_quad, l_max, 1 if covering else 0, rebuild, device, 0)
+        cfg = TjConfig(th_quad, l_max, 1 if covering else 0, rebuild, device, split_factor)
         h = c_void_p()
         rc = self.lib.tj_create(ctypes.byref(cfg), ctypes.byref(h))
         if rc != 0:

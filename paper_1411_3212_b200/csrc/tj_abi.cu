@@ -46,6 +46,7 @@ struct tj_ctx {
   int device = 0;
   int num_sms = 148;
   int scatter_per_sm = 8;
+  int ug_sf = 0;  // method "ug": cells per side (cfg.l_max then holds ceil(log2) of it)
   int join_blocks = 4;  // resident k_join CTAs per SM (occupancy API)
   cudaStream_t st = nullptr;
   cudaStream_t side = nullptr;             // object sort, concurrent with the query scatter
@@ -174,7 +175,7 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   // leaves: <= 4 + 3*(#split nodes); a level holds <= n/(th+1) split nodes
   const int64_t Zmax = int64_t(1) << (2 * lmax);
   int64_t lcap = 4 + 3 * (int64_t)(lmax > 1 ? lmax - 1 : 0) * (n / (th + 1) + 1);
-  c->cap_L = std::min(lcap, Zmax);
+  c->cap_L = c->ug_sf ? Zmax : std::min(lcap, Zmax);  // a uniform grid: every cell is a leaf
   ENS(code, n * 4);
   ENS(okey0, n * 4);
   ENS(okey1, n * 4);
@@ -357,9 +358,14 @@ int launch_stage(tj_ctx* c, int stage) {
       k_mbr<<<Gn, 256, 0, st>>>(d);
       k_finalize_mbr<<<1, 1, 0, st>>>(h);
       k_codes<<<Gn, 256, 0, st>>>(d);
-      for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
-      k_finalize_index<<<1, 1, 0, st>>>(h);
-      k_cell_level<<<Gbig, 256, 0, st>>>(d);
+      if (c->ug_sf) {  // uniform grid: every cell of the l_max grid is a leaf (no tree to build)
+        k_finalize_index<<<1, 1, 0, st>>>(h);
+        cudaMemsetAsync(d.clev, lmax, int64_t(1) << (2 * lmax), st);
+      } else {
+        for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
+        k_finalize_index<<<1, 1, 0, st>>>(h);
+        k_cell_level<<<Gbig, 256, 0, st>>>(d);
+      }
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
       scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
@@ -369,7 +375,7 @@ int launch_stage(tj_ctx* c, int stage) {
         k_shard_mark<<<Gbig, 256, 0, st>>>(d);
       }
       // 3 launches per scan
-      return 12 + F + (c->shard_n > 1 ? 4 : 0);
+      return (c->ug_sf ? 11 : 12 + F) + (c->shard_n > 1 ? 4 : 0);
     case kSortStage: {  // ---- K1's last part: objects into leaf order (side stream) ----
       cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
@@ -438,7 +444,8 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.cap_L = c->cap_L;
   H.kmin_x = H.kmin_y = ~0ull;
   H.kmax_x = H.kmax_y = 0ull;
-  H.l_deep = 1;
+  H.l_deep = c->ug_sf ? c->cfg.l_max : 1;  // a uniform grid has all its cells at one level
+  H.grid_sf = c->ug_sf;
   H.shard_rank = c->shard_rank;
   H.shard_n = c->shard_n;
   if (c->reuse) {  // adaptive reuse: the index's MBR, scales, depth and leaves
@@ -447,6 +454,7 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
     H.width = I.width; H.height = I.height;
     H.wpos = I.wpos; H.hpos = I.hpos;
     H.sx_max = I.sx_max; H.sy_max = I.sy_max; H.sx_deep = I.sx_deep; H.sy_deep = I.sy_deep;
+    H.side_deep = I.side_deep;
     for (int l = 0; l <= kMaxLevel; ++l) {
       H.lw[l] = I.lw[l];
       H.lh[l] = I.lh[l];
@@ -584,9 +592,14 @@ const char* tj_last_error(const tj_ctx* ctx) { return ctx ? ctx->err.c_str() : g
 int tj_create(const tj_config* cfg, tj_ctx** out) {
   tj_ctx* c = nullptr;
   if (!cfg || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
-  // MethodConfig.validate for the quad method (engine.py:73-88)
-  if (cfg->th_quad < 1) return fail(c, TJ_E_BAD_CONFIG, "th_quad must be >= 1");
-  if (cfg->l_max < 1 || cfg->l_max > kMaxLevel) return fail(c, TJ_E_BAD_CONFIG, "l_max must be in [1, 12]");
+  // MethodConfig.validate (engine.py:73-88)
+  if (cfg->split_factor < 0) return fail(c, TJ_E_BAD_CONFIG, "split_factor must be >= 1");
+  if (cfg->split_factor > (1 << kMaxLevel))
+    return fail(c, TJ_E_BAD_CONFIG, "split factors above 4096 are not supported on the device path");
+  if (cfg->split_factor == 0) {
+    if (cfg->th_quad < 1) return fail(c, TJ_E_BAD_CONFIG, "th_quad must be >= 1");
+    if (cfg->l_max < 1 || cfg->l_max > kMaxLevel) return fail(c, TJ_E_BAD_CONFIG, "l_max must be in [1, 12]");
+  }
   if (cfg->rebuild != TJ_REBUILD_EVERY_TICK && cfg->rebuild != TJ_REBUILD_ADAPTIVE)
     return fail(c, TJ_E_BAD_CONFIG, "unknown rebuild policy");
   int ndev = 0;
@@ -597,6 +610,14 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   if (cfg->device < 0 || cfg->device >= ndev) return fail(c, TJ_E_NO_DEVICE, "device ordinal out of range");
   c = new tj_ctx();
   c->cfg = *cfg;
+  if (cfg->split_factor > 0) {  // method "ug": the grid as the leaf level of a 2^L x 2^L cell map
+    c->ug_sf = cfg->split_factor;
+    int L = 1;
+    while ((1 << L) < cfg->split_factor) ++L;
+    c->cfg.l_max = L;
+    c->cfg.th_quad = 1;
+    c->cfg.rebuild = TJ_REBUILD_EVERY_TICK;
+  }
   c->device = cfg->device;
   if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
   if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
@@ -907,7 +928,7 @@ int load_leaves(tj_ctx* c, LeafView& lv) {
   for (int64_t r = 0; r < L; ++r) {
     const int64_t lev = lv.code[r] >> kLevelShift;
     const int64_t z = lv.code[r] & kPayloadMask;
-    lv.packed[r] = (lev << sh) | z;
+    lv.packed[r] = c->ug_sf ? z : (lev << sh) | z;  // ug: cell id = Morton(i, j) (grid.py:68)
   }
   lv.order.resize(L);
   for (int64_t r = 0; r < L; ++r) lv.order[r] = r;
@@ -918,12 +939,41 @@ int load_leaves(tj_ctx* c, LeafView& lv) {
 // Directory entries of leaf r's block [e0, e0 + cnt) in the reference's
 // order (ascending slot = query input order, directory.py:131): the device
 // keeps fill order inside a block; entry -> slot inverts the slots' entries.
+// Method "ug": a query's subqueries are listed row-major over its window
+// (grid.py:91-97), the device keeps them in Morton order; pos[slot] = the
+// slot's index in the reference's list (identity for the quadtree).
+int ug_ref_pos(tj_ctx* c, const std::vector<int2>& le, std::vector<int64_t>& pos) {
+  pos.resize(le.size());
+  for (size_t s = 0; s < le.size(); ++s) pos[s] = (int64_t)s;
+  if (!c->ug_sf) return TJ_OK;
+  std::vector<int32_t> nsub;
+  std::vector<uint32_t> code;
+  int rc;
+  if ((rc = d2h(c, nsub, c->nsub.p, c->m)) || (rc = d2h(c, code, c->lcode.p, c->last.L))) return rc;
+  auto rowmajor = [&](int64_t s) {
+    const uint32_t z = code[le[s].x] & kPayloadMask;
+    return (uint64_t(compact2(z >> 1)) << 32) | compact2(z);  // (j, i)
+  };
+  std::vector<int64_t> tmp;
+  int64_t s0 = 0;
+  for (int64_t q = 0; q < c->m; ++q) {
+    const int k = nsub[q];
+    tmp.resize(k);
+    for (int j = 0; j < k; ++j) tmp[j] = s0 + j;
+    std::sort(tmp.begin(), tmp.end(), [&](int64_t a, int64_t b) { return rowmajor(a) < rowmajor(b); });
+    for (int j = 0; j < k; ++j) pos[tmp[j]] = s0 + j;
+    s0 += k;
+  }
+  return TJ_OK;
+}
+
 int entry_slots(tj_ctx* c, std::vector<int32_t>& eslot) {
   std::vector<int2> le;
+  std::vector<int64_t> pos;
   int rc;
-  if ((rc = d2h(c, le, c->sqle.p, c->last.S))) return rc;
+  if ((rc = d2h(c, le, c->sqle.p, c->last.S)) || (rc = ug_ref_pos(c, le, pos))) return rc;
   eslot.assign(le.size(), -1);
-  for (size_t s = 0; s < le.size(); ++s) eslot[le[s].y] = (int32_t)s;
+  for (size_t s = 0; s < le.size(); ++s) eslot[le[s].y] = (int32_t)pos[s];
   return TJ_OK;
 }
 std::vector<int32_t> block_in_ref_order(const std::vector<int32_t>& eslot, int64_t e0, int64_t cnt) {
@@ -1002,13 +1052,16 @@ int tj_get_subqueries(tj_ctx* c, int64_t* count, int64_t* q_row, int64_t* cell, 
   std::vector<int2> le;
   std::vector<int32_t> nsub;
   if ((rc = d2h(c, le, c->sqle.p, S)) || (rc = d2h(c, nsub, c->nsub.p, c->m))) return rc;
+  std::vector<int64_t> pos;
+  if ((rc = ug_ref_pos(c, le, pos))) return rc;
   int64_t s = 0;  // slots are grouped per query in input order (nsub each)
   for (int64_t q = 0; q < c->m; ++q)
     for (int32_t j = 0; j < nsub[q]; ++j, ++s) {
       const int32_t leaf = le[s].x;
-      if (q_row) q_row[s] = q;
-      if (cell) cell[s] = lv.packed[leaf];
-      if (covering) covering[s] = (uint8_t)(le[s].y - lv.sbase[leaf] >= lv.nisq[leaf]);
+      const int64_t p = pos[s];
+      if (q_row) q_row[p] = q;
+      if (cell) cell[p] = lv.packed[leaf];
+      if (covering) covering[p] = (uint8_t)(le[s].y - lv.sbase[leaf] >= lv.nisq[leaf]);
     }
   return TJ_OK;
 }

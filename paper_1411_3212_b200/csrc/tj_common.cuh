@@ -54,6 +54,8 @@ struct DevHdr {
   int32_t oob;              // OutOfBounds (adaptive reuse: object outside old MBR)
   int32_t count_mismatch;   // CountMismatch
   int32_t ids_wide;         // TJ_OUT_IDS32: some result id does not fit in int32
+  int32_t grid_sf;          // uniform grid (method "ug"): cells per side; 0 = quadtree
+  uint32_t side_deep;       // cells per side of the l_deep grid (2^l_deep, or grid_sf)
   int32_t n_big;            // queries queued for k_merge_big
   int32_t dbg;              // experiment switches (TJ_DEBUG env), 0 in production
   unsigned long long overfull2, overfull8;  // needs_rebuild counters

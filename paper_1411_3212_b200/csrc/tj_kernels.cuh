@@ -168,12 +168,17 @@ __global__ void k_finalize_mbr(DevHdr* h) {
   h->height = __dsub_rn(h->yb, h->ya);
   h->wpos = h->width > 0.0;
   h->hpos = h->height > 0.0;
-  const double side = (double)(1u << h->l_max);
+  // quadtree: 2^l_max cells per side; uniform grid: split_factor (grid.py:39-46)
+  const double side = h->grid_sf ? (double)h->grid_sf : (double)(1u << h->l_max);
   h->sx_max = h->wpos ? __ddiv_rn(side, h->width) : 0.0;
   h->sy_max = h->hpos ? __ddiv_rn(side, h->height) : 0.0;
   for (int l = 0; l <= kMaxLevel; ++l) {
     h->lw[l] = __ddiv_rn(h->width, (double)(1u << l));
     h->lh[l] = __ddiv_rn(h->height, (double)(1u << l));
+  }
+  if (h->grid_sf) {  // the grid's cells are the leaves of level l_max: cell_w = width / split_factor
+    h->lw[h->l_max] = __ddiv_rn(h->width, (double)h->grid_sf);
+    h->lh[h->l_max] = __ddiv_rn(h->height, (double)h->grid_sf);
   }
 }
 
@@ -186,7 +191,7 @@ __global__ void __launch_bounds__(256) k_codes(const Dev d) {
   DevHdr* h = d.h;
   const int64_t n = h->n;
   const int lmax = h->l_max, F = h->F;
-  const uint32_t side = 1u << lmax;
+  const uint32_t side = h->grid_sf ? (uint32_t)h->grid_sf : 1u << lmax;
   const double xa = h->xa, ya = h->ya, sx = h->sx_max, sy = h->sy_max;
   const int wpos = h->wpos, hpos = h->hpos;
   const int sh = 2 * (lmax - F);
@@ -242,7 +247,8 @@ __global__ void __launch_bounds__(256) k_pyr_level(const Dev d, int l) {
 __global__ void k_finalize_index(DevHdr* h) {
   if (h->abort) return;
   h->Z = int64_t(1) << (2 * h->l_deep);
-  const double side = (double)(1u << h->l_deep);
+  h->side_deep = h->grid_sf ? (uint32_t)h->grid_sf : 1u << h->l_deep;
+  const double side = (double)h->side_deep;
   h->sx_deep = h->wpos ? __ddiv_rn(side, h->width) : 0.0;
   h->sy_deep = h->hpos ? __ddiv_rn(side, h->height) : 0.0;
 }
@@ -535,7 +541,7 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
   const double xa = h->xa, ya = h->ya, xb = h->xb, yb = h->yb;
   const double sx = h->sx_deep, sy = h->sy_deep;
   const int wpos = h->wpos, hpos = h->hpos, ld = h->l_deep;
-  const uint32_t side = 1u << ld;
+  const uint32_t side = h->side_deep;
   const int cov_on = h->covering;
   TJ_GRID_STRIDE(q, m) {
     Rect4 r;
@@ -876,7 +882,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       const uint32_t code = d.leaf_code[r];
       const int lev = (int)(code >> kLevelShift);
       const uint32_t z = code & kPayloadMask;
-      const double inv = 1.0 / (double)(1u << lev);
+      const double inv = 1.0 / (h->grid_sf ? (double)h->grid_sf : (double)(1u << lev));
       bx = gxa + (double)compact2(z) * inv * gw;
       by = gya + (double)compact2(z >> 1) * inv * gh;
       // kNK buckets across the leaf: sx_max = 2^l_max / width

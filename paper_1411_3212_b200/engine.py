@@ -4,9 +4,12 @@ Same names, fields, defaults and error behaviour as `tickjoin/engine.py`
 (`MethodConfig` 57-96, `TickStats` 99-121, `RunReport` 124-134, `Engine`
 137-402, module-level `process_tick`/`run` 405-417, QoS helpers 42-54) for
 method "quad".  Underneath, one `tj_tick` call (include/tickjoin_b200.h) runs
-the whole tick on the GPU.  Other reference methods ("ug", "ug_baseline")
-are not built here: asking for them raises `BadConfig` — there is no CPU or
-multi-backend fallback.
+the whole tick on the GPU.  Method "ug" (the uniform grid, `grid.py`) runs
+the same kernels with the grid's cells as the leaves (split factors up to
+4096; `split_factor=None` sweeps the candidates on the first tick, each
+candidate's cost measured by the device pipeline).  "ug_baseline" is not built
+here: asking for it raises `BadConfig` — there is no CPU or multi-backend
+fallback.
 
 Besides the object API, `Engine.process_columns` is the columnar fast path
 (NumPy host arrays or CUDA tensors in, CSR out) that avoids building millions
@@ -30,7 +33,9 @@ from .workload import ColumnarTick, WorkloadRun
 
 L_MAX = 12
 METHODS = ("ug", "ug_baseline", "quad")
-BUILT_METHODS = ("quad",)
+BUILT_METHODS = ("quad", "ug")
+MAX_DEVICE_SPLIT_FACTOR = 4096  # the grid is kept as a dense 2^12 x 2^12 cell map
+DEFAULT_SWEEP = (16, 256, 16)  # engine.py:30
 
 
 @dataclass(frozen=True)
@@ -73,11 +78,17 @@ class MethodConfig:
         if self.method not in METHODS:
             raise BadConfig(f"unknown method {self.method!r}")
         if self.method not in BUILT_METHODS:
-            raise BadConfig(f"method {self.method!r} is not part of the B200 build (quad only)")
-        if self.th_quad < 1:
-            raise BadConfig("th_quad must be >= 1")
-        if not 1 <= self.l_max <= L_MAX:
-            raise BadConfig(f"l_max must be in [1, {L_MAX}]")
+            raise BadConfig(f"method {self.method!r} is not part of the B200 build (quad, ug)")
+        if self.method == "quad":
+            if self.th_quad < 1:
+                raise BadConfig("th_quad must be >= 1")
+            if not 1 <= self.l_max <= L_MAX:
+                raise BadConfig(f"l_max must be in [1, {L_MAX}]")
+        elif self.split_factor is not None:
+            if self.split_factor < 1:
+                raise BadConfig("split_factor must be >= 1")
+            if self.split_factor > MAX_DEVICE_SPLIT_FACTOR:
+                raise BadConfig(f"split factors above {MAX_DEVICE_SPLIT_FACTOR} are not supported on the B200 path")
         if self.schedule not in ("heaviest_first", "unordered"):
             raise BadConfig(f"unknown schedule {self.schedule!r}")
         if self.n_workers < 1 or self.chunk_size < 1 or self.sim_processors < 1:
@@ -88,6 +99,10 @@ class MethodConfig:
     @property
     def name(self) -> str:
         return self.label or self.method
+
+    def sweep_candidates(self) -> list:
+        lo, hi, step = self.sweep or DEFAULT_SWEEP  # engine.py:93-95
+        return list(range(lo, hi + 1, step))
 
 
 @dataclass
@@ -164,9 +179,35 @@ class Engine:
         self.cfg = cfg
         self._split_factor = cfg.split_factor
         self.sweep_costs = None
+        self._ctx = None
+        if cfg.method == "quad" or self._split_factor is not None:
+            self._ctx = self._make_ctx(self._split_factor)
+
+    def _make_ctx(self, split_factor):
+        cfg = self.cfg
+        if cfg.method == "ug":
+            return _native.NativeContext(1, L_MAX, cfg.covering_optimization, 0, cfg.device, split_factor)
         rebuild = _native.TJ_REBUILD_ADAPTIVE if cfg.rebuild == "adaptive" else _native.TJ_REBUILD_EVERY_TICK
-        self._ctx = _native.NativeContext(cfg.th_quad, cfg.l_max, cfg.covering_optimization, rebuild,
-                                          cfg.device)
+        return _native.NativeContext(cfg.th_quad, cfg.l_max, cfg.covering_optimization, rebuild, cfg.device)
+
+    def _sweep(self, ids, xs, ys, qids, qxa, qya, qxb, qyb) -> None:
+        """Split-factor sweep on the first tick (engine.py:152-156, grid.py:125-165): each
+        candidate's cost is tests + decoded bitmap bits, as the device pipeline counts them
+        (containment_tests + decoded_bits); the cheapest wins, ties to the smaller factor.
+        The sweep ignores covering_optimization, like the reference's."""
+        costs = []
+        for sf in self.cfg.sweep_candidates():
+            if sf < 1 or sf > MAX_DEVICE_SPLIT_FACTOR:
+                raise BadConfig(f"sweep candidate {sf} outside [1, {MAX_DEVICE_SPLIT_FACTOR}]")
+            ctx = _native.NativeContext(1, L_MAX, True, 0, self.cfg.device, sf)
+            try:
+                _, _, st = ctx.tick_host(ids, xs, ys, qids, qxa, qya, qxb, qyb)
+            finally:
+                ctx.close()
+            costs.append((sf, int(st.containment_tests) + int(st.decoded_bits)))
+        self.sweep_costs = costs
+        self._split_factor = min(costs, key=lambda c: (c[1], c[0]))[0]
+        self._ctx = self._make_ctx(self._split_factor)
 
     @property
     def split_factor(self) -> Optional[int]:
@@ -178,16 +219,25 @@ class Engine:
         return self._ctx
 
     def close(self) -> None:
-        self._ctx.close()
+        if self._ctx is not None:
+            self._ctx.close()
 
     # -- columnar fast path ----------------------------------------------------
     def process_columns(self, ids, xs, ys, qids, qxa, qya, qxb, qyb, tick_index: int = 0,
                         full_stats: bool = True) -> tuple:
         """SoA host arrays in; (ColumnarResult, TickStats) out."""
         t0 = time.perf_counter()
+        if self._ctx is None:  # method "ug" without a split factor: sweep on this (first) tick
+            if len(ids) == 0:
+                return ColumnarResult(np.asarray(qids, np.int64), np.zeros(len(qids) + 1, np.int64),
+                                      np.zeros(0, np.int64)), TickStats(tick=tick_index, method=self.cfg.name,
+                                                                         n_queries=len(qids))
+            self._sweep(ids, xs, ys, qids, qxa, qya, qxb, qyb)
         offs, res, st = self._ctx.tick_host(ids, xs, ys, qids, qxa, qya, qxb, qyb)
         t1 = time.perf_counter()
         stats = TickStats(tick=tick_index, method=self.cfg.name, n_objects=len(ids), n_queries=len(qids))
+        if self.cfg.method == "ug":
+            stats.split_factor = self._split_factor
         if len(ids):
             _fill_stats(stats, st)
             if full_stats and stats.containment_tests:

@@ -63,7 +63,10 @@ def test_method_config_validation():
     from paper_1411_3212_b200.errors import BadConfig
 
     MethodConfig().validate()
-    for bad in (dict(method="rtree"), dict(method="ug"), dict(th_quad=0), dict(l_max=13), dict(schedule="lifo"),
+    MethodConfig(method="ug").validate()  # split factor swept on the first tick
+    MethodConfig(method="ug", split_factor=37, th_quad=0).validate()  # th_quad is a quad-only field
+    for bad in (dict(method="rtree"), dict(method="ug_baseline"), dict(method="ug", split_factor=0),
+                dict(method="ug", split_factor=5000), dict(th_quad=0), dict(l_max=13), dict(schedule="lifo"),
                 dict(rebuild="never"), dict(n_workers=0)):
         with pytest.raises(BadConfig):
             MethodConfig(**bad).validate()
