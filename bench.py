@@ -284,8 +284,12 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     pool = max(1, min(args.pool, args.steps + args.warmup))
     ticks = gen_ticks(args.workload, pool)  # the same ticks on every rank
-    eng = Engine(MethodConfig(method="quad", device=local))
+    sf = args.split_factor if args.method == "ug" else 0
+    eng = Engine(MethodConfig(method=args.method, split_factor=sf or None, device=local))
     ctx = eng.native
+
+    def new_ctx():
+        return _native.NativeContext(384, 12, True, 0, local, sf)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
     if sharded:
         ctx.set_shard(rank, world)
@@ -348,7 +352,7 @@ def run_ours(args):
     # tick the object sort overlaps the query scatter on a side stream, so K1 alone is timed on a
     # second context with the sort kept on the main stream (TJ_SERIAL_SORT=1), a few ticks
     os.environ["TJ_SERIAL_SORT"] = "1"
-    sctx = _native.NativeContext(384, 12, True, 0, local)
+    sctx = new_ctx()
     os.environ.pop("TJ_SERIAL_SORT")
     sst = []
     for k in range(4):
@@ -418,7 +422,7 @@ def run_ours(args):
             # download overlap (PCIe is full duplex).  ctypes releases the GIL during tj_tick.
             import threading
 
-            ctxs = [ctx] + [_native.NativeContext(384, 12, True, 0, local) for _ in range(args.e2e_contexts - 1)]
+            ctxs = [ctx] + [new_ctx() for _ in range(args.e2e_contexts - 1)]
 
             def host_tick(cx, k):
                 a = hticks[k % pool]
@@ -484,7 +488,8 @@ def run_ours(args):
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
             "config": {"workload": args.workload, "description": DESCR[args.workload],
                        "n_objects": n, "queries_per_tick": int(st0.n_queries),
-                       "results_per_tick": int(st0.results_total), "th_quad": 384, "l_max": 12,
+                       "results_per_tick": int(st0.results_total),
+                       **({"method": "ug", "split_factor": sf} if sf else {"th_quad": 384, "l_max": 12}),
                        "rebuild": "every_tick", "distinct_ticks_cycled": pool,
                        "l2": "inputs (>=560 MB/tick at 10M) exceed the 126 MB L2; no flush",
                        "parallelism": (f"leaf-range sharding over {world} GPUs: NCCL all-gather of each tick's "
@@ -527,6 +532,9 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
+    ap.add_argument("--method", choices=("quad", "ug"), default="quad",
+                    help="index: the quadtree (headline) or the uniform grid (--split-factor cells per side)")
+    ap.add_argument("--split-factor", type=int, default=1024)
     ap.add_argument("--pool", type=int, default=3, help="distinct ticks generated and cycled")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
     ap.add_argument("--ref-sample", type=int, default=500_000)

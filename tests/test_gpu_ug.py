@@ -108,6 +108,9 @@ def test_ug_random_ticks_vs_oracle(pkg, sf):
         for k in ("containment_tests", "subq_intersecting", "subq_covering", "covering_results", "active_cells",
                   "results_total", "decoded_bits"):
             assert getattr(st, k) == ref.counters[k], (sf, cov, k)
+        if sf > 1000:  # (the host-side introspection walks every one of the 16.7M cells)
+            eng.close()
+            continue
         # intermediates: object cells, subquery list (reference order), directory
         assert np.array_equal(eng.native.object_cells(n), ref.obj_cell)
         q, cell, cv = eng.native.subqueries()
