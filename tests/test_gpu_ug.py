@@ -97,7 +97,7 @@ def _rand(rng, n, m, lo=0.0, hi=1000.0, side=(1.0, 120.0)):
 def test_ug_random_ticks_vs_oracle(pkg, sf):
     rng = np.random.default_rng(sf)
     n, m = (40_000, 3000) if sf <= 257 else (6000, 1500)  # the oracle loops over task cells in Python
-    xs, ys, a, b, c, d = _rand(rng, n, m)
+    xs, ys, a, b, c, d = _rand(rng, n, m, side=(1.0, 120.0 if sf <= 257 else 12.0))
     ids = np.arange(n, dtype=np.int64)
     qids = np.arange(m, dtype=np.int64)
     for cov in (True, False):
