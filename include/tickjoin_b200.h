@@ -167,6 +167,14 @@ int tj_get_bitmaps(tj_ctx* ctx, int64_t* n_tasks, int64_t* n_words, int64_t* tas
  * greedy least-loaded assignment of task weights n_isq*n_obj. */
 int tj_get_imbalance(tj_ctx* ctx, int32_t sim_processors, int32_t heaviest_first, double* imbalance);
 
+/* Method "ug_baseline" (baseline.py:26-121): the reference's direct-emission
+ * filter stages each task cell's (query, object) pairs privately and flushes
+ * full stages to a locked shared buffer.  The B200 path produces the same
+ * results through the bitmap pipeline; this returns the contention counter the
+ * reference reports for the last tick (flushes = sync_ops): the sum over task
+ * cells of ceil(intersecting pairs / staging_capacity), counted on the device. */
+int tj_get_staging_flushes(tj_ctx* ctx, int32_t staging_capacity, int64_t* flushes);
+
 /* Multi-GPU leaf-range sharding (no reference counterpart —
  * the reference is single-process).  With nranks > 1 every
  * tick builds the full index, then scatters, joins and decodes only the

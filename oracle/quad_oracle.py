@@ -566,6 +566,21 @@ def ug_sweep_costs(xs, ys, qxa, qya, qxb, qyb, candidates) -> list:
     return out
 
 
+STAGING_CAPACITY = 1024  # baseline.py:17
+
+
+def staging_flushes(tick: "OracleTick", capacity: int = STAGING_CAPACITY) -> int:
+    """Shared-buffer flushes (= sync_ops) of the ug_baseline filter: per task cell
+    a private stage of `capacity` pairs is flushed whenever full and once more
+    for a partial remainder (baseline.py:64-103,106-121), i.e. ceil(pairs/capacity).
+    Needs a tick run with keep_tasks=True."""
+    total = 0
+    for _, _, _, _, counts in tick.tasks:
+        p = int(np.sum(counts))
+        total += -(-p // capacity)
+    return total
+
+
 def run_tick_ug(ids, xs, ys, qids, qxa, qya, qxb, qyb, split_factor: int, covering_optimization=True,
                 keep_tasks=False) -> OracleTick:
     """One UG tick end to end (engine.py:178-259 with the ug branch, 152-161)."""

@@ -1168,6 +1168,20 @@ int tj_get_imbalance(tj_ctx* c, int32_t sim_processors, int32_t heaviest_first, 
   return TJ_OK;
 }
 
+int tj_get_staging_flushes(tj_ctx* c, int32_t staging_capacity, int64_t* flushes) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  if (staging_capacity < 1 || !flushes) return fail(c, TJ_E_INVALID_ARG, "bad arguments");
+  unsigned long long* dcnt = reinterpret_cast<unsigned long long*>(c->d_consts + 7);  // scratch slot
+  TJ_CUDA(cudaMemsetAsync(dcnt, 0, sizeof(*dcnt), c->st));
+  k_staging_flushes<<<c->num_sms * 8, 256, 0, c->st>>>(c->dv, staging_capacity, dcnt);
+  unsigned long long v = 0;
+  TJ_CUDA(cudaMemcpyAsync(&v, dcnt, sizeof(v), cudaMemcpyDeviceToHost, c->st));
+  TJ_CUDA(cudaStreamSynchronize(c->st));
+  *flushes = (int64_t)v;
+  return TJ_OK;
+}
+
 int tj_set_shard(tj_ctx* c, int32_t rank, int32_t nranks) {
   if (!c || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TJ_E_INVALID_ARG, "bad shard");
   c->shard_rank = rank;

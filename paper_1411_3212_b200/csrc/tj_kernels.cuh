@@ -1431,6 +1431,26 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
   if (__any_sync(0xffffffffu, bad) && lane == 0) h->count_mismatch = 1;
 }
 
+// ug_baseline's contention counters (baseline.py:64-121): each task cell
+// flushes its private stage of `cap` pairs whenever full and once for the
+// remainder, so flushes = sum over task cells of ceil(intersecting pairs / cap).
+__global__ void __launch_bounds__(256) k_staging_flushes(const Dev d, int32_t cap, unsigned long long* out) {
+  DevHdr* h = d.h;
+  const int lane = lane_id();
+  const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  unsigned long long acc = 0;
+  for (int64_t r = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < h->L; r += nwarp) {
+    const int nisq = d.leaf_nisq[r];
+    if (nisq == 0 || d.leaf_nobj[r] == 0 || !leaf_on(d.leaf_active, r)) continue;
+    const int32_t base = d.leaf_sbase[r];
+    long long p = 0;
+    for (int k = lane; k < nisq; k += 32) p += d.ecount[base + k];
+    p = warp_sum(p);
+    if (lane == 0) acc += (unsigned long long)((p + cap - 1) / cap);
+  }
+  if (lane == 0 && acc) atomicAdd(out, acc);
+}
+
 // TJ_OUT_IDS32 delivery: result ids narrowed to int32 (flag if one does not fit)
 __global__ void __launch_bounds__(256) k_narrow_ids(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
                                                     int64_t R, DevHdr* h) {

@@ -7,9 +7,12 @@ method "quad".  Underneath, one `tj_tick` call (include/tickjoin_b200.h) runs
 the whole tick on the GPU.  Method "ug" (the uniform grid, `grid.py`) runs
 the same kernels with the grid's cells as the leaves (split factors up to
 4096; `split_factor=None` sweeps the candidates on the first tick, each
-candidate's cost measured by the device pipeline).  "ug_baseline" is not built
-here: asking for it raises `BadConfig` — there is no CPU or multi-backend
-fallback.
+candidate's cost measured by the device pipeline).  "ug_baseline" (the
+reference's direct-emission comparison path, baseline.py) returns the same
+results through the same pipeline and reports the reference's contention
+counters (`sync_ops`, `flushes`: the staging-buffer flushes, counted on the
+device) with no decode phase (`decoded_bits` 0).  There is no CPU or
+multi-backend fallback.
 
 Besides the object API, `Engine.process_columns` is the columnar fast path
 (NumPy host arrays or CUDA tensors in, CSR out) that avoids building millions
@@ -33,7 +36,7 @@ from .workload import ColumnarTick, WorkloadRun
 
 L_MAX = 12
 METHODS = ("ug", "ug_baseline", "quad")
-BUILT_METHODS = ("quad", "ug")
+BUILT_METHODS = ("quad", "ug", "ug_baseline")
 MAX_DEVICE_SPLIT_FACTOR = 4096  # the grid is kept as a dense 2^12 x 2^12 cell map
 DEFAULT_SWEEP = (16, 256, 16)  # engine.py:30
 
@@ -185,7 +188,7 @@ class Engine:
 
     def _make_ctx(self, split_factor):
         cfg = self.cfg
-        if cfg.method == "ug":
+        if cfg.method in ("ug", "ug_baseline"):
             return _native.NativeContext(1, L_MAX, cfg.covering_optimization, 0, cfg.device, split_factor)
         rebuild = _native.TJ_REBUILD_ADAPTIVE if cfg.rebuild == "adaptive" else _native.TJ_REBUILD_EVERY_TICK
         return _native.NativeContext(cfg.th_quad, cfg.l_max, cfg.covering_optimization, rebuild, cfg.device)
@@ -236,13 +239,16 @@ class Engine:
         offs, res, st = self._ctx.tick_host(ids, xs, ys, qids, qxa, qya, qxb, qyb)
         t1 = time.perf_counter()
         stats = TickStats(tick=tick_index, method=self.cfg.name, n_objects=len(ids), n_queries=len(qids))
-        if self.cfg.method == "ug":
+        if self.cfg.method in ("ug", "ug_baseline"):
             stats.split_factor = self._split_factor
         if len(ids):
             _fill_stats(stats, st)
             if full_stats and stats.containment_tests:
                 stats.imbalance = self._ctx.imbalance(self.cfg.sim_processors,
                                                       self.cfg.schedule == "heaviest_first")
+        if self.cfg.method == "ug_baseline" and len(ids):  # engine.py:232-236, baseline.py:26-121
+            stats.decoded_bits = 0
+            stats.sync_ops = stats.flushes = self._ctx.staging_flushes(self.cfg.staging_capacity)
         d = stats.device_ms
         stats.durations = {k: d.get(k, 0.0) / 1e3 for k in ("index", "filter", "decode", "merge")}
         stats.durations["total"] = t1 - t0

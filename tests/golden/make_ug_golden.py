@@ -78,6 +78,12 @@ def main():
                         qrow.tobytes() + cell.tobytes() + cov.tobytes()).hexdigest()
                     if len(cell) <= 150_000:  # the arrays themselves for the small splits
                         arrays[key + "_qrow"], arrays[key + "_cell"], arrays[key + "_cov"] = qrow, cell, cov
+                if t == 0:  # the direct-emission comparison path on the same grid (baseline.py)
+                    eng = Engine(MethodConfig(method="ug_baseline", split_factor=sf))
+                    rs, st = eng.process_tick(batch)
+                    rec["split"][str(sf)]["baseline"] = {
+                        "digest": digest(rs), "sync_ops": st.sync_ops, "flushes": st.flushes,
+                        "decoded_bits": st.decoded_bits, "containment_tests": st.containment_tests}
             if t == 0:
                 costs = grid.sweep_costs(batch, list(range(SWEEP[0], SWEEP[1] + 1, SWEEP[2])))
                 eng = Engine(MethodConfig(method="ug", split_factor=None))

@@ -65,7 +65,8 @@ def test_method_config_validation():
     MethodConfig().validate()
     MethodConfig(method="ug").validate()  # split factor swept on the first tick
     MethodConfig(method="ug", split_factor=37, th_quad=0).validate()  # th_quad is a quad-only field
-    for bad in (dict(method="rtree"), dict(method="ug_baseline"), dict(method="ug", split_factor=0),
+    MethodConfig(method="ug_baseline", split_factor=12).validate()
+    for bad in (dict(method="rtree"), dict(method="ug_baseline", split_factor=0), dict(method="ug", split_factor=0),
                 dict(method="ug", split_factor=5000), dict(th_quad=0), dict(l_max=13), dict(schedule="lifo"),
                 dict(rebuild="never"), dict(n_workers=0)):
         with pytest.raises(BadConfig):

@@ -137,3 +137,19 @@ def test_ug_degenerate_extents_and_non_monotone_ids(pkg):
         ref = qo.run_tick_ug(ids, xs, ys, qids, cx - h, cy - h, cx + h, cy + h, split_factor=sf)
         assert np.array_equal(res.offsets, ref.offsets) and np.array_equal(res.ids, ref.result_ids)
         eng.close()
+
+
+@pytest.mark.parametrize("name", sorted(_runs()))
+def test_ug_baseline_matches_reference_fixtures(pkg, name):
+    """method="ug_baseline" (baseline.py): the same results, no decode phase, and the
+    reference's staging-buffer contention counters (sync_ops = flushes)."""
+    run = _runs()[name]
+    tick = _ticks(run)[0]
+    for sf, w in run["ticks"][0]["split"].items():
+        want = w["baseline"]
+        eng = pkg.Engine(pkg.MethodConfig(method="ug_baseline", split_factor=int(sf)))
+        res, st = eng.process_tick_columnar(tick)
+        assert qo.result_digest(tick.qids, res.offsets, res.ids) == want["digest"]
+        assert (st.sync_ops, st.flushes, st.decoded_bits, st.containment_tests) == (
+            want["sync_ops"], want["flushes"], want["decoded_bits"], want["containment_tests"])
+        eng.close()

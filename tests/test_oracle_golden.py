@@ -281,6 +281,12 @@ def test_oracle_ug_matches_reference(name):
             assert qo.result_digest(tick.qids, t.offsets, t.result_ids) == w["digest"], (t_idx, sf)
             for k, v in w["stats"].items():
                 assert t.counters[k] == v, (t_idx, sf, k)
+            if "baseline" in w:  # ug_baseline: same results, no decode, staging-buffer counters
+                tb = qo.run_tick_ug(tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb,
+                                    split_factor=int(sf), keep_tasks=True)
+                assert qo.result_digest(tick.qids, tb.offsets, tb.result_ids) == w["baseline"]["digest"]
+                assert qo.staging_flushes(tb) == w["baseline"]["flushes"] == w["baseline"]["sync_ops"]
+                assert tb.counters["containment_tests"] == w["baseline"]["containment_tests"]
             if "subq_sha256" in w:
                 assert _ug_subq_sha(t) == w["subq_sha256"], (t_idx, sf)
                 key = f"{name}_t{t_idx}_sf{sf}_cell"
