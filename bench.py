@@ -483,7 +483,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "p50_tick_ms": statistics.median(per_tick), "higher_is_better": True,
+            "p50_tick_ms": statistics.median(per_tick), "max_tick_ms": max(per_tick), "higher_is_better": True,
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
             "config": {"workload": args.workload, "description": DESCR[args.workload],

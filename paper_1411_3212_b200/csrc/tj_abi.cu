@@ -46,6 +46,7 @@ struct tj_ctx {
   int device = 0;
   int num_sms = 148;
   int scatter_per_sm = 8;
+  bool fused_pyr = true;  // TJ_FUSED_PYR=0: one launch per pyramid level
   int ug_sf = 0;  // method "ug": cells per side (cfg.l_max then holds ceil(log2) of it)
   int join_blocks = 4;  // resident k_join CTAs per SM (occupancy API)
   cudaStream_t st = nullptr;
@@ -362,7 +363,14 @@ int launch_stage(tj_ctx* c, int stage) {
         k_finalize_index<<<1, 1, 0, st>>>(h);
         cudaMemsetAsync(d.clev, lmax, int64_t(1) << (2 * lmax), st);
       } else {
-        for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
+        if (c->fused_pyr) {  // levels F-1 .. 0 in spans of kPyrSpan (k_pyr_fused)
+          for (int hi = F; hi > 0; hi -= kPyrSpan) {
+            const int lo = std::max(0, hi - kPyrSpan);
+            k_pyr_fused<<<(int)(int64_t(1) << (2 * lo)), 256, 0, st>>>(d, lo, hi);
+          }
+        } else {
+          for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
+        }
         k_finalize_index<<<1, 1, 0, st>>>(h);
         k_cell_level<<<Gbig, 256, 0, st>>>(d);
       }
@@ -375,7 +383,7 @@ int launch_stage(tj_ctx* c, int stage) {
         k_shard_mark<<<Gbig, 256, 0, st>>>(d);
       }
       // 3 launches per scan
-      return (c->ug_sf ? 11 : 12 + F) + (c->shard_n > 1 ? 4 : 0);
+      return (c->ug_sf ? 11 : 12 + (c->fused_pyr ? (F + kPyrSpan - 1) / kPyrSpan : F)) + (c->shard_n > 1 ? 4 : 0);
     case kSortStage: {  // ---- K1's last part: objects into leaf order (side stream) ----
       cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
@@ -623,6 +631,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
   if (const char* ss = std::getenv("TJ_SERIAL_SORT")) c->serial_sort = std::atoi(ss) != 0;
   if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
+  if (const char* fp = std::getenv("TJ_FUSED_PYR")) c->fused_pyr = std::atoi(fp) != 0;
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   // side-stream priority (TJ_SIDE_PRIO=1: the object sort's blocks go first) measured no gain:

@@ -244,6 +244,59 @@ __global__ void __launch_bounds__(256) k_pyr_level(const Dev d, int l) {
   }
 }
 
+// Levels hi-1 .. lo of the dense pyramid in one launch: CTA b owns node b of
+// level lo and sums its subtree upward from level hi (4^(hi-lo) <= 4096
+// children staged through shared memory), writing every level it computes and
+// noting splits like k_pyr_level (12 launches become 2 at l_max 12).
+constexpr int kPyrSpan = 6;  // levels per fused launch
+__global__ void __launch_bounds__(256) k_pyr_fused(const Dev d, int lo, int hi) {
+  DevHdr* h = d.h;
+  __shared__ uint32_t buf[2][1024];
+  const uint32_t th = (uint32_t)h->th;
+  const int64_t node = blockIdx.x;  // at level lo
+  // level hi-1 from the global level hi
+  {
+    const int l = hi - 1;
+    const int64_t per = int64_t(1) << (2 * (l - lo));  // level-l nodes under this CTA's node
+    const uint32_t* child = d.pyr + pyr_off(hi);
+    uint32_t* self = d.pyr + pyr_off(l);
+    const bool can_split = l >= 1 && l < h->l_max;
+    for (int64_t k0 = 0; k0 < per; k0 += blockDim.x) {
+      const int64_t k = k0 + threadIdx.x;
+      bool split = false;
+      if (k < per) {
+        const int64_t z = node * per + k;
+        const uint4 c = *reinterpret_cast<const uint4*>(child + 4 * z);
+        const uint32_t sum = c.x + c.y + c.z + c.w;
+        self[z] = sum;
+        buf[(hi - 1 - lo) & 1][k] = sum;
+        split = can_split && sum > th;
+      }
+      note_split(h, split, l + 1);
+    }
+  }
+  __syncthreads();
+  for (int l = hi - 2; l >= lo; --l) {
+    const int64_t per = int64_t(1) << (2 * (l - lo));
+    const uint32_t* src = buf[(l + 1 - lo) & 1];
+    uint32_t* dst = buf[(l - lo) & 1];
+    uint32_t* self = d.pyr + pyr_off(l);
+    const bool can_split = l >= 1 && l < h->l_max;
+    for (int64_t k0 = 0; k0 < per; k0 += blockDim.x) {
+      const int64_t k = k0 + threadIdx.x;
+      bool split = false;
+      if (k < per) {
+        const uint32_t sum = src[4 * k] + src[4 * k + 1] + src[4 * k + 2] + src[4 * k + 3];
+        self[node * per + k] = sum;
+        dst[k] = sum;
+        split = can_split && sum > th;
+      }
+      note_split(h, split, l + 1);
+    }
+    __syncthreads();
+  }
+}
+
 __global__ void k_finalize_index(DevHdr* h) {
   if (h->abort) return;
   h->Z = int64_t(1) << (2 * h->l_deep);
