@@ -147,3 +147,26 @@ def test_two_sharded_contexts_reproduce_the_tick():
         assert np.array_equal(offs, f_offs) and np.array_equal(ids, f_ids), n
         assert sum(len(p[1]) for p in parts) == len(f_ids)
     full.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("sf", [7, 256])
+def test_two_sharded_ug_contexts_reproduce_the_tick(sf):
+    """Leaf-range sharding is index-agnostic: the uniform grid's cells shard the same way."""
+    from paper_1411_3212_b200 import _native
+
+    tick = _small_tick(seed=10)
+    args = (tick["ids"], tick["xs"], tick["ys"], tick["qids"], *tick["rects"])
+    full = _native.NativeContext(1, 12, True, 0, 0, sf)
+    f_offs, f_ids, _ = full.tick_host(*args)
+    for n in (2, 3):
+        parts = []
+        for r in range(n):
+            ctx = _native.NativeContext(1, 12, True, 0, 0, sf)
+            ctx.set_shard(r, n)
+            o, i, _ = ctx.tick_host(*args)
+            parts.append((o, i))
+            ctx.close()
+        offs, ids = merge_partials(parts)
+        assert np.array_equal(offs, f_offs) and np.array_equal(ids, f_ids), n
+    full.close()
