@@ -393,7 +393,7 @@ def run_ours(args):
                 a = sh.full
                 return ctx.tick_ptrs(sh.n, *(x.data_ptr() for x in a[:3]), sh.m, *(x.data_ptr() for x in a[3:]),
                                      _native.TJ_MEM_DEVICE, _native.TJ_MEM_HOST | out_flag), \
-                    h2d_bytes(sh.mine)
+                    sum(x.numel() * x.element_size() for x in sh.mine)  # all 8 columns are copied and gathered
         else:
             hticks = [[torch.from_numpy(a).pin_memory() for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb,
                                                                     t.qyb)] for t in ticks]
