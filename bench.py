@@ -415,7 +415,7 @@ def run_ours(args):
             for k in range(e_steps):
                 (out, st), hb = tick_host(k)
                 h2d += hb
-                d2h += 8 * (out.n_q + 1) + out.id_bytes * out.n_results
+                d2h += out.offset_bytes * (out.n_q + 1) + out.id_bytes * out.n_results
                 idb = out.id_bytes
                 eq += int(st.n_queries)
             e1.record(stream)
@@ -445,7 +445,7 @@ def run_ours(args):
                 for k in range(j, e_steps, len(ctxs)):
                     out, st, hb = host_tick(ctxs[j], k)
                     acc[j][0] += hb
-                    acc[j][1] += 8 * (out.n_q + 1) + out.id_bytes * out.n_results
+                    acc[j][1] += out.offset_bytes * (out.n_q + 1) + out.id_bytes * out.n_results
                     idbs.add(out.id_bytes)
                     acc[j][2] += int(st.n_queries)
 
@@ -472,7 +472,7 @@ def run_ours(args):
                "contexts": 1 if sharded else args.e2e_contexts,
                "id_bytes": idb,
                "api": ("tj_tick (C ABI): pinned host inputs -> device, results CSR -> pinned host"
-                       + (" (ids as int32: TJ_OUT_IDS32, every id < 2^31)" if idb == 4 else " (int64 ids)")
+                       + (" (TJ_OUT_IDS32: int32 ids and offsets, every id and offset < 2^31)" if idb == 4 else " (int64 ids)")
                        + ("; per rank: H2D of its 1/G slice, NCCL all-gather, D2H of its leaf-range CSR"
                           if sharded else ""))}
 

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define TJ_ABI_VERSION 2
+#define TJ_ABI_VERSION 3
 
 /* status codes — errors.py:4-45 */
 #define TJ_OK 0
@@ -40,10 +40,12 @@ extern "C" {
 /* memory spaces of caller buffers */
 #define TJ_MEM_HOST 0   /* pageable or pinned host memory                  */
 #define TJ_MEM_DEVICE 1 /* device memory on the context's CUDA device      */
-/* tj_tick_in.out_mem flag: deliver result ids as int32 (tj_tick_out.ids32,
- * id_bytes = 4) when every result id of the tick fits in int32; otherwise
- * the tick falls back to int64 ids (id_bytes = 8).  Halves the result bytes
- * a host caller downloads per tick; the values are the same. */
+/* tj_tick_in.out_mem flag: compact 32-bit delivery.  Result ids come as int32
+ * (tj_tick_out.ids32, id_bytes = 4) when every result id of the tick fits in
+ * int32, else as int64 (id_bytes = 8); CSR offsets come as int32
+ * (offsets32, offset_bytes = 4) when the tick has fewer than 2^31 results,
+ * else as int64.  Halves the bytes a host caller downloads per tick; the
+ * values are the same. */
 #define TJ_OUT_IDS32 0x100
 
 /* rebuild policies — MethodConfig.rebuild, engine.py:70,163-170 */
@@ -89,11 +91,14 @@ typedef struct tj_tick_in {
 typedef struct tj_tick_out {
   int64_t n_q;
   int64_t n_results;
-  const int64_t* offsets; /* n_q + 1 */
+  const int64_t* offsets; /* n_q + 1 (offset_bytes == 8; else NULL) */
   const int64_t* ids;     /* n_results (id_bytes == 8; else NULL) */
   int32_t mem;
   int32_t id_bytes;       /* 8: ids holds the results; 4: ids32 does  */
   const int32_t* ids32;   /* n_results (id_bytes == 4; else NULL) */
+  const int32_t* offsets32; /* n_q + 1 (offset_bytes == 4; else NULL) */
+  int32_t offset_bytes;   /* 8: offsets holds the CSR offsets; 4: offsets32 does */
+  int32_t reserved;
 } tj_tick_out;
 
 /* TickStats counters (engine.py:99-121) plus device stage times. */

@@ -53,7 +53,8 @@ class TjTickIn(ctypes.Structure):
 
 class TjTickOut(ctypes.Structure):
     _fields_ = [("n_q", c_int64), ("n_results", c_int64), ("offsets", c_void_p), ("ids", c_void_p),
-                ("mem", c_int32), ("id_bytes", c_int32), ("ids32", c_void_p)]
+                ("mem", c_int32), ("id_bytes", c_int32), ("ids32", c_void_p), ("offsets32", c_void_p),
+                ("offset_bytes", c_int32), ("reserved", c_int32)]
 
 
 class TjStats(ctypes.Structure):
@@ -160,8 +161,9 @@ class NativeContext:
 
     # -- hot path ---------------------------------------------------------
     def tick_host(self, ids, xs, ys, qids, qxa, qya, qxb, qyb, ids32: bool = False):
-        """Host arrays in, host CSR out (copied into fresh NumPy arrays).  ids32: ask for int32
-        result ids (TJ_OUT_IDS32); the returned array is int32 only if every id fit."""
+        """Host arrays in, host CSR out (copied into fresh NumPy arrays).  ids32: ask for the
+        compact 32-bit delivery (TJ_OUT_IDS32): ids come back int32 only if every id fit,
+        offsets int32 only if the tick has fewer than 2^31 results."""
         arrs = [np.ascontiguousarray(ids, np.int64), np.ascontiguousarray(xs, np.float64),
                 np.ascontiguousarray(ys, np.float64), np.ascontiguousarray(qids, np.int64),
                 np.ascontiguousarray(qxa, np.float64), np.ascontiguousarray(qya, np.float64),
@@ -173,7 +175,8 @@ class NativeContext:
         st = TjStats()
         self._check(self.lib.tj_tick(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
         m = tout.n_q
-        offs = np.ctypeslib.as_array(ctypes.cast(tout.offsets, POINTER(c_int64)), shape=(m + 1,)).copy()
+        osrc, otyp = (tout.offsets32, c_int32) if tout.offset_bytes == 4 else (tout.offsets, c_int64)
+        offs = np.ctypeslib.as_array(ctypes.cast(osrc, POINTER(otyp)), shape=(m + 1,)).copy()
         res = np.zeros(0, np.int32 if tout.id_bytes == 4 else np.int64)
         if tout.n_results:
             src, typ = (tout.ids32, c_int32) if tout.id_bytes == 4 else (tout.ids, c_int64)

@@ -68,7 +68,7 @@ struct tj_ctx {
   // subqueries
   DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf;
   // join / outputs
-  DBuf bitmap, outids, outoff, scratch;
+  DBuf bitmap, outids, outoff, scratch, outoff32;
   // scan / radix scratch
   DBuf partial, partial2, rhist, roffs, sstate, sstate2;
   int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
@@ -672,7 +672,7 @@ int tj_destroy(tj_ctx* c) {
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->qpos, &c->qwin, &c->crect, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
-                 &c->outids, &c->outoff, &c->scratch, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
+                 &c->outids, &c->outoff, &c->scratch, &c->outoff32, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)
     if (b->p) cudaFree(b->p);
   if (c->h_off) cudaFreeHost(c->h_off);
@@ -878,22 +878,35 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     }
   }
   const int64_t idb = use32 ? 4 : 8;
+  const bool off32 = want32 && R < (int64_t(1) << 31);
+  const int64_t ob = off32 ? 4 : 8;
+  if (off32) {
+    if ((rc = ensure(c, c->outoff32, (size_t)(m + 1) * 4))) return rc;
+    k_narrow_offsets<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(c->outoff), P<int32_t>(c->outoff32), m + 1);
+    ++S.kernel_launches;
+  }
   out->id_bytes = (int32_t)idb;
+  out->offset_bytes = (int32_t)ob;
   out->ids = nullptr;
   out->ids32 = nullptr;
+  out->offsets = nullptr;
+  out->offsets32 = nullptr;
   if (out_space == TJ_MEM_DEVICE) {
-    out->offsets = P<int64_t>(c->outoff);
+    if (off32) out->offsets32 = P<int32_t>(c->outoff32);
+    else out->offsets = P<int64_t>(c->outoff);
     if (use32) out->ids32 = R ? P<int32_t>(c->scratch) : nullptr;
     else out->ids = n ? P<int64_t>(c->outids) : nullptr;
     out->mem = TJ_MEM_DEVICE;
   } else {
-    if ((rc = ensure_host(c, c->h_off, c->h_off_bytes, (m + 1) * 8))) return rc;
+    if ((rc = ensure_host(c, c->h_off, c->h_off_bytes, (m + 1) * ob))) return rc;
     if ((rc = ensure_host(c, c->h_ids, c->h_ids_bytes, R * idb))) return rc;
-    TJ_CUDA(cudaMemcpyAsync(c->h_off, c->outoff.p, (m + 1) * 8, cudaMemcpyDeviceToHost, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->h_off, off32 ? c->outoff32.p : c->outoff.p, (m + 1) * ob, cudaMemcpyDeviceToHost,
+                            c->st));
     if (R) TJ_CUDA(cudaMemcpyAsync(c->h_ids, use32 ? c->scratch.p : c->outids.p, R * idb, cudaMemcpyDeviceToHost,
                                    c->st));
     TJ_CUDA(cudaStreamSynchronize(c->st));
-    out->offsets = (const int64_t*)c->h_off;
+    if (off32) out->offsets32 = (const int32_t*)c->h_off;
+    else out->offsets = (const int64_t*)c->h_off;
     if (use32) out->ids32 = (const int32_t*)c->h_ids;
     else out->ids = (const int64_t*)c->h_ids;
     out->mem = TJ_MEM_HOST;

@@ -1522,6 +1522,12 @@ __global__ void __launch_bounds__(256) k_narrow_ids(const int64_t* __restrict__ 
   if (__any_sync(0xffffffffu, wide) && lane_id() == 0) h->ids_wide = 1;
 }
 
+// TJ_OUT_IDS32 delivery of the CSR offsets (the caller checked R < 2^31)
+__global__ void __launch_bounds__(256) k_narrow_offsets(const int64_t* __restrict__ src, int32_t* __restrict__ dst,
+                                                        int64_t cnt) {
+  TJ_GRID_STRIDE(i, cnt) __stcs(dst + i, (int32_t)__ldcs(reinterpret_cast<const long long*>(src) + i));
+}
+
 // ---------------------------------------------------------------------------
 // CTA-wide sort of one segment (used only when object ids are not increasing
 // in input order: then lists must be sorted by id, decode.py:117).

@@ -253,7 +253,7 @@ def test_decode_merge_paths_all_list_shapes(pkg, th):
 
 
 def test_int32_id_delivery(pkg):
-    """TJ_OUT_IDS32: the same CSR with int32 ids; ids beyond int32 fall back to int64."""
+    """TJ_OUT_IDS32: the same CSR with int32 ids and offsets; ids beyond int32 fall back to int64."""
     from paper_1411_3212_b200 import _native
 
     rng = np.random.default_rng(23)
@@ -265,8 +265,8 @@ def test_int32_id_delivery(pkg):
                 np.arange(n, dtype=np.int64) * 50_000):  # the last: ids up to 2.5e9 > 2^31
         o64, r64, _ = ctx.tick_host(ids, xs, ys, qids, a, b, c, d)
         o32, r32, _ = ctx.tick_host(ids, xs, ys, qids, a, b, c, d, ids32=True)
-        assert np.array_equal(o64, o32) and np.array_equal(r64, r32.astype(np.int64))
-        assert r32.dtype == (np.int64 if ids.max() >= 2**31 else np.int32)
+        assert np.array_equal(o64, o32.astype(np.int64)) and np.array_equal(r64, r32.astype(np.int64))
+        assert r32.dtype == (np.int64 if ids.max() >= 2**31 else np.int32) and o32.dtype == np.int32
     ctx.close()
 
 
