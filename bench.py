@@ -24,6 +24,7 @@ Strong scaling; rank 0 prints the max-over-ranks device time.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import statistics
@@ -318,6 +319,8 @@ def run_ours(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    gc.collect()
+    gc.disable()  # no collector pauses between ticks inside the timed region
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev[0].record(stream)
     stats = []
@@ -328,6 +331,7 @@ def run_ours(args):
         stats.append(st)
         queries += int(st.n_queries)  # every rank sees the whole tick: count once
     torch.cuda.synchronize()
+    gc.enable()
     clk = clocks.stop()
     total_ms = ev[0].elapsed_time(ev[-1])
     per_tick = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
