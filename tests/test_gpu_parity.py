@@ -469,3 +469,41 @@ def test_adaptive_rebuild_matches_reference(pkg, name):
         assert st.n_leaves == want["n_leaves"] and st.l_deep == want["l_deep"], t
         assert qo.result_digest(tick.qids, res.offsets, res.ids) == want["digest"], t
     eng.close()
+
+
+def _d2h(ptr, count, dtype):
+    """Copy `count` elements at a raw device pointer to a new NumPy array (cudaMemcpy D2H)."""
+    import ctypes
+
+    rt = ctypes.CDLL("libcudart.so.12")
+    rt.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+    out = np.empty(count, dtype)
+    assert rt.cudaMemcpy(out.ctypes.data, ptr, out.nbytes, 2) == 0  # cudaMemcpyDeviceToHost
+    return out
+
+
+def test_device_pointer_tick_and_compact_device_delivery(pkg):
+    """tj_tick with device-resident inputs and outputs (the path bench.py times), in the
+    default int64 and the TJ_OUT_IDS32 compact layouts, equals the host-buffer tick."""
+    import torch
+
+    from paper_1411_3212_b200 import _native
+
+    rng = np.random.default_rng(31)
+    n, m = 60_000, 6000
+    xs, ys, a, b, c, d = _rand_tick(rng, n, m)
+    ids = np.arange(n, dtype=np.int64)
+    qids = np.arange(m, dtype=np.int64)
+    ctx = _native.NativeContext(64, 12, True, 0, 0)
+    o_ref, r_ref, _ = ctx.tick_host(ids, xs, ys, qids, a, b, c, d)
+    dev = [torch.from_numpy(np.ascontiguousarray(x)).cuda() for x in (ids, xs, ys, qids, a, b, c, d)]
+    ptr = [t.data_ptr() for t in dev]
+    torch.cuda.synchronize()
+    for flag in (0, _native.TJ_OUT_IDS32):
+        out, st = ctx.tick_ptrs(n, *ptr[:3], m, *ptr[3:], _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE | flag)
+        assert out.mem == _native.TJ_MEM_DEVICE and out.n_results == len(r_ref)
+        assert (out.id_bytes, out.offset_bytes) == ((4, 4) if flag else (8, 8))
+        offs = _d2h(out.offsets32 if flag else out.offsets, m + 1, np.int32 if flag else np.int64)
+        res = _d2h(out.ids32 if flag else out.ids, out.n_results, np.int32 if flag else np.int64)
+        assert np.array_equal(offs.astype(np.int64), o_ref) and np.array_equal(res.astype(np.int64), r_ref)
+    ctx.close()
