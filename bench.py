@@ -311,17 +311,21 @@ def run_ours(args):
         return ctx.tick_ptrs(n, *(x.data_ptr() for x in a[:3]), m, *(x.data_ptr() for x in a[3:]),
                              _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
 
+    # the clock sampler starts before the warm-up (its start-up otherwise leaves the GPU idle,
+    # clocks ramp down, and the first timed tick pays the ramp); samples are kept from the
+    # timed region only
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    gc.collect()
     for k in range(args.warmup):
         tick_dev(k)
     torch.cuda.synchronize()
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    gc.collect()
+    clocks.lines.clear()
     gc.disable()  # no collector pauses between ticks inside the timed region
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     ev[0].record(stream)
     stats = []
     queries = 0
@@ -335,6 +339,8 @@ def run_ours(args):
     clk = clocks.stop()
     total_ms = ev[0].elapsed_time(ev[-1])
     per_tick = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
+    if os.environ.get("TJ_BENCH_TICKS"):  # diagnostics: every timed tick's duration
+        print("ticks_ms", [round(t, 3) for t in per_tick], file=sys.stderr)
     if world > 1:
         t = torch.tensor([total_ms] + per_tick, device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)

@@ -746,7 +746,10 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     c->n = n;
     c->m = m;
     if ((rc = prepare_static(c, n, m))) return rc;
-    if (c->last_L == 0) c->last_L = c->cap_L;
+    // first tick: assume < 2^16 leaves (two radix passes); a larger tree aborts and replays the
+    // tick with more passes once.  Starting from the capacity bound instead would capture the first
+    // tick's graphs with a pass count later ticks no longer use (a re-capture when its inputs recur).
+    if (c->last_L == 0) c->last_L = std::min<int64_t>(c->cap_L, int64_t(1) << 16);
     c->obj_passes = passes_for(std::max<int64_t>(c->last_L, 1) - 1);  // grows (tick replay) if L crosses a digit
     // adaptive rebuild (engine.py:163-174): check the previous index against this tick's objects
     c->reuse = false;
