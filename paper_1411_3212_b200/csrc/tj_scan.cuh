@@ -241,6 +241,9 @@ struct ExclOut {
 // ballots (stable: warp w / round k / lane order), stages the tile by digit in
 // shared memory and writes digit runs coalesced.
 // ---------------------------------------------------------------------------
+#ifndef TJ_RADIX_MINB
+#define TJ_RADIX_MINB 2  // resident downsweep CTAs per SM the register budget is cut for (2: -9% vs 3; 1 and 4 slower)
+#endif
 #ifndef TJ_RADIX_BITS
 #define TJ_RADIX_BITS 8
 #endif
@@ -292,7 +295,7 @@ k_radix_upsweep(KeySrc keys, const int64_t* n_ptr, const DevHdr* h, int shift,
 
 // vals_in == nullptr: the value of item i is i (first pass over input rows)
 template <typename KeySrc>
-__global__ void __launch_bounds__(kRadixThreads, 3)
+__global__ void __launch_bounds__(kRadixThreads, TJ_RADIX_MINB)
 k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
                   int32_t* vals_out, const int64_t* n_ptr, const DevHdr* h, int shift,
                   const int64_t* offs /* [digits][G] exclusive */) {
