@@ -156,7 +156,8 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
-def gen_ticks(name: str, count: int, seed_offset: int = 0):
+def iter_workload(name: str, count: int, seed_offset: int = 0):
+    """The workload's first `count` ticks, lazily (one tick in memory at a time)."""
     import numpy as np
 
     from paper_1411_3212_b200.workload import ColumnarTick, WorkloadConfig, iter_ticks
@@ -167,12 +168,12 @@ def gen_ticks(name: str, count: int, seed_offset: int = 0):
     for kw in parts:
         kw = dict(kw)
         kw["seed"] = kw["seed"] + seed_offset
-        streams.append(list(iter_ticks(WorkloadConfig(n_ticks=count, **kw))))
+        streams.append(iter_ticks(WorkloadConfig(n_ticks=count, **kw)))
     if len(streams) == 1:
-        return streams[0]
-    ticks = []
-    for k in range(count):
-        ts, off = [s_[k] for s_ in streams], 0
+        yield from streams[0]
+        return
+    for k, ts in enumerate(zip(*streams)):
+        off = 0
         cols = {c: [] for c in ("ids", "xs", "ys", "qids", "qxa", "qya", "qxb", "qyb")}
         for t in ts:
             cols["ids"].append(t.ids + off)
@@ -180,8 +181,11 @@ def gen_ticks(name: str, count: int, seed_offset: int = 0):
             for c in ("xs", "ys", "qxa", "qya", "qxb", "qyb"):
                 cols[c].append(getattr(t, c))
             off += t.n_objects
-        ticks.append(ColumnarTick(k, **{c: np.concatenate(v) for c, v in cols.items()}))
-    return ticks
+        yield ColumnarTick(k, **{c: np.concatenate(v) for c, v in cols.items()})
+
+
+def gen_ticks(name: str, count: int, seed_offset: int = 0):
+    return list(iter_workload(name, count, seed_offset))
 
 
 def cpu_reference_sample(n_objects: int, seed: int = 3):

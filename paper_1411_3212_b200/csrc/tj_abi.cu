@@ -72,13 +72,15 @@ struct tj_ctx {
   // scan / radix scratch
   DBuf partial, partial2, rhist, roffs, sstate, sstate2;
   int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
-  bool lb_scan = false;
-  bool serial_sort = false;
+  bool lb_scan = false;       // single-pass look-back scan (measured slower here than reduce-then-scan)
+  bool serial_sort = false;   // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)
   // adaptive rebuild: the last built index (header fields + the buffers it lives in)
   bool have_index = false;
   bool reuse = false;  // this tick reuses it
+  int32_t reuse_not_mono = 0, reuse_not_id = 0;  // id-order flags of this tick, from the reuse check pass
   DevHdr idx{};
-  const void* idx_bufs[3] = {nullptr, nullptr, nullptr};  // zmap, leaf codes, leaf counts  // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)    // single-pass look-back scan (measured slower here than reduce-then-scan)
+  // (the kept index lives in zmap, sized by l_max only, and in the leaf codes, which keep their
+  // contents when n grows the leaf capacity: see prepare_static)
   // pinned host outputs
   void* h_off = nullptr;
   size_t h_off_bytes = 0;
@@ -115,21 +117,23 @@ int fail(tj_ctx* c, int code, const std::string& msg) {
                   std::string(#call) + ": " + cudaGetErrorString(e_));                  \
   } while (0)
 
-// grow-only device buffer
-int ensure(tj_ctx* c, DBuf& b, size_t bytes) {
+// grow-only device buffer; `keep`: the old contents survive a reallocation
+int ensure(tj_ctx* c, DBuf& b, size_t bytes, bool keep = false) {
   if (bytes == 0) bytes = 16;
   if (b.bytes >= bytes) return TJ_OK;
-  if (b.p) {
-    cudaStreamSynchronize(c->st);
-    cudaFree(b.p);
-    b.p = nullptr;
-    b.bytes = 0;
-  }
-  cudaError_t e = cudaMalloc(&b.p, bytes);
+  void* np_ = nullptr;
+  cudaError_t e = cudaMalloc(&np_, bytes);
   if (e != cudaSuccess) {
     cudaGetLastError();
     return fail(c, TJ_E_OOM, std::string("cudaMalloc(") + std::to_string(bytes) + "): " + cudaGetErrorString(e));
   }
+  if (b.p) {
+    cudaStreamSynchronize(c->st);
+    if (c->side) cudaStreamSynchronize(c->side);
+    if (keep) cudaMemcpy(np_, b.p, b.bytes, cudaMemcpyDeviceToDevice);
+    cudaFree(b.p);
+  }
+  b.p = np_;
   b.bytes = bytes;
   return TJ_OK;
 }
@@ -187,7 +191,8 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(pyr, pyr_off(F + 1) * 4);
   ENS(clev, Zmax);
   ENS(zmap, Zmax * 4);
-  ENS(lcode, c->cap_L * 4);
+  // the adaptive policy's kept index: leaf codes survive growth (zmap is sized by l_max alone)
+  if ((rc = ensure(c, c->lcode, (size_t)(c->cap_L * 4), true)) != TJ_OK) return rc;
   ENS(lnobj, c->cap_L * 4);
   ENS(lobase, c->cap_L * 4);
   ENS(lnisq, c->cap_L * 4);
@@ -471,6 +476,9 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
     H.Z = I.Z;
     H.L = I.L;
     H.reuse_index = 1;
+    // the reuse branch of stage 0 skips k_mbr: the check pass measured this tick's id order
+    H.not_monotone = c->reuse_not_mono;
+    H.not_identity = c->reuse_not_id;
   }
   const char* dbg = std::getenv("TJ_DEBUG");
   H.dbg = dbg ? std::atoi(dbg) : 0;
@@ -753,8 +761,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     c->obj_passes = passes_for(std::max<int64_t>(c->last_L, 1) - 1);  // grows (tick replay) if L crosses a digit
     // adaptive rebuild (engine.py:163-174): check the previous index against this tick's objects
     c->reuse = false;
-    if (c->cfg.rebuild == TJ_REBUILD_ADAPTIVE && c->have_index && c->idx_bufs[0] == c->zmap.p &&
-        c->idx_bufs[1] == c->lcode.p && c->idx_bufs[2] == c->lnobj.p) {
+    if (c->cfg.rebuild == TJ_REBUILD_ADAPTIVE && c->have_index) {
       if ((rc = prepare_dynamic(c))) return rc;
       fill_dev(c, ids, xs, ys, qxa, qya, qxb, qyb);
       c->reuse = true;
@@ -778,6 +785,8 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       // needs_rebuild (quadtree.py:250-270): escaped objects, a leaf over 8 x th, or > 5% over 2 x th
       const bool rebuild = H.oob || H.overfull8 > 0 || (double)H.overfull2 / (double)std::max<int64_t>(H.L, 1) > 0.05;
       c->reuse = !rebuild;
+      c->reuse_not_mono = H.not_monotone;
+      c->reuse_not_id = H.not_identity;
     }
     bool done = false;
     for (int attempt = 0; attempt < 8 && !done; ++attempt) {
@@ -812,9 +821,6 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     if (!c->reuse) {  // this tick built the index: keep it for the adaptive policy
       c->idx = H;
       c->have_index = true;
-      c->idx_bufs[0] = c->zmap.p;
-      c->idx_bufs[1] = c->lcode.p;
-      c->idx_bufs[2] = c->lnobj.p;
     }
     if (H.dup) return fail(c, TJ_E_DUPLICATE_RESULT, "a (query, object) pair was produced twice");
     if (H.count_mismatch) return fail(c, TJ_E_COUNT_MISMATCH, "decoded counts disagree with popcounts");

@@ -471,6 +471,38 @@ def test_adaptive_rebuild_matches_reference(pkg, name):
     eng.close()
 
 
+@pytest.mark.parametrize("name", sorted(_adaptive_runs()))
+def test_adaptive_reuse_with_non_monotone_ids(pkg, name):
+    """Adaptive ticks that reuse the index with ids that are neither arange nor
+    increasing: the reused tick must look ids up and sort lists by
+    id.  ids' = K - id reverses the order; mapped back, every list equals the
+    reference digest, and the rebuild decisions are unchanged."""
+    run = _adaptive_runs()[name]
+    cfg = dict(run["config"])
+    th = cfg.pop("th_quad")
+    if isinstance(cfg.get("query_side"), list):
+        cfg["query_side"] = tuple(cfg["query_side"])
+    K = 10**9
+    eng = _engine(pkg, th=th, rebuild="adaptive")
+    for t, tick in enumerate(pkg.iter_ticks(pkg.WorkloadConfig(**cfg))):
+        want = run["ticks"][t]
+        res, st = eng.process_columns(K - tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb,
+                                      tick.qyb)
+        assert st.rebuilt == want["rebuilt"], t
+        lens = np.diff(res.offsets)
+        # ascending by the (reversed) id within every list
+        d = np.diff(res.ids)
+        inner = np.ones(len(res.ids), bool)
+        inner[res.offsets[1:-1] - 1] = False
+        assert np.all((d > 0) | ~inner[:-1]), t
+        # back to the original ids: each list reversed is ascending again
+        orig = (K - res.ids)
+        q = np.repeat(np.arange(len(lens)), lens)
+        order = np.lexsort((orig, q))
+        assert qo.result_digest(tick.qids, res.offsets, orig[order]) == want["digest"], t
+    eng.close()
+
+
 def _d2h(ptr, count, dtype):
     """Copy `count` elements at a raw device pointer to a new NumPy array (cudaMemcpy D2H)."""
     import ctypes
