@@ -12,7 +12,7 @@ A step = one `tj_tick` (index build -> query scatter -> per-leaf bitmap join
 -> decode -> canonical per-query lists) over one tick.
 
   python bench.py [--gpus N --steps K --warmup W]           # our arm
-  python bench.py --impl reference [...]                    # CPU reference arm (oracle port)
+  python bench.py --impl reference [...]                    # CPU reference arm (tickjoin from baseline/_ref)
 
 Under torchrun (N>1) the same 10M-object tick is split over the ranks: each
 rank holds 1/N of the updates and queries, an NCCL all-gather gives every rank
@@ -188,6 +188,107 @@ def gen_ticks(name: str, count: int, seed_offset: int = 0):
     return list(iter_workload(name, count, seed_offset))
 
 
+class RefEngineSample:
+    """The REFERENCE engine (`tickjoin`, installed unmodified in baseline/_ref) on a bounded
+    sample of the bench workload's tick, through its public API
+    `Engine(MethodConfig("quad", n_workers=...)).process_tick(TickBatch)` (engine.py:178-259).
+
+    A full C5 tick takes the reference minutes (10M objects, 10M queries), so a step is one
+    `process_tick` on ALL the tick's objects with one chunk of its queries: the queries sorted by
+    the Morton code of their centres and cut into `k` contiguous chunks of m/k (compact regions,
+    so every chunk carries its leaves' whole per-task cost, not a thin slice of it).  D0 = the
+    same call with no queries (the index build over all objects; median of the warm-up runs).
+    A chunk's tick-time estimate is D0 + k * (D_chunk - D0); the value is m over the mean estimate.
+    Object construction (Python objects, untimed by the reference too) happens once, up front.
+    """
+
+    def __init__(self, workload: str = "C5", k: int = 100, n_workers: int = 0, tick_index: int = 0):
+        import numpy as np
+
+        p = os.path.join(ROOT, "baseline", "_ref")
+        if not os.path.isdir(os.path.join(p, "tickjoin")):
+            raise FileNotFoundError("baseline/_ref/tickjoin is not installed (see DESIGN.md §6)")
+        if p not in sys.path:
+            sys.path.insert(0, p)
+        from tickjoin import engine as ref_engine
+        from tickjoin import geometry as ref_geom
+
+        self.E, self.G = ref_engine, ref_geom
+        self.n_workers = n_workers or (os.cpu_count() or 1)
+        it = iter_workload(workload, tick_index + 1)
+        for tick in it:
+            pass
+        self.tick = tick
+        self.m = int(tick.n_queries)
+        self.k = max(1, min(k, self.m))
+        G = ref_geom
+        t0 = time.perf_counter()
+        self.objects = [G.MovingObject(i, G.Point(x, y))
+                        for i, x, y in zip(tick.ids.tolist(), tick.xs.tolist(), tick.ys.tolist())]
+        self.setup_s = time.perf_counter() - t0
+        # Morton order of the query centres (16 bits per axis over the queries' extent)
+        cx = (tick.qxa + tick.qxb) * 0.5
+        cy = (tick.qya + tick.qyb) * 0.5
+
+        def q16(v):
+            lo, hi = float(v.min()), float(v.max())
+            s = 65535.0 / (hi - lo) if hi > lo else 0.0
+            return np.minimum(((v - lo) * s).astype(np.int64), 65535).astype(np.uint64)
+
+        def spread(v):
+            v = (v | (v << np.uint64(16))) & np.uint64(0x0000FFFF0000FFFF)
+            v = (v | (v << np.uint64(8))) & np.uint64(0x00FF00FF00FF00FF)
+            v = (v | (v << np.uint64(4))) & np.uint64(0x0F0F0F0F0F0F0F0F)
+            v = (v | (v << np.uint64(2))) & np.uint64(0x3333333333333333)
+            return (v | (v << np.uint64(1))) & np.uint64(0x5555555555555555)
+
+        code = spread(q16(cx)) | (spread(q16(cy)) << np.uint64(1))
+        self.order = np.argsort(code, kind="stable")
+        self.d0 = []
+
+    def _engine(self):
+        return self.E.Engine(self.E.MethodConfig(method="quad", n_workers=self.n_workers))
+
+    def chunk_queries(self, j: int):
+        t, G = self.tick, self.G
+        lo, hi = (j * self.m) // self.k, ((j + 1) * self.m) // self.k
+        rows = self.order[lo:hi]
+        return [G.Query(int(q), G.Rect(a, b, c, d)) for q, a, b, c, d in
+                zip(t.qids[rows].tolist(), t.qxa[rows].tolist(), t.qya[rows].tolist(), t.qxb[rows].tolist(),
+                    t.qyb[rows].tolist())]
+
+    def run_d0(self) -> float:
+        _, st = self._engine().process_tick(self.G.TickBatch(self.tick.tick_index, self.objects, []))
+        self.d0.append(st.durations["total"])
+        return self.d0[-1]
+
+    def run_chunk(self, j: int) -> dict:
+        qs = self.chunk_queries(j)
+        gc.collect()
+        _, st = self._engine().process_tick(self.G.TickBatch(self.tick.tick_index, self.objects, qs))
+        d0 = statistics.median(self.d0)
+        dur = dict(st.durations)
+        est = d0 + self.k * (dur["total"] - d0)
+        stages = {"index_objects": d0, "index_queries": self.k * (dur["index"] - d0),
+                  "filter": self.k * dur["filter"], "decode": self.k * dur["decode"],
+                  "merge": self.k * dur.get("merge", 0.0)}
+        return {"chunk": j, "queries": len(qs), "D_s": dur["total"], "est_tick_s": est, "stages_s": stages,
+                "results": int(st.results_total)}
+
+    def spread_chunks(self, count: int):
+        """`count` chunk indices spread evenly over the k chunks (dense and sparse regions alike)."""
+        return [(i * self.k) // count + (self.k // (2 * count)) for i in range(count)]
+
+
+def reference_sample_text(rs: "RefEngineSample", steps: int) -> str:
+    return (f"reference tickjoin Engine(MethodConfig('quad', n_workers={rs.n_workers})).process_tick from "
+            f"baseline/_ref on the C5 tick {rs.tick.tick_index}: all {rs.tick.n_objects:,} objects with one "
+            f"Morton-contiguous chunk of {rs.m // rs.k:,} of its {rs.m:,} queries per step ({steps} chunk(s) spread "
+            f"over the k={rs.k} chunks); tick time = D0 + k*(D_chunk - D0), D0 = the same call with no queries "
+            f"(index build over all objects, median {statistics.median(rs.d0):.2f} s); the reference's threads "
+            f"share one GIL (effectively one core)")
+
+
 def cpu_reference_sample(n_objects: int, seed: int = 3):
     """The CPU reference (oracle port, oracle/quad_oracle.py) on one tick of the same
     generator configuration with `n_objects` objects; returns (queries/s, seconds, m)."""
@@ -215,6 +316,63 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
+    try:
+        rs = RefEngineSample(args.workload, k=args.ref_chunks)
+    except FileNotFoundError as e:
+        print(f"reference engine unavailable ({e}); timing the NumPy port instead", file=sys.stderr)
+        return run_reference_port(args)
+    for _ in range(max(1, args.warmup)):  # warm-up: the no-query calls that give D0
+        rs.run_d0()
+    runs = [rs.run_chunk(j) for j in rs.spread_chunks(args.steps)]
+    est = [r["est_tick_s"] for r in runs]
+    value = rs.m / statistics.mean(est)
+    stages = {k: statistics.mean(r["stages_s"][k] for r in runs) for k in runs[0]["stages_s"]}
+    sample = reference_sample_text(rs, args.steps)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(est),
+        "p50_tick_ms": 1e3 * statistics.median(est), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
+        "config": ref_config(args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+                         "sample": sample, "n_workers": rs.n_workers, "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_stage_s_per_tick": stages,
+        "reference_runs": [{k: v for k, v in r.items() if k != "stages_s"} for r in runs],
+        "object_setup_s": rs.setup_s,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def ref_config(args):
+    """The `config` object of both arms (identical, so the two lines describe the same workload)."""
+    return {"workload": args.workload, "description": DESCR[args.workload], "method": "quad", "th_quad": 384,
+            "l_max": 12, "rebuild": "every_tick",
+            "l2": "inputs (>=560 MB/tick at 10M) exceed the 126 MB L2; no flush"}
+
+
+def cpu_baseline_line(args):
+    """`cpu_baseline` of our arm: the reference engine on one bounded chunk of the same tick
+    (RefEngineSample: D0 once + the middle chunk, about 30 s of CPU work); the NumPy port if the
+    reference is not installed."""
+    try:
+        rs = RefEngineSample(args.workload, k=args.ref_chunks)
+    except FileNotFoundError:
+        qps, dt, m = cpu_reference_sample(args.cpu_sample)
+        return {"value": qps, "unit": UNIT, "cores": 1, "kind": "port",
+                "sample": (f"oracle/quad_oracle.run_tick (NumPy port of the reference QUAD tick) on one tick of "
+                           f"{args.cpu_sample:,} objects / {m:,} queries with the workload's generator config; "
+                           f"{dt:.1f} s single-threaded (baseline/_ref not installed)")}
+    rs.run_d0()
+    r = rs.run_chunk(rs.k // 2)
+    return {"value": rs.m / r["est_tick_s"], "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
+            "sample": reference_sample_text(rs, 1), "n_workers": rs.n_workers,
+            "est_tick_s": r["est_tick_s"], "stages_s": r["stages_s"]}
+
+
+def run_reference_port(args):
+    rank, world, _ = dist_env()
     n_sample = args.ref_sample
     times, qs = [], []
     for s in range(args.warmup + args.steps):
@@ -231,7 +389,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.mean(times),
         "p50_tick_ms": 1e3 * statistics.median(times), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
-        "config": {"workload": args.workload, "description": DESCR[args.workload], "parallelism": "cpu"},
+        "config": ref_config(args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -492,11 +650,7 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        qps, dt, m = cpu_reference_sample(args.cpu_sample)
-        cpu = {"value": qps, "unit": UNIT, "cores": 1, "kind": "port",
-               "sample": (f"oracle/quad_oracle.run_tick (NumPy port of the reference QUAD tick) on one tick of "
-                          f"{args.cpu_sample:,} objects / {m:,} queries with the workload's generator config "
-                          f"(gaussian, 25 hotspots, 5u); {dt:.1f} s single-threaded")}
+        cpu = cpu_baseline_line(args)
 
     if rank == 0:
         line = {
@@ -505,15 +659,14 @@ def run_ours(args):
             "p50_tick_ms": statistics.median(per_tick), "max_tick_ms": max(per_tick), "higher_is_better": True,
             "scaling": "strong" if sharded else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (RNG-identical reference generator)",
-            "config": {"workload": args.workload, "description": DESCR[args.workload],
-                       "n_objects": n, "queries_per_tick": int(st0.n_queries),
-                       "results_per_tick": int(st0.results_total),
-                       **({"method": "ug", "split_factor": sf} if sf else {"th_quad": 384, "l_max": 12}),
-                       "rebuild": "every_tick", "distinct_ticks_cycled": pool,
-                       "l2": "inputs (>=560 MB/tick at 10M) exceed the 126 MB L2; no flush",
-                       "parallelism": (f"leaf-range sharding over {world} GPUs: NCCL all-gather of each tick's "
-                                       f"updates, per-rank join/decode of its Morton leaf range" if sharded
-                                       else "1 GPU")},
+            "config": ref_config(args),
+            "config_detail": {"n_objects": n, "queries_per_tick": int(st0.n_queries),
+                              "results_per_tick": int(st0.results_total),
+                              **({"method": "ug", "split_factor": sf} if sf else {}),
+                              "distinct_ticks_cycled": pool,
+                              "parallelism": (f"leaf-range sharding over {world} GPUs: NCCL all-gather of each "
+                                              f"tick's updates, per-rank join/decode of its Morton leaf range"
+                                              if sharded else "1 GPU")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "kernel": "tj::k_join",
                          "bytes_per_launch": join_bytes, "ms_per_launch": join_ms, "peak_source": peak_src,
@@ -556,7 +709,9 @@ def main(argv=None):
     ap.add_argument("--split-factor", type=int, default=1024)
     ap.add_argument("--pool", type=int, default=3, help="distinct ticks generated and cycled")
     ap.add_argument("--cpu-sample", type=int, default=1_000_000)
-    ap.add_argument("--ref-sample", type=int, default=500_000)
+    ap.add_argument("--ref-sample", type=int, default=500_000, help="objects per tick of the port fallback")
+    ap.add_argument("--ref-chunks", type=int, default=20,
+                    help="reference arm: the tick's queries are cut into this many Morton-contiguous chunks")
     ap.add_argument("--e2e-steps", type=int, default=12)
     ap.add_argument("--e2e-contexts", type=int, default=3,
                     help="tj_tick contexts driven from this many host threads in the e2e leg (overlap of "

@@ -171,6 +171,11 @@ int tj_get_bitmaps(tj_ctx* ctx, int64_t* n_tasks, int64_t* n_words, int64_t* tas
 /* simulate_assignment over heaviest-first tasks (scheduler.py:31-54):
  * greedy least-loaded assignment of task weights n_isq*n_obj. */
 int tj_get_imbalance(tj_ctx* ctx, int32_t sim_processors, int32_t heaviest_first, double* imbalance);
+/* Object counts of the non-empty leaves in ascending packed cell order: the
+ * array the reference's _occupancy_stats reduces (engine.py:261-267), so the
+ * host computes occupancy mean / var / dispersion exactly as NumPy does.
+ * counts == NULL: only *n_active is returned. */
+int tj_get_occupancy(tj_ctx* ctx, int64_t* counts, int64_t cap, int64_t* n_active);
 
 /* Method "ug_baseline" (baseline.py:26-121): the reference's direct-emission
  * filter stages each task cell's (query, object) pairs privately and flushes

@@ -76,7 +76,7 @@ class TjIndexInfo(ctypes.Structure):
 EXPORTED = (
     "tj_abi_version", "tj_device_count", "tj_create", "tj_destroy", "tj_last_error", "tj_tick",
     "tj_get_index", "tj_get_object_cells", "tj_get_subqueries", "tj_get_directory", "tj_get_bitmaps",
-    "tj_get_imbalance", "tj_get_staging_flushes", "tj_set_shard", "tj_get_stream", "tj_host_alloc", "tj_host_free",
+    "tj_get_imbalance", "tj_get_occupancy", "tj_get_staging_flushes", "tj_set_shard", "tj_get_stream", "tj_host_alloc", "tj_host_free",
 )
 
 _lib: Optional[ctypes.CDLL] = None
@@ -105,6 +105,7 @@ def load_library() -> ctypes.CDLL:
     lib.tj_get_directory.argtypes = [c_void_p, c_void_p, c_int64, c_void_p, i64p, c_void_p, i64p, c_int64]
     lib.tj_get_bitmaps.argtypes = [c_void_p, i64p, i64p] + [c_void_p] * 6 + [c_int64] * 3
     lib.tj_get_imbalance.argtypes = [c_void_p, c_int32, c_int32, POINTER(c_double)]
+    lib.tj_get_occupancy.argtypes = [c_void_p, c_void_p, c_int64, POINTER(c_int64)]
     lib.tj_get_staging_flushes.argtypes = [c_void_p, c_int32, POINTER(c_int64)]
     lib.tj_get_stream.argtypes = [c_void_p, POINTER(c_void_p)]
     lib.tj_set_shard.argtypes = [c_void_p, c_int32, c_int32]
@@ -260,6 +261,14 @@ class NativeContext:
         v = c_int64(0)
         self._check(self.lib.tj_get_staging_flushes(self.h, staging_capacity, ctypes.byref(v)))
         return v.value
+
+    def occupancy(self) -> np.ndarray:
+        """Object counts of the non-empty leaves, ascending packed cell order (int64)."""
+        n = c_int64(0)
+        self._check(self.lib.tj_get_occupancy(self.h, None, 0, ctypes.byref(n)))
+        out = np.zeros(n.value, np.int64)
+        self._check(self.lib.tj_get_occupancy(self.h, _ptr(out), len(out), ctypes.byref(n)))
+        return out
 
     def imbalance(self, sim_processors: int, heaviest_first: bool) -> float:
         v = c_double(0.0)

@@ -1199,6 +1199,28 @@ int tj_get_imbalance(tj_ctx* c, int32_t sim_processors, int32_t heaviest_first, 
   return TJ_OK;
 }
 
+int tj_get_occupancy(tj_ctx* c, int64_t* counts, int64_t cap, int64_t* n_active) {
+  int rc;
+  if ((rc = need_tick(c))) return rc;
+  if (!n_active) return fail(c, TJ_E_INVALID_ARG, "bad arguments");
+  std::vector<int32_t> nobj;
+  std::vector<uint32_t> code;
+  if ((rc = d2h(c, nobj, c->lnobj.p, c->last.L)) || (rc = d2h(c, code, c->lcode.p, c->last.L))) return rc;
+  std::vector<std::pair<int64_t, int32_t>> occ;  // (packed cell, count) of the non-empty leaves
+  const int sh = 2 * c->cfg.l_max;
+  for (int64_t r = 0; r < c->last.L; ++r)
+    if (nobj[r] > 0) {
+      const int64_t lev = code[r] >> kLevelShift, z = code[r] & kPayloadMask;
+      occ.emplace_back(c->ug_sf ? z : (lev << sh) | z, nobj[r]);
+    }
+  std::sort(occ.begin(), occ.end());
+  *n_active = (int64_t)occ.size();
+  if (!counts) return TJ_OK;
+  if (cap < (int64_t)occ.size()) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
+  for (size_t k = 0; k < occ.size(); ++k) counts[k] = occ[k].second;
+  return TJ_OK;
+}
+
 int tj_get_staging_flushes(tj_ctx* c, int32_t staging_capacity, int64_t* flushes) {
   int rc;
   if ((rc = need_tick(c))) return rc;

@@ -168,7 +168,9 @@ def _fill_stats(stats: TickStats, st: "_native.TjStats") -> None:
     if a:
         s1, s2 = int(st.occ_sum), int(st.occ_sumsq)
         stats.occupancy_mean = s1 / a
-        stats.occupancy_var = (a * s2 - s1 * s1) / (a * a)  # exact rational, one rounding
+        stats.occupancy_var = (a * s2 - s1 * s1) / (a * a)  # exact rational, one rounding; the engine
+        # replaces mean / var with NumPy's reductions over the per-leaf counts (bit-identical to the
+        # reference) unless full_stats is off
         stats.dispersion = stats.occupancy_var / stats.occupancy_mean
     stats.device_ms = dict(index=st.t_index_ms, filter=st.t_filter_ms, decode=st.t_decode_ms,
                            merge=st.t_merge_ms, total=st.t_total_ms)
@@ -243,6 +245,11 @@ class Engine:
             stats.split_factor = self._split_factor
         if len(ids):
             _fill_stats(stats, st)
+            if full_stats and stats.active_cells:  # engine.py:261-267 on the same array, in NumPy
+                occ = self._ctx.occupancy()
+                stats.occupancy_mean = float(occ.mean())
+                stats.occupancy_var = float(occ.var())
+                stats.dispersion = stats.occupancy_var / stats.occupancy_mean
             if full_stats and stats.containment_tests:
                 stats.imbalance = self._ctx.imbalance(self.cfg.sim_processors,
                                                       self.cfg.schedule == "heaviest_first")

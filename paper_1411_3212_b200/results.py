@@ -59,3 +59,35 @@ class ColumnarResult:
                 raise DuplicateResult(f"query {q} received a result from two subqueries")
             out[q] = v.tolist()
         return ResultSet(out)
+
+
+def merge_results(chunks, issued_query_ids) -> ResultSet:
+    """Per-issuer union of (query id, object ids) chunks (reference `decode.merge_results`,
+    decode.py:102-123): every issued query present (empty when nothing matched), each list
+    ascending; `DuplicateResult` on a pair produced twice or on results for a query that was
+    never issued.  Vectorised: one lexsort over all (query, object) pairs."""
+    out: dict = {int(q): [] for q in issued_query_ids}
+    qs, vs = [], []
+    for qid, ids in chunks:
+        ids = np.asarray(ids, np.int64).ravel()
+        if len(ids):
+            qs.append(np.full(len(ids), int(qid), np.int64))
+            vs.append(ids)
+    if not qs:
+        return ResultSet(out)
+    q = np.concatenate(qs)
+    v = np.concatenate(vs)
+    order = np.lexsort((v, q))
+    q, v = q[order], v[order]
+    if len(v) > 1:
+        same = (q[1:] == q[:-1]) & (v[1:] == v[:-1])
+        if same.any():
+            raise DuplicateResult(f"query {int(q[1:][same][0])} received a result from two subqueries")
+    starts = np.flatnonzero(np.concatenate([[True], q[1:] != q[:-1]]))
+    ends = np.concatenate([starts[1:], [len(q)]])
+    for s, e in zip(starts.tolist(), ends.tolist()):
+        qid = int(q[s])
+        if qid not in out:
+            raise DuplicateResult(f"results for a query that was never issued: {qid}")
+        out[qid] = v[s:e].tolist()
+    return ResultSet(out)

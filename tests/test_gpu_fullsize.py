@@ -3,12 +3,14 @@
 Configs A (all ticks) and the small fixtures are checked elsewhere against
 reference digests.  Here, at the sizes the bench runs:
 
-* C @5u (the headline, 10M skewed objects): tick 0 — the whole CSR equals the
-  NumPy QUAD oracle's (`oracle/quad_oracle.run_tick`, the reference pipeline
-  restated) together with its counters, and the C brute-force checker's;
-  ticks 0..2 — every query's result count and id digest equal the checker's.
-* C @2u, C @10u, C @20u, E (50M: 40M uniform + 10M extreme hotspot, 1u): two
-  ticks each, every query's count and digest against the checker.
+* C @5u (the headline, 10M skewed objects): ticks 0 and 1 — the whole CSR
+  equals the NumPy QUAD oracle's (`oracle/quad_oracle.run_tick`, the reference
+  pipeline restated) together with its counters, and the C brute-force
+  checker's; ticks 0..4 — the whole CSR equals the checker's.
+* C @2u and C @10u: two ticks each, the whole CSR against the checker.
+* C @20u (2.3e9 results per tick) and E (50M: 40M uniform + 10M extreme
+  hotspot, 1u): two ticks each, every query's count and id digest against the
+  checker.
 * B (1M gaussian, 50u): five ticks against the REFERENCE ENGINE's own results
   (sha256 of its CSR, tests/golden/digests_b.json, made by
   tests/golden/make_b_golden.py) and all 20 ticks against the checker.
@@ -83,15 +85,16 @@ def device_tick(torch, ctx, tick):
     return off, ids, st
 
 
-def stratified_rows(tick, lens, k=500, seed=0):
+def stratified_rows(tick, lens, k=600, seed=0):
     """Query rows to compare list by list: longest lists (hotspot cores, heaviest
-    leaves), rects on the objects' MBR edges, empty lists, random."""
+    leaves), the rects nearest to (or across) the objects' MBR edges, empty lists,
+    random."""
     rng = np.random.default_rng(seed)
     m = tick.n_queries
     longest = np.argsort(lens, kind="stable")[-k:]
     xa, ya, xb, yb = tick.xs.min(), tick.ys.min(), tick.xs.max(), tick.ys.max()
-    edge = np.flatnonzero((tick.qxa <= xa) | (tick.qya <= ya) | (tick.qxb >= xb) | (tick.qyb >= yb))
-    edge = rng.permutation(edge)[:k]
+    gap = np.minimum(np.minimum(tick.qxa - xa, tick.qya - ya), np.minimum(xb - tick.qxb, yb - tick.qyb))
+    edge = np.argsort(gap, kind="stable")[:k]  # negative gap: the rect crosses the MBR edge
     empty = rng.permutation(np.flatnonzero(lens == 0))[:k]
     rand = rng.choice(m, min(m, k), replace=False)
     return np.unique(np.concatenate([longest, edge, empty, rand]).astype(np.int64))
@@ -110,7 +113,7 @@ def compare_rows(torch, tick, off, ids, g, rows):
         assert np.array_equal(got, r_ref)
 
 
-def check_tick(torch, ctx, tick, cell, label):
+def check_tick(torch, ctx, tick, cell, label, full=False):
     off, ids, st = device_tick(torch, ctx, tick)
     assert int(st.results_total) == ids.numel()
     lens, dig = device_summary(torch, off, ids)
@@ -121,6 +124,11 @@ def check_tick(torch, ctx, tick, cell, label):
     rows = stratified_rows(tick, lens, seed=int(st.results_total) & 0xFFFF)
     assert len(rows) >= 2000 or len(rows) >= tick.n_queries // 2
     compare_rows(torch, tick, off, ids, g, rows)
+    if full:  # the whole CSR, list for list, against the checker's exact lists
+        o_ref, r_ref = g.lists(tick.qxa, tick.qya, tick.qxb, tick.qyb)
+        assert np.array_equal(off.cpu().numpy(), o_ref), f"{label}: offsets differ"
+        assert np.array_equal(ids.cpu().numpy(), r_ref), f"{label}: ids differ"
+        del o_ref, r_ref
     g.close()
     del off, ids
     torch.cuda.empty_cache()
@@ -135,10 +143,11 @@ def _ctx():
 
 # ---------------------------------------------------------------- the headline --
 
-def test_c5_tick0_whole_csr_equals_quad_oracle():
-    """Config C @5u tick 0: the whole CSR and the TickStats counters equal the
-    NumPy restatement of the reference QUAD pipeline (about a minute on the host)."""
-    tick = next(bench.iter_workload("C5", 1))
+@pytest.mark.parametrize("t", [0, 1])
+def test_c5_whole_csr_equals_quad_oracle(t):
+    """Config C @5u ticks 0 and 1: the whole CSR and the TickStats counters equal the
+    NumPy restatement of the reference QUAD pipeline (about a minute per tick on the host)."""
+    tick = list(bench.iter_workload("C5", t + 1))[t]
     ctx = _ctx()
     offs, res, st = ctx.tick_host(tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb)
     ctx.close()
@@ -156,15 +165,17 @@ def test_c5_tick0_whole_csr_equals_quad_oracle():
     assert np.array_equal(offs, o2) and np.array_equal(res, r2)
 
 
-FULL = [("C5", 3, 5.0), ("C2", 2, 4.0), ("C10", 2, 10.0), ("C20", 2, 20.0), ("E", 2, 2.0)]
+# (workload, ticks, checker cell size, whole CSR compared list for list as well)
+FULL = [("C5", 5, 5.0, True), ("C2", 2, 4.0, True), ("C10", 2, 10.0, True), ("C20", 2, 20.0, False),
+        ("E", 2, 2.0, False)]
 
 
-@pytest.mark.parametrize("name,ticks,cell", FULL, ids=[f[0] for f in FULL])
-def test_fullsize_every_query(torch_cuda, name, ticks, cell):
+@pytest.mark.parametrize("name,ticks,cell,full", FULL, ids=[f[0] for f in FULL])
+def test_fullsize_every_query(torch_cuda, name, ticks, cell, full):
     ctx = _ctx()
     try:
         for tick in bench.iter_workload(name, ticks):
-            st, lens = check_tick(torch_cuda, ctx, tick, cell, f"{name} tick {tick.tick_index}")
+            st, lens = check_tick(torch_cuda, ctx, tick, cell, f"{name} tick {tick.tick_index}", full=full)
             if name == "C5" and tick.tick_index == 0:  # SURVEY.md §8 measured sizes (reference, tick 0)
                 assert int(st.results_total) == 169_197_114
                 assert int(st.n_leaves) == 60_820 and int(st.l_deep) == 11
