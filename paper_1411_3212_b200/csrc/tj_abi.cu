@@ -60,13 +60,13 @@ struct tj_ctx {
   // inputs
   DBuf ids, xs, ys, qxa, qya, qxb, qyb;
   // objects
-  DBuf code, okey0, okey1, oval0, oval1, sx, sy;
+  DBuf code, okey0, okey1, oval0, oval1, sx, sy, tx, ty;
   // index
   DBuf linfo, pyr, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf qpos, qwin, crect, nsub, qsbase, biglist, leafcnt;
+  DBuf nsub, qsbase, biglist, leafcnt, qnb, qwb;
   // subqueries
-  DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf;
+  DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf, ewb;
   // join / outputs
   DBuf bitmap, outids, outoff, scratch, outoff32;
   // scan / radix scratch
@@ -188,6 +188,8 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(oval1, n * 4);
   ENS(sx, n * 8);
   ENS(sy, n * 8);
+  ENS(tx, n * 8);
+  ENS(ty, n * 8);
   ENS(pyr, pyr_off(F + 1) * 4);
   ENS(clev, Zmax);
   ENS(zmap, Zmax * 4);
@@ -204,12 +206,11 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(leafcur, c->cap_L * 2 * 4);
   ENS(lactive, c->cap_L);
   ENS(lwpre, c->cap_L * 8);
-  ENS(qpos, m * sizeof(int4));
-  ENS(qwin, m * sizeof(int4));
-  ENS(crect, m * sizeof(Rect4));
   ENS(leafcnt, c->cap_L * sizeof(int4));
   ENS(nsub, m * 4);
   ENS(qsbase, m * 4);
+  ENS(qnb, m * 4);
+  ENS(qwb, m * 4);
   ENS(biglist, m * 4);
   ENS(outoff, (m + 1) * 8);
   ENS(partial, 1024 * 8);
@@ -233,6 +234,7 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sqcount, c->cap_S * 4);
   ENS(erect, c->cap_S * sizeof(Rect4));
   ENS(ecount, c->cap_S * 4);
+  ENS(ewb, c->cap_S * 4);
   ENS(slotoff, (c->cap_S + 1) * 8);
   ENS(bitmap, c->cap_W * 4);
   {  // look-back scan state: enough tiles for the longest scanned array
@@ -283,6 +285,9 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.leaf_ubase = P<int64_t>(c->lubase);
   d.nsub = P<int32_t>(c->nsub);
   d.qsbase = P<int32_t>(c->qsbase);
+  d.qnb = P<int32_t>(c->qnb);
+  d.qwb = P<int32_t>(c->qwb);
+  d.ewb = P<int32_t>(c->ewb);
   d.sq_le = P<int2>(c->sqle);
   d.sq_count = P<int32_t>(c->sqcount);
   d.erect = P<Rect4>(c->erect);
@@ -295,9 +300,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.sidx = d.oval[c->obj_passes & 1];
   d.leaf_cur = P<int32_t>(c->leafcur);
   d.leaf_cnt = P<int4>(c->leafcnt);
-  d.qpos = P<int4>(c->qpos);
-  d.qwin = P<int4>(c->qwin);
-  d.crect = P<Rect4>(c->crect);
   d.unit_leaf = P<int32_t>(c->unitleaf);
   d.big_list = P<int32_t>(c->biglist);
   d.leaf_active = c->shard_n > 1 ? P<uint8_t>(c->lactive) : nullptr;
@@ -305,27 +307,45 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.scratch = P<int64_t>(c->scratch);
 }
 
-// stable LSD radix sort of (key, value) pairs over `passes` 8-bit digits
-template <typename KeySrc>
+// one pass of the stable LSD radix sort: digit histograms, their scan, the
+// rank-and-scatter (with the (x, y) payload when XY)
+template <bool XY, typename KeySrc>
 void radix_pass(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc keys, const int32_t* vin, uint32_t* kout,
-                int32_t* vout, const int64_t* n_ptr, int shift) {
+                int32_t* vout, const double* xin, const double* yin, double* xout, double* yout,
+                const int64_t* n_ptr, int shift) {
   const int Gr = 2 * c->num_sms;
   k_radix_upsweep<<<Gr, kRadixThreads, 0, st>>>(keys, n_ptr, c->d_hdr, shift, P<uint32_t>(c->rhist));
   scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)}, c->d_consts,
               c->d_hdr, (int64_t*)nullptr, st);
-  k_radix_downsweep<<<Gr, kRadixThreads, 0, st>>>(keys, vin, kout, vout, n_ptr, c->d_hdr, shift,
-                                                  P<int64_t>(c->roffs));
+  k_radix_downsweep<KeySrc, XY><<<Gr, kRadixThreads, radix_smem_bytes<XY>(), st>>>(
+      keys, vin, kout, vout, xin, yin, xout, yout, n_ptr, c->d_hdr, shift, P<int64_t>(c->roffs));
 }
 
-// stable LSD radix sort of (key, input row) pairs over `passes` 8-bit digits;
-// the first pass takes its keys from `first` and the rows implicitly
-template <typename KeySrc>
-void radix_sort(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc first, uint32_t* k[2], int32_t* v[2],
-                const int64_t* n_ptr, int passes) {
-  radix_pass(c, st, sp, first, (const int32_t*)nullptr, k[1], v[1], n_ptr, 0);
-  for (int p = 1; p < passes; ++p) {
+// Objects into leaf order: stable LSD radix sort of (leaf rank, input row)
+// over `passes` 8-bit digits.  The first pass computes the keys from the
+// l_max codes and the zmap (quadtree.py:161-165) and takes the rows
+// implicitly; the coordinates ride along in every pass (sequential reads and
+// staged writes), the last pass writes them in leaf order (sx, sy) and no keys.
+void sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
+  Dev& d = c->dv;
+  DevHdr* h = c->d_hdr;
+  const int P_ = c->obj_passes;
+  double* bx[2] = {P<double>(c->sx), P<double>(c->tx)};
+  double* by[2] = {P<double>(c->sy), P<double>(c->ty)};
+  const double *xin = d.xs, *yin = d.ys;
+  for (int p = 0; p < P_; ++p) {
     const int src = p & 1, dst = src ^ 1;
-    radix_pass(c, st, sp, ArrKey{k[src]}, v[src], k[dst], v[dst], n_ptr, kRadixBits * p);
+    const bool last = p == P_ - 1;
+    const int ob = (P_ - 1 - p) & 1;  // the last pass lands in (sx, sy)
+    uint32_t* kout = last ? nullptr : d.okey[dst];
+    if (p == 0)
+      radix_pass<true>(c, st, sp, ObjKey{d.code, d.zmap, h}, (const int32_t*)nullptr, kout, d.oval[dst], xin, yin,
+                       bx[ob], by[ob], &h->n, 0);
+    else
+      radix_pass<true>(c, st, sp, ArrKey{d.okey[src]}, d.oval[src], kout, d.oval[dst], xin, yin, bx[ob], by[ob],
+                       &h->n, kRadixBits * p);
+    xin = bx[ob];
+    yin = by[ob];
   }
 }
 
@@ -393,22 +413,20 @@ int launch_stage(tj_ctx* c, int stage) {
       cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
                    c->lb_scan ? P<unsigned long long>(c->sstate2) : nullptr, c->scan_words};
-      k_obj_keys<<<Gn, 256, 0, ss>>>(d);
-      radix_sort(c, ss, sp2, ArrKey{d.okey[0]}, d.okey, d.oval, &h->n, c->obj_passes);
-      k_gather<double><<<Gn, 256, 0, ss>>>(d, d.xs, d.sx);
-      k_gather<double><<<Gn, 256, 0, ss>>>(d, d.ys, d.sy);
+      sort_objects(c, ss, sp2);
       // 5 launches per radix pass (upsweep + 3-kernel scan + downsweep)
-      return 3 + 5 * c->obj_passes;
+      return 5 * c->obj_passes;
     }
     case 1: {  // ---- K2: query -> leaf scatter (concurrent with the object sort) ----
       k_query_count<<<Gs, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
+      scan_launch(sp, ArrIn<int32_t>{d.qnb}, ExclOut<int32_t>{d.qwb}, &h->m, h, &h->Wb, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
       scan_launch(sp, LeafSqIn{d.leaf_cnt}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
                   (int64_t*)nullptr, st);
       k_query_fill<<<Gs, 256, 0, st>>>(d);
       k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
-      return 10;
+      return 13;
     }
     case 2: {  // ---- join preparation -----------------------------------
       const int extra = 0;
@@ -661,6 +679,10 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
+  cudaFuncSetAttribute(k_radix_downsweep<ObjKey, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)radix_smem_bytes<true>());
+  cudaFuncSetAttribute(k_radix_downsweep<ArrKey, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)radix_smem_bytes<true>());
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->join_blocks, k_join, kJT, sizeof(JoinSmem));
   if (c->join_blocks < 1) c->join_blocks = 1;
 
@@ -676,9 +698,9 @@ int tj_destroy(tj_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   drop_graphs(c);
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
-                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->pyr, &c->clev,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->pyr, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->qpos, &c->qwin, &c->crect, &c->leafcnt, &c->nsub, &c->qsbase, &c->biglist, &c->sqle,
+                 &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qnb, &c->qwb, &c->ewb, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->outoff32, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)
@@ -809,7 +831,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       }
       if (H.abort & 1) c->cap_S = std::max<int64_t>(2 * c->cap_S, H.S + H.S / 4 + 256);
       if (H.abort & 2) {
-        c->cap_W = std::max<int64_t>(c->cap_W, H.W + H.W / 4 + 4096);
+        c->cap_W = std::max<int64_t>(c->cap_W, 8 * H.Wb + 2 * H.Wb + 4096);
         c->cap_U = std::max<int64_t>(c->cap_U, H.U + H.U / 4 + 1024);
       }
       if (H.abort & 4) c->cap_R = std::max<int64_t>(2 * c->cap_R, H.R + H.R / 4 + 4096);
@@ -1143,9 +1165,9 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
   std::vector<uint32_t> bm;
-  std::vector<int32_t> info, eslot;
-  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, info, c->ecount.p, H.S)) ||
-      (rc = entry_slots(c, eslot)))
+  std::vector<int32_t> info, eslot, ewb;
+  if ((rc = d2h(c, bm, c->bitmap.p, 8 * H.Wb)) || (rc = d2h(c, info, c->ecount.p, H.S)) ||
+      (rc = d2h(c, ewb, c->ewb.p, H.S)) || (rc = entry_slots(c, eslot)))
     return rc;
   int64_t t = 0, w = 0, k = 0;
   if (task_woff) task_woff[0] = 0;
@@ -1158,9 +1180,8 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
     if (task_nisq) task_nisq[t] = ni;
     const int64_t nb = (no + 31) / 32;
     const std::vector<int32_t> rows = block_in_ref_order(eslot, lv.sbase[r], ni);
-    if (words)
-      for (int64_t j = 0; j < ni; ++j)
-        std::memcpy(words + w + j * nb, bm.data() + lv.woff[r] + (rows[j] - lv.sbase[r]) * nb, nb * 4);
+    if (words)  // the linear layout linear[s * blocks + b] (bitmap.py:105-111) from the slot-ordered rows
+      for (int64_t j = 0; j < ni; ++j) std::memcpy(words + w + j * nb, bm.data() + 8 * (int64_t)ewb[rows[j]], nb * 4);
     if (counts) {
       if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
       for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)info[rows[j]];

@@ -293,19 +293,37 @@ k_radix_upsweep(KeySrc keys, const int64_t* n_ptr, const DevHdr* h, int shift,
   }
 }
 
-// vals_in == nullptr: the value of item i is i (first pass over input rows)
-template <typename KeySrc>
+// vals_in == nullptr: the value of item i is i (first pass over input rows).
+// keys_out == nullptr: the keys are not written (last pass).
+// Payload (x, y) doubles (xin != nullptr): item i's payload is xin[i], yin[i]
+// (the input arrays on the first pass, the previous pass's output after);
+// it moves with the item through the same shared-memory staging, so every
+// pass reads and writes it coalesced instead of a random gather afterwards.
+struct RadixSmem {
+  uint32_t wcnt[kRadixWarps][kRadixDigits];
+  uint32_t base[kRadixDigits];     // running global offset per digit (this chunk)
+  uint32_t tprefix[kRadixDigits];  // tile-local exclusive prefix per digit
+  uint32_t skey[kRadixTile];
+  int32_t sval[kRadixTile];
+  int64_t shs[33];
+};
+struct RadixSmemXY {
+  RadixSmem r;
+  double sx[kRadixTile];
+  double sy[kRadixTile];
+};
+
+template <typename KeySrc, bool XY>
 __global__ void __launch_bounds__(kRadixThreads, TJ_RADIX_MINB)
-k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
-                  int32_t* vals_out, const int64_t* n_ptr, const DevHdr* h, int shift,
+k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
+                  const double* __restrict__ xin, const double* __restrict__ yin, double* __restrict__ xout,
+                  double* __restrict__ yout, const int64_t* n_ptr, const DevHdr* h, int shift,
                   const int64_t* offs /* [digits][G] exclusive */) {
   if (h->abort) return;
-  __shared__ uint32_t wcnt[kRadixWarps][kRadixDigits];
-  __shared__ uint32_t base[kRadixDigits];     // running global offset per digit (this chunk)
-  __shared__ uint32_t tprefix[kRadixDigits];  // tile-local exclusive prefix per digit
-  __shared__ uint32_t skey[kRadixTile];
-  __shared__ int32_t sval[kRadixTile];
-  __shared__ int64_t shs[33];
+  extern __shared__ __align__(16) unsigned char radix_smem[];
+  RadixSmem& S = *reinterpret_cast<RadixSmem*>(radix_smem);
+  double* sx = XY ? reinterpret_cast<RadixSmemXY*>(radix_smem)->sx : nullptr;
+  double* sy = XY ? reinterpret_cast<RadixSmemXY*>(radix_smem)->sy : nullptr;
   const int64_t n = *n_ptr, G = gridDim.x;
   const int64_t chunk = radix_chunk(n, G);
   const int64_t b = blockIdx.x * chunk;
@@ -314,7 +332,7 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
 #pragma unroll
   for (int j = 0; j < kRadixDPT; ++j)
     if (t + j * kRadixThreads < kRadixDigits)
-      base[t + j * kRadixThreads] = (uint32_t)offs[(int64_t)(t + j * kRadixThreads) * G + blockIdx.x];
+      S.base[t + j * kRadixThreads] = (uint32_t)offs[(int64_t)(t + j * kRadixThreads) * G + blockIdx.x];
   const uint32_t lt = (1u << lane) - 1u;
   // keys/values of the current tile are loaded one tile ahead (all IPT loads in flight)
   uint32_t key[kRadixIPT];
@@ -330,7 +348,7 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
   };
   if (b < e) load_tile(b);
   for (int64_t tb = b; tb < e; tb += kRadixTile) {
-    for (int k = t; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&wcnt[0][0])[k] = 0;
+    for (int k = t; k < kRadixWarps * kRadixDigits; k += kRadixThreads) (&S.wcnt[0][0])[k] = 0;
     __syncthreads();
     uint32_t dig[kRadixIPT], rk[kRadixIPT];
     // warp w owns items [tb + w*32*IPT, ...), processed in rounds of 32 in order
@@ -350,8 +368,8 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
       const int leader = __ffs(peers) - 1;
       uint32_t old = 0;
       if (ok && lane == leader) {
-        old = wcnt[w][dig[r]];
-        wcnt[w][dig[r]] = old + __popc(peers);
+        old = S.wcnt[w][dig[r]];
+        S.wcnt[w][dig[r]] = old + __popc(peers);
       }
       old = __shfl_sync(0xffffffffu, old, leader);
       rk[r] = old + __popc(peers & lt);
@@ -368,42 +386,69 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out,
       if (dgt < kRadixDigits) {
 #pragma unroll
         for (int ww = 0; ww < kRadixWarps; ++ww) {
-          const uint32_t c = wcnt[ww][dgt];
-          wcnt[ww][dgt] = acc;
+          const uint32_t c = S.wcnt[ww][dgt];
+          S.wcnt[ww][dgt] = acc;
           acc += c;
         }
       }
       run[j] = acc;
       int64_t tot;
-      const int64_t ex = block_excl_scan((int64_t)acc, shs, &tot);
-      if (dgt < kRadixDigits) tprefix[dgt] = (uint32_t)(ex + carry);
+      const int64_t ex = block_excl_scan((int64_t)acc, S.shs, &tot);
+      if (dgt < kRadixDigits) S.tprefix[dgt] = (uint32_t)(ex + carry);
       carry += tot;
     }
     __syncthreads();
+    uint32_t pos[kRadixIPT];
 #pragma unroll
     for (int r = 0; r < kRadixIPT; ++r) {
+      pos[r] = 0xffffffffu;
       if (dig[r] < (uint32_t)kRadixDigits) {
-        const uint32_t pos = tprefix[dig[r]] + wcnt[w][dig[r]] + rk[r];
-        skey[pos] = key[r];
-        sval[pos] = val[r];
+        pos[r] = S.tprefix[dig[r]] + S.wcnt[w][dig[r]] + rk[r];
+        S.skey[pos[r]] = key[r];
+        S.sval[pos[r]] = val[r];
+      }
+    }
+    if constexpr (XY) {  // payload: coalesced loads straight into the staged order, 4 in flight per lane
+#pragma unroll
+      for (int r0 = 0; r0 < kRadixIPT; r0 += 4) {
+        double xv[4], yv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int64_t i = tb + (int64_t)w * 32 * kRadixIPT + (r0 + u) * 32 + lane;
+          xv[u] = pos[r0 + u] != 0xffffffffu ? __ldcs(xin + i) : 0.0;
+          yv[u] = pos[r0 + u] != 0xffffffffu ? __ldcs(yin + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (pos[r0 + u] != 0xffffffffu) {
+            sx[pos[r0 + u]] = xv[u];
+            sy[pos[r0 + u]] = yv[u];
+          }
       }
     }
     if (tb + kRadixTile < e) load_tile(tb + kRadixTile);  // next tile in flight during the scatter
     __syncthreads();
     const int tile_n = (int)((e - tb) < kRadixTile ? (e - tb) : kRadixTile);
     for (int p = t; p < tile_n; p += kRadixThreads) {
-      const uint32_t k = skey[p];
+      const uint32_t k = S.skey[p];
       const uint32_t d = (k >> shift) & (kRadixDigits - 1);
-      const int64_t dst = (int64_t)base[d] + (p - tprefix[d]);
-      keys_out[dst] = k;
-      vals_out[dst] = sval[p];
+      const int64_t dst = (int64_t)S.base[d] + (p - S.tprefix[d]);
+      if (keys_out) keys_out[dst] = k;
+      vals_out[dst] = S.sval[p];
+      if constexpr (XY) {
+        xout[dst] = sx[p];
+        yout[dst] = sy[p];
+      }
     }
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < kRadixDPT; ++j)
-      if (t + j * kRadixThreads < kRadixDigits) base[t + j * kRadixThreads] += run[j];
+      if (t + j * kRadixThreads < kRadixDigits) S.base[t + j * kRadixThreads] += run[j];
     __syncthreads();
   }
 }
+
+template <bool XY>
+constexpr size_t radix_smem_bytes() { return XY ? sizeof(RadixSmemXY) : sizeof(RadixSmem); }
 
 }  // namespace tj

@@ -96,8 +96,11 @@ def stratified_rows(tick, lens, k=600, seed=0):
     gap = np.minimum(np.minimum(tick.qxa - xa, tick.qya - ya), np.minimum(xb - tick.qxb, yb - tick.qyb))
     edge = np.argsort(gap, kind="stable")[:k]  # negative gap: the rect crosses the MBR edge
     empty = rng.permutation(np.flatnonzero(lens == 0))[:k]
-    rand = rng.choice(m, min(m, k), replace=False)
-    return np.unique(np.concatenate([longest, edge, empty, rand]).astype(np.int64))
+    rows = np.unique(np.concatenate([longest, edge, empty]).astype(np.int64))
+    want = min(m, max(2000, len(rows) + k))  # top up with random rows: >= 2,000 distinct in all
+    while len(rows) < want:
+        rows = np.unique(np.concatenate([rows, rng.choice(m, want - len(rows), replace=False)]))
+    return rows
 
 
 def compare_rows(torch, tick, off, ids, g, rows):
