@@ -64,9 +64,9 @@ struct tj_ctx {
   // index
   DBuf linfo, pyr, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf nsub, qsbase, biglist, leafcnt, qnb, qwb;
+  DBuf qpos, qwin, crect, nsub, qsbase, biglist, leafcnt;
   // subqueries
-  DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf, ewb;
+  DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf;
   // join / outputs
   DBuf bitmap, outids, outoff, scratch, outoff32;
   // scan / radix scratch
@@ -74,6 +74,7 @@ struct tj_ctx {
   int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
   bool lb_scan = false;       // single-pass look-back scan (measured slower here than reduce-then-scan)
   bool serial_sort = false;   // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)
+  bool sort_xy = false;       // TJ_SORT_XY=1: coordinates carried through the radix passes (no gathers)
   // adaptive rebuild: the last built index (header fields + the buffers it lives in)
   bool have_index = false;
   bool reuse = false;  // this tick reuses it
@@ -186,8 +187,8 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(okey1, n * 4);
   ENS(oval0, n * 4);
   ENS(oval1, n * 4);
-  ENS(sx, n * 8);
-  ENS(sy, n * 8);
+  ENS(sx, n * 8 + 16);  // + slack: the join's bulk copies round a tile up to 16 bytes
+  ENS(sy, n * 8 + 16);
   ENS(tx, n * 8);
   ENS(ty, n * 8);
   ENS(pyr, pyr_off(F + 1) * 4);
@@ -209,8 +210,9 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(leafcnt, c->cap_L * sizeof(int4));
   ENS(nsub, m * 4);
   ENS(qsbase, m * 4);
-  ENS(qnb, m * 4);
-  ENS(qwb, m * 4);
+  ENS(qpos, m * sizeof(int4));
+  ENS(qwin, m * sizeof(int4));
+  ENS(crect, m * sizeof(Rect4));
   ENS(biglist, m * 4);
   ENS(outoff, (m + 1) * 8);
   ENS(partial, 1024 * 8);
@@ -234,7 +236,6 @@ int prepare_dynamic(tj_ctx* c) {
   ENS(sqcount, c->cap_S * 4);
   ENS(erect, c->cap_S * sizeof(Rect4));
   ENS(ecount, c->cap_S * 4);
-  ENS(ewb, c->cap_S * 4);
   ENS(slotoff, (c->cap_S + 1) * 8);
   ENS(bitmap, c->cap_W * 4);
   {  // look-back scan state: enough tiles for the longest scanned array
@@ -285,9 +286,9 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.leaf_ubase = P<int64_t>(c->lubase);
   d.nsub = P<int32_t>(c->nsub);
   d.qsbase = P<int32_t>(c->qsbase);
-  d.qnb = P<int32_t>(c->qnb);
-  d.qwb = P<int32_t>(c->qwb);
-  d.ewb = P<int32_t>(c->ewb);
+  d.qpos = P<int4>(c->qpos);
+  d.qwin = P<int4>(c->qwin);
+  d.crect = P<Rect4>(c->crect);
   d.sq_le = P<int2>(c->sqle);
   d.sq_count = P<int32_t>(c->sqcount);
   d.erect = P<Rect4>(c->erect);
@@ -322,14 +323,16 @@ void radix_pass(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc keys, con
 }
 
 // Objects into leaf order: stable LSD radix sort of (leaf rank, input row)
-// over `passes` 8-bit digits.  The first pass computes the keys from the
-// l_max codes and the zmap (quadtree.py:161-165) and takes the rows
-// implicitly; the coordinates ride along in every pass (sequential reads and
-// staged writes), the last pass writes them in leaf order (sx, sy) and no keys.
-void sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
+// over `passes` 8-bit digits (keys from k_obj_keys, rows implicit in the
+// first pass; the last pass writes no keys), then the coordinates gathered
+// into leaf order.  TJ_SORT_XY=1: the coordinates ride along through every
+// pass instead (sequential reads and staged writes; measured slower here).
+int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
   Dev& d = c->dv;
   DevHdr* h = c->d_hdr;
   const int P_ = c->obj_passes;
+  const int Gn = grid_for(c, c->n);
+  k_obj_keys<<<Gn, 256, 0, st>>>(d);
   double* bx[2] = {P<double>(c->sx), P<double>(c->tx)};
   double* by[2] = {P<double>(c->sy), P<double>(c->ty)};
   const double *xin = d.xs, *yin = d.ys;
@@ -338,15 +341,23 @@ void sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
     const bool last = p == P_ - 1;
     const int ob = (P_ - 1 - p) & 1;  // the last pass lands in (sx, sy)
     uint32_t* kout = last ? nullptr : d.okey[dst];
-    if (p == 0)
-      radix_pass<true>(c, st, sp, ObjKey{d.code, d.zmap, h}, (const int32_t*)nullptr, kout, d.oval[dst], xin, yin,
-                       bx[ob], by[ob], &h->n, 0);
-    else
-      radix_pass<true>(c, st, sp, ArrKey{d.okey[src]}, d.oval[src], kout, d.oval[dst], xin, yin, bx[ob], by[ob],
-                       &h->n, kRadixBits * p);
-    xin = bx[ob];
-    yin = by[ob];
+    const int32_t* vin = p == 0 ? (const int32_t*)nullptr : d.oval[src];
+    if (c->sort_xy) {
+      radix_pass<true>(c, st, sp, ArrKey{d.okey[src]}, vin, kout, d.oval[dst], xin, yin, bx[ob], by[ob], &h->n,
+                       kRadixBits * p);
+      xin = bx[ob];
+      yin = by[ob];
+    } else {
+      radix_pass<false>(c, st, sp, ArrKey{d.okey[src]}, vin, kout, d.oval[dst], nullptr, nullptr, nullptr, nullptr,
+                        &h->n, kRadixBits * p);
+    }
   }
+  if (!c->sort_xy) {
+    k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
+    k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
+  }
+  // 5 launches per radix pass (upsweep + 3-kernel scan + downsweep)
+  return 1 + 5 * P_ + (c->sort_xy ? 0 : 2);
 }
 
 // The per-tick launch sequence, in stages (index build, query scatter, join
@@ -413,20 +424,17 @@ int launch_stage(tj_ctx* c, int stage) {
       cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
                    c->lb_scan ? P<unsigned long long>(c->sstate2) : nullptr, c->scan_words};
-      sort_objects(c, ss, sp2);
-      // 5 launches per radix pass (upsweep + 3-kernel scan + downsweep)
-      return 5 * c->obj_passes;
+      return sort_objects(c, ss, sp2);
     }
     case 1: {  // ---- K2: query -> leaf scatter (concurrent with the object sort) ----
       k_query_count<<<Gs, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.nsub}, ExclOut<int32_t>{d.qsbase}, &h->m, h, &h->S, st);
-      scan_launch(sp, ArrIn<int32_t>{d.qnb}, ExclOut<int32_t>{d.qwb}, &h->m, h, &h->Wb, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 1, 0, 0);
       scan_launch(sp, LeafSqIn{d.leaf_cnt}, ExclOut<int32_t>{d.leaf_sbase}, &h->L, h,
                   (int64_t*)nullptr, st);
       k_query_fill<<<Gs, 256, 0, st>>>(d);
       k_leaf_stats<<<Gbig, 256, 0, st>>>(d);
-      return 13;
+      return 10;
     }
     case 2: {  // ---- join preparation -----------------------------------
       const int extra = 0;
@@ -448,7 +456,7 @@ int launch_stage(tj_ctx* c, int stage) {
       scan_launch(sp, ArrIn<int32_t>{d.sq_count}, ExclOut<int64_t>{d.slot_off}, &h->S, h, &h->R, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
       k_close_offsets<<<1, 1, 0, st>>>(d);
-      k_decode_query<<<c->num_sms * 10, kDQThreads, 0, st>>>(d);  // 10 CTAs of 4 warps fill an SM (48 regs)
+      k_decode_query<<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);  // the CTAs its register budget lets reside
       return 8;
     default:  // ---- lists that need a sort by id ----------------------------
       k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
@@ -656,6 +664,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
   if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
   if (const char* ss = std::getenv("TJ_SERIAL_SORT")) c->serial_sort = std::atoi(ss) != 0;
+  if (const char* sx = std::getenv("TJ_SORT_XY")) c->sort_xy = std::atoi(sx) != 0;
   if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
   if (const char* fp = std::getenv("TJ_FUSED_PYR")) c->fused_pyr = std::atoi(fp) != 0;
   cudaSetDevice(c->device);
@@ -679,10 +688,10 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   }
   for (auto& e : c->ev) cudaEventCreate(&e);
   cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
-  cudaFuncSetAttribute(k_radix_downsweep<ObjKey, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)radix_smem_bytes<true>());
   cudaFuncSetAttribute(k_radix_downsweep<ArrKey, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)radix_smem_bytes<true>());
+  cudaFuncSetAttribute(k_radix_downsweep<ArrKey, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)radix_smem_bytes<false>());
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->join_blocks, k_join, kJT, sizeof(JoinSmem));
   if (c->join_blocks < 1) c->join_blocks = 1;
 
@@ -700,7 +709,7 @@ int tj_destroy(tj_ctx* c) {
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
                  &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->pyr, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qnb, &c->qwb, &c->ewb, &c->biglist, &c->sqle,
+                 &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qpos, &c->qwin, &c->crect, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->outoff32, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
   for (DBuf* b : all)
@@ -831,7 +840,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       }
       if (H.abort & 1) c->cap_S = std::max<int64_t>(2 * c->cap_S, H.S + H.S / 4 + 256);
       if (H.abort & 2) {
-        c->cap_W = std::max<int64_t>(c->cap_W, 8 * H.Wb + 2 * H.Wb + 4096);
+        c->cap_W = std::max<int64_t>(c->cap_W, H.W + H.W / 4 + 4096);
         c->cap_U = std::max<int64_t>(c->cap_U, H.U + H.U / 4 + 1024);
       }
       if (H.abort & 4) c->cap_R = std::max<int64_t>(2 * c->cap_R, H.R + H.R / 4 + 4096);
@@ -1165,9 +1174,9 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
   std::vector<uint32_t> bm;
-  std::vector<int32_t> info, eslot, ewb;
-  if ((rc = d2h(c, bm, c->bitmap.p, 8 * H.Wb)) || (rc = d2h(c, info, c->ecount.p, H.S)) ||
-      (rc = d2h(c, ewb, c->ewb.p, H.S)) || (rc = entry_slots(c, eslot)))
+  std::vector<int32_t> info, eslot;
+  if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, info, c->ecount.p, H.S)) ||
+      (rc = entry_slots(c, eslot)))
     return rc;
   int64_t t = 0, w = 0, k = 0;
   if (task_woff) task_woff[0] = 0;
@@ -1180,8 +1189,9 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
     if (task_nisq) task_nisq[t] = ni;
     const int64_t nb = (no + 31) / 32;
     const std::vector<int32_t> rows = block_in_ref_order(eslot, lv.sbase[r], ni);
-    if (words)  // the linear layout linear[s * blocks + b] (bitmap.py:105-111) from the slot-ordered rows
-      for (int64_t j = 0; j < ni; ++j) std::memcpy(words + w + j * nb, bm.data() + 8 * (int64_t)ewb[rows[j]], nb * 4);
+    if (words)
+      for (int64_t j = 0; j < ni; ++j)
+        std::memcpy(words + w + j * nb, bm.data() + lv.woff[r] + (rows[j] - lv.sbase[r]) * nb, nb * 4);
     if (counts) {
       if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
       for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)info[rows[j]];

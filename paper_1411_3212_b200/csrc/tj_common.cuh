@@ -39,8 +39,7 @@ struct DevHdr {
   int32_t reuse_index;      // adaptive policy: this tick reuses the previous index
   int64_t Z, L;             // deepest cells, leaves
   int64_t S, S_i, S_c;      // subqueries: all / intersecting / covering
-  int64_t n_tasks, W, U;    // join tasks, bitmap words (the reference's count), work units
-  int64_t Wb;               // bitmap rows as laid out on the device: 8-word (32-byte) blocks, slot order
+  int64_t n_tasks, W, U;    // join tasks, bitmap words, work units
   int64_t R;                // results
   int64_t R_check;          // results counted in query order (must equal R)
   // statistics (engine.py:212-258)

@@ -56,9 +56,6 @@ struct Dev {
   // queries
   int32_t* nsub;
   int32_t* qsbase;
-  int32_t* qnb;             // per query: 8-word bitmap blocks of its intersecting subqueries (count pass)
-  int32_t* qwb;             // exclusive prefix of qnb: the query's first bitmap block (rows in slot order)
-  int32_t* ewb;             // per directory entry (intersecting): first bitmap block of its row
   // subqueries
   int2* sq_le;              // per subquery slot: (leaf rank, directory entry); query and covering flag are
                             // implied (slot ranges per query; entry row >= the leaf's intersecting count)
@@ -68,7 +65,10 @@ struct Dev {
   int4* linfo;              // per leaf: object base, object count, entry base, intersecting count
   int64_t* slot_off;        // per slot (S + 1): start of its run in the output CSR
   int32_t* leaf_cur;       // per leaf x {intersecting, covering}: fill cursor of large-window pairs
-  int4* leaf_cnt;          // per leaf: intersecting / covering pairs (x, y; z, w unused)
+  int4* leaf_cnt;          // per leaf: intersecting / covering pairs of small windows, of large windows
+  int4* qpos;              // per small-window query: each pair's place in its leaf block
+  int4* qwin;              // per query: deepest-cell window of its clipped rect (count pass -> fill pass)
+  Rect4* crect;            // per query: clipped rect (count pass -> fill pass)
   int32_t* unit_leaf;      // join work unit -> leaf
   uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
   int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
@@ -79,12 +79,6 @@ struct Dev {
   int64_t* out_ids;
   int64_t* out_off;
 };
-
-// Bitmap rows are stored in SLOT order (query-major, the order the decode
-// reads them), each row padded to whole 32-byte sectors: a leaf of nobj
-// objects has a row of ceil(nobj/32) words in ceil(nobj/256) 8-word blocks.
-// The join scatters whole sectors; the decode streams them.
-__host__ __device__ __forceinline__ int row_blocks(int nobj) { return (nobj + 255) >> 8; }
 
 // multi-GPU leaf-range sharding: leaf r belongs to this rank (always, unsharded)
 __device__ __forceinline__ bool leaf_on(const uint8_t* active, int64_t r) { return !active || active[r]; }
@@ -399,16 +393,37 @@ struct ZOut {
   }
 };
 
-// object -> leaf rank (quadtree.py:161-165): the key of the first radix pass,
-// computed on the fly from the l_max code and the zmap
-struct ObjKey {
-  const uint32_t* code;
-  const uint32_t* zmap;
-  const DevHdr* h;
-  __device__ uint32_t operator()(int64_t i) const {
-    return zmap[code[i] >> (2 * (h->l_max - h->l_deep))] & kPayloadMask;
+// object -> leaf rank (quadtree.py:161-165) as the radix key; the value of
+// the first radix pass is the input row itself (implicit)
+__global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const int64_t n = h->n;
+  const int sh = 2 * (h->l_max - h->l_deep);
+  TJ_GRID_STRIDE(i, n) d.okey[0][i] = d.zmap[d.code[i] >> sh] & kPayloadMask;
+}
+
+// Payload gather into leaf order, one array per launch: each launch's random
+// reads hit one 80 MB array (at 10M objects) that can stay L2-resident,
+// instead of two arrays (160 MB) thrashing the 126 MB L2 together.
+template <typename T>
+__global__ void __launch_bounds__(256) k_gather(const Dev d, const T* __restrict__ src, T* __restrict__ dst) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const int64_t n = h->n;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
+    int32_t r[4];  // four independent gathers in flight per thread
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = p0 + u * stride < n ? d.sidx[p0 + u * stride] : 0;
+    T v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = p0 + u * stride < n ? __ldcg(src + r[u]) : T(0);
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (p0 + u * stride < n) __stcs(dst + p0 + u * stride, v[u]);
   }
-};
+}
 
 // checks after a size became known: abort bits make the rest of the tick a no-op
 __global__ void k_check_caps(DevHdr* h, int stage, int radix_bits_obj, int radix_bits_sq) {
@@ -418,7 +433,6 @@ __global__ void k_check_caps(DevHdr* h, int stage, int radix_bits_obj, int radix
     if (radix_bits_sq < 32 && (2 * h->L - 1) >> radix_bits_sq) atomicOr(&h->abort, 32);
   } else if (stage == 1) {
     if (h->S > h->cap_S) atomicOr(&h->abort, 1);
-    if (8 * h->Wb > h->cap_W) atomicOr(&h->abort, 2);
   } else if (stage == 2) {
     if (h->W > h->cap_W || h->U > h->cap_U) atomicOr(&h->abort, 2);
   } else if (stage == 3) {
@@ -548,13 +562,13 @@ __device__ __forceinline__ bool clip_window(const Dev& d, int64_t q, double xa, 
 }
 
 // Counting sort of the (query, leaf) pairs into per-leaf directory blocks
-// (directory.py:119-158), two passes over the queries, both recomputing the
-// clip, the window and the leaves from the input rect (the zmap probes hit
-// L2; nothing per query is handed from one pass to the other but its counts):
-//  count: every pair bumps its leaf's intersecting or covering counter; the
-//    query's subquery count and bitmap-row blocks are written;
-//  fill: (after scans of the block sizes and of the per-query counts) every
-//    pair takes a place in its leaf block from the leaf's cursor.
+// (directory.py:119-158), two passes over the queries:
+//  count: every pair bumps its leaf's intersecting or covering counter.  A
+//    small window (<= 2x2 deepest cells, every query of configs A-C keeps
+//    the counter's old value — its place in the block — for the fill;
+//  fill: (after a scan of the block sizes) a small-window pair lands at that
+//    place with no further atomics; pairs of larger windows take places after
+//    the small ones from a cursor.
 // Within a block, entries are in this (unordered) fill order; the join and
 // the decode are invariant to it and the introspection entry points return
 // the reference's query order (directory.py:131).
@@ -562,125 +576,118 @@ __device__ __forceinline__ bool pair_cov(const Dev& d, int lev, uint32_t z, cons
   return cov_on && covers(r, lev, z, d.h);
 }
 
-struct ScatterCtx {
-  double xa, ya, xb, yb, sx, sy;
-  int wpos, hpos, ld, cov_on;
-  uint32_t side;
-  __device__ explicit ScatterCtx(const DevHdr* h)
-      : xa(h->xa), ya(h->ya), xb(h->xb), yb(h->yb), sx(h->sx_deep), sy(h->sy_deep), wpos(h->wpos),
-        hpos(h->hpos), ld(h->l_deep), cov_on(h->covering), side(h->side_deep) {}
-};
-
 // clip (geometry.py:80-88), window (quadtree.py:182-183), count subqueries
 // per query and (query, leaf) pairs per leaf block
 __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const int64_t m = h->m;
-  const ScatterCtx g(h);
+  const double xa = h->xa, ya = h->ya, xb = h->xb, yb = h->yb;
+  const double sx = h->sx_deep, sy = h->sy_deep;
+  const int wpos = h->wpos, hpos = h->hpos, ld = h->l_deep;
+  const uint32_t side = h->side_deep;
+  const int cov_on = h->covering;
   TJ_GRID_STRIDE(q, m) {
     Rect4 r;
     int4 w;
-    int cnt = 0, nb8 = 0;
-    if (clip_window(d, q, g.xa, g.ya, g.xb, g.yb, g.sx, g.sy, g.wpos, g.hpos, g.side, r, w)) {
+    int cnt = 0;
+    if (clip_window(d, q, xa, ya, xb, yb, sx, sy, wpos, hpos, side, r, w)) {
       if (is_small(w)) {
         uint32_t key[4], rank[4];
-        const int ne = enum_small(w, g.ld, d.zmap, key, rank);
+        const int ne = enum_small(w, ld, d.zmap, key, rank);
+        int pos[4] = {0, 0, 0, 0};
+        uint32_t rc[4] = {0, 0, 0, 0};
 #pragma unroll
         for (int k = 0; k < 4; ++k)
           if (k < ne && leaf_on(d.leaf_active, rank[k])) {
-            const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, g.cov_on);
+            const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, cov_on);
             int4* c = d.leaf_cnt + rank[k];
-            atomicAdd(cv ? &c->y : &c->x, 1);
-            if (!cv) nb8 += row_blocks(d.leaf_nobj[rank[k]]);
+            const int v = atomicAdd(cv ? &c->y : &c->x, 1);  // owned pairs, in order
+            const uint32_t packed = rank[k] | (cv ? 0x80000000u : 0u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {  // (no local-memory indexing)
+              pos[j] = (j == cnt) ? v : pos[j];
+              rc[j] = (j == cnt) ? packed : rc[j];
+            }
             ++cnt;
           }
+        // the fill needs no window walk for these: their leaves (covering flag in bit 31) and places
+        d.qpos[q] = make_int4(pos[0], pos[1], pos[2], pos[3]);
+        w = make_int4((int)rc[0], (int)rc[1], (int)rc[2], (int)rc[3]);
       } else {
-        enum_window(w.x, w.y, w.z, w.w, g.ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
+        d.qpos[q] = make_int4(-1, 0, 0, 0);  // a window the fill walks again
+        enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
           if (!leaf_on(d.leaf_active, rank)) return;
           int4* c = d.leaf_cnt + rank;
-          const bool cv = pair_cov(d, lev, z, r, g.cov_on);
-          atomicAdd(cv ? &c->y : &c->x, 1);
-          if (!cv) nb8 += row_blocks(d.leaf_nobj[rank]);
+          atomicAdd(pair_cov(d, lev, z, r, cov_on) ? &c->w : &c->z, 1);
           ++cnt;
         });
       }
     }
-    d.qnb[q] = nb8;
     d.nsub[q] = cnt;
+    d.qwin[q] = w;
+    d.crect[q] = r;
   }
 }
 
 
-__device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, uint32_t rank, bool cv, const Rect4& r,
-                                              int32_t& wb) {
-  const int4 c = d.leaf_cnt[rank];
-  const int32_t e = d.leaf_sbase[rank] + (cv ? c.x : 0) + atomicAdd(&d.leaf_cur[2 * rank + (cv ? 1 : 0)], 1);
+__device__ __forceinline__ void emit_subquery(const Dev& d, int32_t slot, uint32_t rank, int32_t e, const Rect4& r) {
   d.sq_le[slot] = make_int2((int32_t)rank, e);  // one 8-byte store
   d.erect[e] = r;  // the join's input, in entry order
-  if (!cv) {
-    d.ewb[e] = wb;
-    wb += row_blocks(d.leaf_nobj[rank]);
-  }
 }
 
 // Fill: per query, subqueries in ascending packed (level, z) order — the
 // depth-first walk yields z-ascending order within each level, so a per-level
-// counting placement gives the reference's order (quadtree.py:194-217).  Each
-// intersecting entry also gets its bitmap row's place: the query's first block
-// plus the blocks of its earlier slots (rows in slot order).
+// counting placement gives the reference's order (quadtree.py:194-217).
 __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const int64_t m = h->m;
-  const ScatterCtx g(h);
+  const int ld = h->l_deep;
+  const int cov_on = h->covering;
   TJ_GRID_STRIDE(q, m) {
     const int n = d.nsub[q];
     if (n == 0) continue;
-    Rect4 r;
-    int4 w;
-    clip_window(d, q, g.xa, g.ya, g.xb, g.yb, g.sx, g.sy, g.wpos, g.hpos, g.side, r, w);
+    const Rect4 r = d.crect[q];  // clip from the count pass
+    const int4 p4 = d.qpos[q];
+    const int4 w = d.qwin[q];  // small window: its leaves as found by the count pass; else the window
     const int32_t base = d.qsbase[q];
-    int32_t wb = d.qwb[q];
-    if (is_small(w)) {
-      uint32_t key[4], rank[4];
-      const int ne = enum_small(w, g.ld, d.zmap, key, rank);
-      int k2 = 0;
+    if (p4.x >= 0) {
+      const uint32_t rc[4] = {(uint32_t)w.x, (uint32_t)w.y, (uint32_t)w.z, (uint32_t)w.w};
+      const int pos[4] = {p4.x, p4.y, p4.z, p4.w};
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (k < ne && leaf_on(d.leaf_active, rank[k])) {
-          const bool cv = pair_cov(d, (int)(key[k] >> kLevelShift), key[k] & kPayloadMask, r, g.cov_on);
-          emit_subquery(d, base + k2, rank[k], cv, r, wb);
-          ++k2;
+        if (k < n) {
+          const uint32_t rank = rc[k] & 0x7fffffffu;
+          const bool cv = (rc[k] >> 31) != 0;
+          const int4 c = d.leaf_cnt[rank];
+          const int32_t e = d.leaf_sbase[rank] + (cv ? c.x + c.z : 0) + pos[k];
+          emit_subquery(d, base + k, rank, e, r);
         }
       continue;
     }
-    int cur[kMaxLevel + 1], curb[kMaxLevel + 1];
+    int cur[kMaxLevel + 1];
 #pragma unroll
-    for (int l = 0; l <= kMaxLevel; ++l) cur[l] = curb[l] = 0;
+    for (int l = 0; l <= kMaxLevel; ++l) cur[l] = 0;
     if (n > 1) {
-      enum_window(w.x, w.y, w.z, w.w, g.ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
-        if (!leaf_on(d.leaf_active, rank)) return;
-        cur[lev]++;
-        if (!pair_cov(d, lev, z, r, g.cov_on)) curb[lev] += row_blocks(d.leaf_nobj[rank]);
+      enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t, uint32_t rank) {
+        if (leaf_on(d.leaf_active, rank)) cur[lev]++;
       });
-      int run = 0, runb = wb;
+      int run = 0;
 #pragma unroll
       for (int l = 0; l <= kMaxLevel; ++l) {
-        const int c = cur[l], cb = curb[l];
+        const int c = cur[l];
         cur[l] = run;
-        curb[l] = runb;
         run += c;
-        runb += cb;
       }
-    } else {
-#pragma unroll
-      for (int l = 0; l <= kMaxLevel; ++l) curb[l] = wb;
     }
-    enum_window(w.x, w.y, w.z, w.w, g.ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
+    enum_window(w.x, w.y, w.z, w.w, ld, d.zmap, [&](int lev, uint32_t z, uint32_t rank) {
       if (!leaf_on(d.leaf_active, rank)) return;
-      const bool cv = pair_cov(d, lev, z, r, g.cov_on);
-      emit_subquery(d, base + cur[lev]++, rank, cv, r, curb[lev]);
+      const bool cv = pair_cov(d, lev, z, r, cov_on);
+      const int4 c = d.leaf_cnt[rank];
+      const int32_t e = d.leaf_sbase[rank] + (cv ? c.x + c.z + c.y : c.x) +
+                        atomicAdd(&d.leaf_cur[2 * rank + (cv ? 1 : 0)], 1);
+      emit_subquery(d, base + cur[lev]++, rank, e, r);
     });
   }
 }
@@ -860,7 +867,6 @@ struct JoinSmem {
   uint32_t tab[2 * kRows * kTileBlocks];  // [axis][k][b], row stride = tile blocks
   ushort4 kb[kQC];                        // bucket of xa, xb, ya, yb
   int32_t cnt[kQC];
-  int32_t wb[kQC];                        // first bitmap block of each subquery's row
 };
 
 // Monotone bucket map of one axis of a leaf.  Any base and positive scale
@@ -902,6 +908,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
     const int b0 = ot * kTileBlocks, nbt = min(kTileBlocks, nb - b0);
     const int P = min(nobj - b0 * 32, nbt * 32);
     const int32_t ob = li.x + b0 * 32;
+    const int64_t woff = d.leaf_woff[r];
     const int32_t sbase = li.z;
     const bool table = nisq >= kTableMinQ;
     // ---- stage the tile's objects -------------------------------------------
@@ -974,7 +981,6 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       const int nq = min(kQC, nisq - c0);
       for (int t = tid; t < nq; t += kJT) {
         S.cnt[t] = 0;
-        S.wb[t] = d.ewb[sbase + c0 + t];
         if (table) {
           const Rect4 R = erect[c0 + t];
           S.kb[t] = make_ushort4((unsigned short)bucket(R.xa, bx, scx), (unsigned short)bucket(R.xb, bx, scx),
@@ -982,7 +988,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
         }
       }
       __syncthreads();
-      uint32_t* out = d.bitmap + b0;  // row of subquery s: out + 8 * S.wb[s]
+      uint32_t* out = d.bitmap + woff + (int64_t)c0 * nb + b0;
       if (table) {
         const uint32_t* TX = S.tab;
         const uint32_t* TY = S.tab + kRows * nbt;
@@ -1005,7 +1011,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
               if (in_rect(S.ox[o], S.oy[o], R)) D |= 1u << bit;
             } while (A);
           }
-          out[8 * (int64_t)S.wb[s] + b] = D;
+          out[(int64_t)s * nb + b] = D;
           if (D) atomicAdd(&S.cnt[s], __popc(D));
         }
       } else {
@@ -1025,7 +1031,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
             if (in_rect(S.ox[o], S.oy[o], R)) w |= 1u << k;
           }
           if (s < nq) {
-            out[8 * (int64_t)S.wb[s] + b] = w;
+            out[(int64_t)s * nb + b] = w;
             if (w) atomicAdd(&S.cnt[s], __popc(w));
           }
         }
@@ -1252,12 +1258,11 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
   for (int64_t q0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; q0 < m; q0 += nwarp * 32) {
     const int64_t ql = q0 + lane;
     int k = 0;
-    int32_t s0 = 0, qb = 0;
+    int32_t s0 = 0;
     int64_t qo = 0, cnt = 0;
     if (ql < m) {
       k = d.nsub[ql];
       s0 = d.qsbase[ql];
-      qb = d.qwb[ql];
       qo = d.slot_off[s0];
       cnt = d.slot_off[s0 + k] - qo;
       d.out_off[ql] = qo;
@@ -1274,13 +1279,13 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         const int kq = __shfl_sync(0xffffffffu, k, l0);
         const int32_t sq0 = __shfl_sync(0xffffffffu, s0, l0);
         const int64_t cq = __shfl_sync(0xffffffffu, cnt, l0);
-        int32_t wb = __shfl_sync(0xffffffffu, qb, l0);  // the query's rows follow in slot order
         const bool rmerge = mono && kq > 1 && kq <= kRankRuns && cq < (int64_t(1) << 30);
         int64_t* cat = rmerge ? d.scratch : d.out_ids;  // runs concatenated here
         int64_t pos = base;
         for (int j = 0; j < kq; ++j) {
           const int32_t s = sq0 + j;
           const int64_t cj = d.sq_count[s];
+          if (cj == 0) continue;
           const int2 le = d.sq_le[s];
           const int32_t leaf = le.x;
           const int4 li = d.linfo[leaf];
@@ -1289,9 +1294,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
           const int nbw = (nobj + 31) >> 5;
           const int row = le.y - li.z;
           const bool cov = row >= li.w;
-          const uint32_t* wpt = cov ? nullptr : d.bitmap + 8 * (int64_t)wb;
-          if (!cov) wb += row_blocks(nobj);
-          if (cj == 0) continue;
+          const uint32_t* wpt = cov ? nullptr : d.bitmap + d.leaf_woff[leaf] + (int64_t)row * nbw;
           const uint32_t tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
           int64_t got = 0;
           for (int b0 = 0; b0 < nbw; b0 += 32) {
@@ -1326,30 +1329,23 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
       const int32_t slo = __shfl_sync(0xffffffffu, s0, l0);
       const int32_t shi = __shfl_sync(0xffffffffu, s0 + k, l1 - 1);
       const int64_t T = __shfl_sync(0xffffffffu, qo + cnt, l1 - 1) - base;
-      // the window's bitmap rows are contiguous: they start at its first query's block
-      int32_t wcarry = __shfl_sync(0xffffffffu, qb, l0);
       // ---- A: bits -> leaf positions, at their output positions in sa
       for (int32_t c0 = slo; c0 < shi; c0 += 32) {
         const int32_t s = c0 + lane;
-        int nbw = 0, obase = 0, blk = 0;
+        int nbw = 0, obase = 0;
         int64_t wof = -1;
         uint32_t tail = 0;
-        bool cov = false;
-        if (s < shi) {
+        if (s < shi && d.sq_count[s] > 0) {
           const int2 le = d.sq_le[s];
-          const int4 li = d.linfo[le.x];
+          const int32_t leaf = le.x;
+          const int4 li = d.linfo[leaf];
           const int nobj = li.y;
-          cov = le.y - li.z >= li.w;
-          blk = cov ? 0 : row_blocks(nobj);
-          if (d.sq_count[s] > 0) {
-            obase = li.x;
-            nbw = (nobj + 31) >> 5;
-            tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
-          }
+          const int row = le.y - li.z;
+          obase = li.x;
+          nbw = (nobj + 31) >> 5;
+          tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
+          wof = row >= li.w ? -1 : d.leaf_woff[leaf] + (int64_t)row * nbw;
         }
-        const int binc = warp_incl_scan(blk);
-        if (nbw && !cov) wof = 8 * (int64_t)(wcarry + binc - blk);
-        wcarry += __shfl_sync(0xffffffffu, binc, 31);
         const int winc = warp_incl_scan(nbw);
         const int wexc = winc - nbw;
         const int TW = __shfl_sync(0xffffffffu, winc, 31);
