@@ -447,6 +447,12 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=dev)
     pool = max(1, min(args.pool, args.steps + args.warmup))
     ticks = gen_ticks(args.workload, pool)  # the same ticks on every rank
+    if args.shuffle_ids:  # ids not increasing in input order: every tick a fresh permutation of 0..n-1
+        from paper_1411_3212_b200.workload import ColumnarTick
+
+        rng_ids = np.random.default_rng(12345)
+        ticks = [ColumnarTick(t.tick_index, ids=rng_ids.permutation(t.n_objects).astype(np.int64), xs=t.xs,
+                              ys=t.ys, qids=t.qids, qxa=t.qxa, qya=t.qya, qxb=t.qxb, qyb=t.qyb) for t in ticks]
     sf = args.split_factor if args.method == "ug" else 0
     eng = Engine(MethodConfig(method=args.method, split_factor=sf or None, device=local))
     ctx = eng.native
@@ -520,6 +526,16 @@ def run_ours(args):
     join_bytes = 16 * st0.task_objects + 36 * st0.task_subqueries + 4 * st0.bitmap_words
     achieved = join_bytes / (join_ms / 1e3) / 1e9
     traffic, traffic_src = ncu_traffic("k_join")
+    # the dominant kernel, the per-query decode (K4): 4*W (bitmap words read) + 4*R (leaf position ->
+    # input row) + 8*R (result ids written) + 8*(m + 1) (CSR offsets); timed alone between events
+    R_ = int(st0.results_total)
+    m_q = int(st0.n_queries)
+    dec_ms = mean("t_decode_kernel_ms")
+    dec_bytes = 4 * int(st0.bitmap_words) + 12 * R_ + 8 * (m_q + 1)
+    dec_traffic, dec_traffic_src = ncu_traffic("k_decode_query")
+    # the query scatter (K2): 40*m (4 rect doubles + count/base per query) + 8*S (slot) + 8*L
+    sc_ms = mean("t_scatter_ms")
+    sc_bytes = 40 * m_q + 8 * int(st0.n_subqueries) + 8 * int(st0.n_leaves)
     # index build (K0 + K1) against its compulsory bytes 44n + 4Z + 12L.  In the
     # tick the object sort overlaps the query scatter on a side stream, so K1 alone is timed on a
     # second context with the sort kept on the main stream (TJ_SERIAL_SORT=1), a few ticks
@@ -664,14 +680,27 @@ def run_ours(args):
                               "results_per_tick": int(st0.results_total),
                               **({"method": "ug", "split_factor": sf} if sf else {}),
                               "distinct_ticks_cycled": pool,
+                              "object_ids": ("a random permutation of 0..n-1 per tick" if args.shuffle_ids
+                                             else "arange(n)"),
+                              "id_order": ("monotone", "keyed", "sorted")[int(st0.id_order)],
                               "parallelism": (f"leaf-range sharding over {world} GPUs: NCCL all-gather of each "
                                               f"tick's updates, per-rank join/decode of its Morton leaf range"
                                               if sharded else "1 GPU")},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic, "kernel": "tj::k_join",
-                         "bytes_per_launch": join_bytes, "ms_per_launch": join_ms, "peak_source": peak_src,
-                         "traffic_source": traffic_src,
-                         "tests_per_s": st0.containment_tests / (join_ms / 1e3)},
+            "roofline": {"bound": "hbm", "achieved": dec_bytes / (dec_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": dec_bytes / (dec_ms / 1e3) / 1e9 / peak, "traffic": dec_traffic,
+                         "kernel": "tj::k_decode_query", "bytes_per_launch": dec_bytes, "ms_per_launch": dec_ms,
+                         "bytes_model": "4W + 12R + 8(m+1)", "peak_source": peak_src,
+                         "traffic_source": dec_traffic_src},
+            "roofline_join": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                              "frac": achieved / peak, "traffic": traffic, "kernel": "tj::k_join",
+                              "bytes_per_launch": join_bytes, "ms_per_launch": join_ms,
+                              "bytes_model": "16 P_a + 36 S_a + 4 W", "traffic_source": traffic_src,
+                              "tests_per_s": st0.containment_tests / (join_ms / 1e3)},
+            "roofline_scatter": {"kernels": "K2 query scatter (k_query_count, scans, k_query_fill, k_leaf_stats; "
+                                            "concurrent with the object sort)", "ms": sc_ms,
+                                 "compulsory_bytes": sc_bytes, "bytes_model": "40m + 8S + 8L",
+                                 "achieved": sc_bytes / (sc_ms / 1e3) / 1e9,
+                                 "frac": sc_bytes / (sc_ms / 1e3) / 1e9 / peak},
             "roofline_index": {"kernels": "K0 + K1 index build (MBR .. objects in leaf order), timed alone "
                                           "(object sort on the main stream, TJ_SERIAL_SORT=1)",
                                "ms": build_ms, "compulsory_bytes": build_bytes,
@@ -680,6 +709,7 @@ def run_ours(args):
             "stage_ms": {"build": mean("t_build_ms"), "sort": mean("t_sort_ms"),
                          "scatter": mean("t_scatter_ms"), "join": join_ms,
                          "bitmaps": mean("t_filter_ms"), "decode": mean("t_decode_ms"),
+                         "decode_kernel": dec_ms,
                          "merge": mean("t_merge_ms"), "total": mean("t_total_ms")},
             "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": int(sum(int(s.kernel_launches) for s in stats)),
@@ -720,6 +750,9 @@ def main(argv=None):
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--e2e-ids64", action="store_true",
                     help="e2e leg downloads int64 result ids instead of asking for int32 (TJ_OUT_IDS32)")
+    ap.add_argument("--shuffle-ids", action="store_true",
+                    help="object ids a random permutation of 0..n-1 per tick instead of arange (non-monotone ids: "
+                         "leaf blocks put in id order on the device: keyed lists)")
     ap.add_argument("--sharded", action="store_true",
                     help="leaf-range sharded path (NCCL all-gather + tj_set_shard) even at N=1")
     args = ap.parse_args(argv)

@@ -21,7 +21,7 @@
 extern "C" {
 #endif
 
-#define TJ_ABI_VERSION 3
+#define TJ_ABI_VERSION 4
 
 /* status codes — errors.py:4-45 */
 #define TJ_OK 0
@@ -124,7 +124,21 @@ typedef struct tj_stats {
   double t_build_ms;           /* index build alone (K0 + K1: MBR .. leaf directory of objects) */
   double t_scatter_ms;         /* query -> leaf scatter + subquery directory (K2) */
   double t_sort_ms;            /* objects into leaf order (K1's last part, concurrent with K2) */
+  int32_t id_order;            /* how result lists were put in id order (decode.py:117):
+                                  TJ_IDS_MONOTONE, TJ_IDS_KEYED or TJ_IDS_SORTED */
+  int32_t reserved2;
+  double t_decode_kernel_ms;   /* the per-query decode kernel alone (K4 without the offsets scan) */
 } tj_stats;
+
+/* tj_stats.id_order */
+enum {
+  TJ_IDS_MONOTONE = 0, /* ids increase with the input row: runs merge by row                    */
+  TJ_IDS_KEYED = 1,    /* ids are not the rows: objects ranked by id (counting sort over a
+                          presence bitmap), leaf blocks in id order with 32-bit id offsets,
+                          runs merge by offset                                                */
+  TJ_IDS_SORTED = 2    /* each multi-result list sorted by id: the first such tick of a
+                          context, duplicate ids, or an id range of 2^28 or more             */
+};
 
 /* Reference-order index view (QuadIndex, quadtree.py:41-67). */
 typedef struct tj_index_info {

@@ -65,7 +65,8 @@ class TjStats(ctypes.Structure):
         ("rebuilt", c_int32), ("retries", c_int32)] + [
         (k, c_double) for k in ("t_index_ms", "t_filter_ms", "t_decode_ms", "t_merge_ms", "t_total_ms")] + [
         ("mbr", c_double * 4), ("t_join_ms", c_double), ("task_objects", c_int64), ("task_subqueries", c_int64),
-        ("kernel_launches", c_int64), ("t_build_ms", c_double), ("t_scatter_ms", c_double), ("t_sort_ms", c_double)]
+        ("kernel_launches", c_int64), ("t_build_ms", c_double), ("t_scatter_ms", c_double), ("t_sort_ms", c_double),
+        ("id_order", c_int32), ("reserved2", c_int32), ("t_decode_kernel_ms", c_double)]
 
 
 class TjIndexInfo(ctypes.Structure):

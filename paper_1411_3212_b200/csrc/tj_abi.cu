@@ -34,11 +34,12 @@ struct DBuf {
 struct TickGraph {
   Dev dv;
   int64_t n = 0, m = 0;
-  int obj_passes = 0, shard_n = 0, launches[7] = {};
+  int obj_passes = 0, shard_n = 0, launches[8] = {};
   bool reuse = false;
+  bool key_req = false;
   const void* scan_state[2] = {nullptr, nullptr};  // host-side buffers baked into the graph
   int64_t scan_words = 0;
-  cudaGraphExec_t exec[7] = {};
+  cudaGraphExec_t exec[8] = {};
 };
 
 struct tj_ctx {
@@ -52,7 +53,7 @@ struct tj_ctx {
   cudaStream_t st = nullptr;
   cudaStream_t side = nullptr;             // object sort, concurrent with the query scatter
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  cudaEvent_t ev[9] = {};
+  cudaEvent_t ev[10] = {};
   DevHdr* d_hdr = nullptr;
   DevHdr* h_hdr = nullptr;  // pinned
   int64_t* d_consts = nullptr;
@@ -61,6 +62,7 @@ struct tj_ctx {
   DBuf ids, xs, ys, qxa, qya, qxb, qyb;
   // objects
   DBuf code, okey0, okey1, oval0, oval1, sx, sy, tx, ty;
+  DBuf loff, presence, prespre, order;  // keyed lists (ids that are not the rows)
   // index
   DBuf linfo, pyr, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
@@ -79,6 +81,13 @@ struct tj_ctx {
   bool have_index = false;
   bool reuse = false;  // this tick reuses it
   int32_t reuse_not_mono = 0, reuse_not_id = 0;  // id-order flags of this tick, from the reuse check pass
+  unsigned long long reuse_id_kmin = 0, reuse_id_kmax = 0;
+  // keyed lists (ids that are not the rows): the id-key kernels join the launch sequence when the
+  // previous tick's ids qualified — a wrong guess costs speed, never results (k_key_decide checks on
+  // the device; TJ_KEYED=0 turns them off)
+  bool key_auto = true;
+  bool key_req = false;
+  bool dup_ids_seen = false;
   DevHdr idx{};
   // (the kept index lives in zmap, sized by l_max only, and in the leaf codes, which keep their
   // contents when n grows the leaf capacity: see prepare_static)
@@ -191,6 +200,12 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(sy, n * 8 + 16);
   ENS(tx, n * 8);
   ENS(ty, n * 8);
+  if (c->key_req) {
+    ENS(loff, n * 4);
+    ENS(presence, (int64_t(1) << (kKeyBits - 5)) * 4 + 64);
+    ENS(prespre, (int64_t(1) << (kKeyBits - 5)) * 4 + 64);
+    ENS(order, n * 4);
+  }
   ENS(pyr, pyr_off(F + 1) * 4);
   ENS(clev, Zmax);
   ENS(zmap, Zmax * 4);
@@ -299,6 +314,10 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.out_ids = P<int64_t>(c->outids);
   d.out_off = P<int64_t>(c->outoff);
   d.sidx = d.oval[c->obj_passes & 1];
+  d.loff = P<uint32_t>(c->loff);
+  d.presence = P<uint32_t>(c->presence);
+  d.pres_pre = P<int32_t>(c->prespre);
+  d.order = P<int32_t>(c->order);
   d.leaf_cur = P<int32_t>(c->leafcur);
   d.leaf_cnt = P<int4>(c->leafcnt);
   d.unit_leaf = P<int32_t>(c->unitleaf);
@@ -313,13 +332,13 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
 template <bool XY, typename KeySrc>
 void radix_pass(tj_ctx* c, cudaStream_t st, const ScanPlan& sp, KeySrc keys, const int32_t* vin, uint32_t* kout,
                 int32_t* vout, const double* xin, const double* yin, double* xout, double* yout,
-                const int64_t* n_ptr, int shift) {
+                const int64_t* n_ptr, int shift, int gate = 0) {
   const int Gr = 2 * c->num_sms;
   k_radix_upsweep<<<Gr, kRadixThreads, 0, st>>>(keys, n_ptr, c->d_hdr, shift, P<uint32_t>(c->rhist));
   scan_launch(sp, ArrIn<uint32_t>{P<uint32_t>(c->rhist)}, ExclOut<int64_t>{P<int64_t>(c->roffs)}, c->d_consts,
               c->d_hdr, (int64_t*)nullptr, st);
   k_radix_downsweep<KeySrc, XY><<<Gr, kRadixThreads, radix_smem_bytes<XY>(), st>>>(
-      keys, vin, kout, vout, xin, yin, xout, yout, n_ptr, c->d_hdr, shift, P<int64_t>(c->roffs));
+      keys, vin, kout, vout, xin, yin, xout, yout, n_ptr, c->d_hdr, shift, P<int64_t>(c->roffs), gate);
 }
 
 // Objects into leaf order: stable LSD radix sort of (leaf rank, input row)
@@ -332,6 +351,16 @@ int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
   DevHdr* h = c->d_hdr;
   const int P_ = c->obj_passes;
   const int Gn = grid_for(c, c->n);
+  int launched = 0;
+  if (c->key_req) {  // keyed lists: eligibility, duplicate ids, id ranks (idle kernels when the device declines)
+    k_key_decide<<<1, 1, 0, st>>>(h);
+    k_key_zero<<<c->num_sms * 8, 256, 0, st>>>(d);
+    k_key_presence<<<Gn, 256, 0, st>>>(d);
+    scan_launch(sp, PopIn{d.presence}, ExclOut<int32_t>{d.pres_pre}, &h->pres_words, h, &h->pres_total, st);
+    k_key_close<<<1, 1, 0, st>>>(h);
+    k_key_order<<<Gn, 256, 0, st>>>(d);
+    launched += 8;
+  }
   k_obj_keys<<<Gn, 256, 0, st>>>(d);
   double* bx[2] = {P<double>(c->sx), P<double>(c->tx)};
   double* by[2] = {P<double>(c->sy), P<double>(c->ty)};
@@ -341,30 +370,36 @@ int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
     const bool last = p == P_ - 1;
     const int ob = (P_ - 1 - p) & 1;  // the last pass lands in (sx, sy)
     uint32_t* kout = last ? nullptr : d.okey[dst];
-    const int32_t* vin = p == 0 ? (const int32_t*)nullptr : d.oval[src];
+    // first pass: the input rows, or (keyed lists, ids not increasing) the rows in id order
+    const int32_t* vin = p == 0 ? (c->key_req ? (const int32_t*)d.order : nullptr) : d.oval[src];
+    const int gate = p == 0 && c->key_req ? 1 : 0;
     if (c->sort_xy) {
       radix_pass<true>(c, st, sp, ArrKey{d.okey[src]}, vin, kout, d.oval[dst], xin, yin, bx[ob], by[ob], &h->n,
-                       kRadixBits * p);
+                       kRadixBits * p, gate);
       xin = bx[ob];
       yin = by[ob];
     } else {
       radix_pass<false>(c, st, sp, ArrKey{d.okey[src]}, vin, kout, d.oval[dst], nullptr, nullptr, nullptr, nullptr,
-                        &h->n, kRadixBits * p);
+                        &h->n, kRadixBits * p, gate);
     }
+  }
+  if (c->key_req) {  // keyed lists: every leaf position's id offset
+    k_key_loff<<<Gn, 256, 0, st>>>(d);
+    launched += 1;
   }
   if (!c->sort_xy) {
     k_gather<double><<<Gn, 256, 0, st>>>(d, d.xs, d.sx);
     k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
   }
   // 5 launches per radix pass (upsweep + 3-kernel scan + downsweep)
-  return 1 + 5 * P_ + (c->sort_xy ? 0 : 2);
+  return launched + 1 + 5 * P_ + (c->sort_xy ? 0 : 2);
 }
 
 // The per-tick launch sequence, in stages (index build, query scatter, join
 // preparation, join, decode, merge); no host synchronisation inside.  Stage
 // boundaries carry the timing events.  Returns the kernels launched.
-constexpr int kStages = 6;
-constexpr int kSortStage = 6;  // the object sort: its own graph, on the side stream
+constexpr int kStages = 7;
+constexpr int kSortStage = 7;  // the object sort: its own graph, on the side stream
 
 int launch_stage(tj_ctx* c, int stage) {
   cudaStream_t st = c->st;
@@ -450,14 +485,19 @@ int launch_stage(tj_ctx* c, int stage) {
     case 3:  // ---- K3: join ---------------------------------------------
       k_join<<<c->num_sms * c->join_blocks, kJT, sizeof(JoinSmem), st>>>(d);
       return 1;
-    case 4:  // ---- K4: offsets, decode + canonical lists ------------------
+    case 4:  // ---- K4: result offsets ---------------------------------------
       k_cov_counts<<<Gbig, 256, 0, st>>>(d);
       k_slot_counts<<<Gbig, 256, 0, st>>>(d);
       scan_launch(sp, ArrIn<int32_t>{d.sq_count}, ExclOut<int64_t>{d.slot_off}, &h->S, h, &h->R, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 3, 0, 0);
       k_close_offsets<<<1, 1, 0, st>>>(d);
-      k_decode_query<<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);  // the CTAs its register budget lets reside
-      return 8;
+      return 7;
+    case 5:  // ---- K4: decode + canonical lists (its own stage: timed alone) ----
+      // the CTAs its register budget lets reside; the instantiations for the other id modes return at once
+      k_decode_query<kIdsRows><<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);
+      k_decode_query<kIdsKeyed><<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);
+      k_decode_query<kIdsLookup><<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);
+      return 3;
     default:  // ---- lists that need a sort by id ----------------------------
       k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
       return 1;
@@ -465,7 +505,7 @@ int launch_stage(tj_ctx* c, int stage) {
 }
 
 // timing event recorded after each stage: build, scatter, prep, join, decode, merge
-constexpr int kStageEvent[kStages] = {6, 1, 2, 3, 4, 5};
+constexpr int kStageEvent[kStages] = {6, 1, 2, 3, 9, 4, 5};
 
 void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   DevHdr& H = *c->h_hdr;
@@ -487,6 +527,9 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.grid_sf = c->ug_sf;
   H.shard_rank = c->shard_rank;
   H.shard_n = c->shard_n;
+  H.id_kmin = ~0ull;
+  H.id_kmax = 0ull;
+  H.key_req = c->key_req ? 1 : 0;
   if (c->reuse) {  // adaptive reuse: the index's MBR, scales, depth and leaves
     const DevHdr& I = c->idx;
     H.xa = I.xa; H.ya = I.ya; H.xb = I.xb; H.yb = I.yb;
@@ -505,6 +548,8 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
     // the reuse branch of stage 0 skips k_mbr: the check pass measured this tick's id order
     H.not_monotone = c->reuse_not_mono;
     H.not_identity = c->reuse_not_id;
+    H.id_kmin = c->reuse_id_kmin;
+    H.id_kmax = c->reuse_id_kmax;
   }
   const char* dbg = std::getenv("TJ_DEBUG");
   H.dbg = dbg ? std::atoi(dbg) : 0;
@@ -520,7 +565,7 @@ int check_launch(tj_ctx* c) {
 
 bool same_shape(const TickGraph& g, const tj_ctx* c) {
   return g.n == c->n && g.m == c->m && g.obj_passes == c->obj_passes && g.shard_n == c->shard_n &&
-         g.reuse == c->reuse &&
+         g.reuse == c->reuse && g.key_req == c->key_req &&
          g.scan_state[0] == c->sstate.p && g.scan_state[1] == c->sstate2.p && g.scan_words == c->scan_words &&
          std::memcmp(&g.dv, &c->dv, sizeof(Dev)) == 0;
 }
@@ -563,6 +608,7 @@ int run_tick(tj_ctx* c, int64_t* launches) {
       ng.obj_passes = c->obj_passes;
       ng.shard_n = c->shard_n;
       ng.reuse = c->reuse;
+      ng.key_req = c->key_req;
       ng.scan_state[0] = c->sstate.p;
       ng.scan_state[1] = c->sstate2.p;
       ng.scan_words = c->scan_words;
@@ -667,6 +713,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   if (const char* sx = std::getenv("TJ_SORT_XY")) c->sort_xy = std::atoi(sx) != 0;
   if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
   if (const char* fp = std::getenv("TJ_FUSED_PYR")) c->fused_pyr = std::atoi(fp) != 0;
+  if (const char* ky = std::getenv("TJ_KEYED")) c->key_auto = std::atoi(ky) != 0;
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   // side-stream priority (TJ_SIDE_PRIO=1: the object sort's blocks go first) measured no gain:
@@ -707,7 +754,7 @@ int tj_destroy(tj_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   drop_graphs(c);
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
-                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->pyr, &c->clev,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->loff, &c->presence, &c->prespre, &c->order, &c->pyr, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qpos, &c->qwin, &c->crect, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
@@ -818,6 +865,8 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       c->reuse = !rebuild;
       c->reuse_not_mono = H.not_monotone;
       c->reuse_not_id = H.not_identity;
+      c->reuse_id_kmin = H.id_kmin;
+      c->reuse_id_kmax = H.id_kmax;
     }
     bool done = false;
     for (int attempt = 0; attempt < 8 && !done; ++attempt) {
@@ -853,6 +902,11 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
       c->idx = H;
       c->have_index = true;
     }
+    // keyed lists for the next tick, predicted from this one's ids
+    if (H.dup_ids) c->dup_ids_seen = true;
+    c->key_req = c->key_auto && !c->sort_xy && !c->dup_ids_seen && H.not_identity &&
+                 ((H.id_kmax - H.id_kmin) >> kKeyBits) == 0;
+    S.id_order = H.key_mode ? TJ_IDS_KEYED : (!H.not_monotone ? TJ_IDS_MONOTONE : TJ_IDS_SORTED);
     if (H.dup) return fail(c, TJ_E_DUPLICATE_RESULT, "a (query, object) pair was produced twice");
     if (H.count_mismatch) return fail(c, TJ_E_COUNT_MISMATCH, "decoded counts disagree with popcounts");
     R = H.R;
@@ -876,11 +930,14 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     float ks = 0;
     cudaEventElapsedTime(&ks, c->ev[7], c->ev[8]);
     S.t_sort_ms = ks;
+    float kd = 0;
+    cudaEventElapsedTime(&kd, c->ev[9], c->ev[4]);
+    S.t_decode_kernel_ms = kd;
     S.t_total_ms = tot;
     S.task_objects = (int64_t)H.task_obj;
     S.task_subqueries = (int64_t)H.task_isq;
     S.containment_tests = (int64_t)H.tests;
-    S.decoded_bits = H.W * 32;
+    S.decoded_bits = (int64_t)H.W_ref * 32;
     S.subq_intersecting = (int64_t)H.sum_isq;
     S.subq_covering = (int64_t)H.sum_cov;
     S.covering_results = (int64_t)H.cov_results;
@@ -891,7 +948,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     S.n_leaves = H.L;
     S.l_deep = H.l_deep;
     S.n_tasks = H.n_tasks;
-    S.bitmap_words = H.W;
+    S.bitmap_words = (int64_t)H.W_ref;
     S.n_subqueries = H.S;
     S.work_units = H.U;
     S.rebuilt = c->reuse ? 0 : 1;
@@ -1045,6 +1102,26 @@ std::vector<int32_t> block_in_ref_order(const std::vector<int32_t>& eslot, int64
   return es;
 }
 
+// Objects of the last tick in device leaf order: rows[k] = input row at leaf position k, refpos[k] =
+// its place in the reference's leaf block (input order, directory.py:128).  Keyed lists put each
+// leaf block in id order on the device, so refpos is a permutation there; the identity otherwise.
+int leaf_order(tj_ctx* c, const LeafView& lv, std::vector<int32_t>& rows, std::vector<int32_t>& refpos) {
+  int rc;
+  if ((rc = d2h(c, rows, c->dv.sidx, c->n))) return rc;
+  refpos.resize(rows.size());
+  for (size_t k = 0; k < refpos.size(); ++k) refpos[k] = (int32_t)k;
+  if (!c->last.key_mode) return TJ_OK;
+  std::vector<int32_t> ord;
+  for (size_t r = 0; r < lv.nobj.size(); ++r) {
+    const int32_t b = lv.obase[r], no = lv.nobj[r];
+    ord.resize(no);
+    for (int32_t j = 0; j < no; ++j) ord[j] = j;
+    std::sort(ord.begin(), ord.end(), [&](int32_t a, int32_t x) { return rows[b + a] < rows[b + x]; });
+    for (int32_t j = 0; j < no; ++j) refpos[b + ord[j]] = b + j;
+  }
+  return TJ_OK;
+}
+
 int need_tick(tj_ctx* c) {
   if (!c) return TJ_E_INVALID_ARG;
   if (!c->have) return fail(c, TJ_E_INVALID_ARG, "no completed tick with objects to introspect");
@@ -1140,11 +1217,12 @@ int tj_get_directory(tj_ctx* c, int64_t* obj_rows, int64_t obj_cap, int64_t* isq
   if ((rc = load_leaves(c, lv))) return rc;
   if (obj_rows) {
     if (obj_cap < c->n) return fail(c, TJ_E_INVALID_ARG, "obj_rows buffer too small");
-    std::vector<int32_t> sidx;
-    if ((rc = d2h(c, sidx, c->dv.sidx, c->n))) return rc;
+    std::vector<int32_t> rows, refpos, byref(c->n);
+    if ((rc = leaf_order(c, lv, rows, refpos))) return rc;
+    for (int64_t k = 0; k < c->n; ++k) byref[refpos[k]] = rows[k];
     int64_t k = 0;
     for (int64_t r : lv.order)
-      for (int32_t j = 0; j < lv.nobj[r]; ++j) obj_rows[k++] = sidx[lv.obase[r] + j];
+      for (int32_t j = 0; j < lv.nobj[r]; ++j) obj_rows[k++] = byref[lv.obase[r] + j];
   }
   if (isq || cov) {
     if (sq_cap < (int64_t)std::max(H.sum_isq, H.sum_cov)) return fail(c, TJ_E_INVALID_ARG, "sq buffers too small");
@@ -1168,9 +1246,9 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   if ((rc = need_tick(c))) return rc;
   const DevHdr& H = c->last;
   if (n_tasks) *n_tasks = H.n_tasks;
-  if (n_words) *n_words = H.W;
+  if (n_words) *n_words = (int64_t)H.W_ref;
   if (!task_cell && !words && !counts) return TJ_OK;
-  if (task_cap < H.n_tasks || word_cap < H.W) return fail(c, TJ_E_INVALID_ARG, "bitmap buffers too small");
+  if (task_cap < H.n_tasks || word_cap < (int64_t)H.W_ref) return fail(c, TJ_E_INVALID_ARG, "bitmap buffers too small");
   LeafView lv;
   if ((rc = load_leaves(c, lv))) return rc;
   std::vector<uint32_t> bm;
@@ -1178,6 +1256,8 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
   if ((rc = d2h(c, bm, c->bitmap.p, H.W)) || (rc = d2h(c, info, c->ecount.p, H.S)) ||
       (rc = entry_slots(c, eslot)))
     return rc;
+  std::vector<int32_t> orows, refpos;
+  if (c->last.key_mode && words && (rc = leaf_order(c, lv, orows, refpos))) return rc;
   int64_t t = 0, w = 0, k = 0;
   if (task_woff) task_woff[0] = 0;
   for (int64_t r : lv.order) {
@@ -1189,9 +1269,20 @@ int tj_get_bitmaps(tj_ctx* c, int64_t* n_tasks, int64_t* n_words, int64_t* task_
     if (task_nisq) task_nisq[t] = ni;
     const int64_t nb = (no + 31) / 32;
     const std::vector<int32_t> rows = block_in_ref_order(eslot, lv.sbase[r], ni);
-    if (words)
+    if (words && !c->last.key_mode)
       for (int64_t j = 0; j < ni; ++j)
-        std::memcpy(words + w + j * nb, bm.data() + lv.woff[r] + (rows[j] - lv.sbase[r]) * nb, nb * 4);
+        std::memcpy(words + w + j * nb, bm.data() + lv.woff[r] + (rows[j] - lv.sbase[r]) * row_words((int)nb), nb * 4);
+    if (words && c->last.key_mode)  // device bit k of the leaf block -> the reference's bit refpos[k]
+      for (int64_t j = 0; j < ni; ++j) {
+        const uint32_t* src = bm.data() + lv.woff[r] + (rows[j] - lv.sbase[r]) * row_words((int)nb);
+        uint32_t* dst = words + w + j * nb;
+        std::memset(dst, 0, nb * 4);
+        for (int64_t p = 0; p < no; ++p)
+          if ((src[p >> 5] >> (p & 31)) & 1u) {
+            const int64_t q = refpos[lv.obase[r] + p] - lv.obase[r];
+            dst[q >> 5] |= 1u << (q & 31);
+          }
+      }
     if (counts) {
       if (k + ni > count_cap) return fail(c, TJ_E_INVALID_ARG, "counts buffer too small");
       for (int64_t j = 0; j < ni; ++j) counts[k + j] = (int64_t)info[rows[j]];

@@ -39,7 +39,8 @@ struct DevHdr {
   int32_t reuse_index;      // adaptive policy: this tick reuses the previous index
   int64_t Z, L;             // deepest cells, leaves
   int64_t S, S_i, S_c;      // subqueries: all / intersecting / covering
-  int64_t n_tasks, W, U;    // join tasks, bitmap words, work units
+  int64_t n_tasks, W, U;    // join tasks, bitmap words (rows sector-padded), work units
+  unsigned long long W_ref; // bitmap words without the row padding (the reference's count)
   int64_t R;                // results
   int64_t R_check;          // results counted in query order (must equal R)
   // statistics (engine.py:212-258)
@@ -61,6 +62,17 @@ struct DevHdr {
   unsigned long long overfull2, overfull8;  // needs_rebuild counters
   int32_t shard_rank, shard_n;              // leaf-range sharding (n == 1: off)
   int64_t shard_total;                      // total leaf work weight
+  // object ids that are not the input rows ("keyed" lists): every leaf block is put in id order on
+  // the device and carries its ids as 32-bit offsets from id_min (Dev::loff), so the decode merges
+  // runs and emits ids with leaf-local loads (no per-result random id lookups, no per-list sorts)
+  unsigned long long id_kmin, id_kmax;      // order-preserving keys (id ^ 2^63) of the smallest / largest id
+  int64_t id_min;
+  int64_t pres_words;                       // presence bitmap words in use (0: no id counting sort)
+  int64_t pres_total;                       // set bits: n when the ids are distinct
+  int32_t key_req;                          // host: this tick's sequence carries the id-key kernels
+  int32_t key_mode;                         // device: keyed lists (ids not the rows, range < 2^28, distinct)
+  int32_t key_sorted;                       // keyed and not increasing: objects enter the leaf sort in id order
+  int32_t dup_ids;                          // two objects share an id (keyed lists off: k_merge_big sorts)
 };
 
 // dense pyramid layout: level 0 (root) padded to 4 entries, level l >= 1 at

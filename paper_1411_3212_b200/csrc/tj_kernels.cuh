@@ -38,7 +38,12 @@ struct Dev {
   uint32_t* code;
   uint32_t* okey[2];
   int32_t* oval[2];
-  const int32_t* sidx;  // sorted input rows (points into oval[])
+  const int32_t* sidx;  // objects in leaf order: input rows (points into oval[])
+  // keyed lists (DevHdr::key_mode): per leaf position, id - id_min (< 2^28); leaf blocks in id order
+  uint32_t* loff;
+  uint32_t* presence;   // one bit per id offset (2^28 bits): duplicate detection and id ranks
+  int32_t* pres_pre;    // exclusive prefix of the presence words' popcounts
+  int32_t* order;       // id rank -> input row (key_sorted ticks)
   double* sx;
   double* sy;
   // index
@@ -115,6 +120,7 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
   DevHdr* h = d.h;
   const int64_t n = h->n;
   unsigned long long mnx = ~0ull, mny = ~0ull, mxx = 0ull, mxy = 0ull;
+  unsigned long long imn = ~0ull, imx = 0ull;  // id range (rank mode keys)
   int bad = 0, notid = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
@@ -140,6 +146,9 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
         mxy = ky > mxy ? ky : mxy;
         notid |= (v[u] != i);
         bad |= (i + 1 < n) && (v[u] >= nx[u]);
+        const unsigned long long ik = (unsigned long long)v[u] ^ 0x8000000000000000ull;
+        imn = ik < imn ? ik : imn;
+        imx = ik > imx ? ik : imx;
       }
     }
   }
@@ -147,11 +156,15 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
   mny = shfl_min64(mny);
   mxx = shfl_max64(mxx);
   mxy = shfl_max64(mxy);
+  imn = shfl_min64(imn);
+  imx = shfl_max64(imx);
   if (lane_id() == 0) {
     atomicMin(&h->kmin_x, mnx);
     atomicMin(&h->kmin_y, mny);
     atomicMax(&h->kmax_x, mxx);
     atomicMax(&h->kmax_y, mxy);
+    atomicMin(&h->id_kmin, imn);
+    atomicMax(&h->id_kmax, imx);
   }
   if (__any_sync(0xffffffffu, bad) && lane_id() == 0) atomicOr(&h->not_monotone, 1);
   if (__any_sync(0xffffffffu, notid) && lane_id() == 0) atomicOr(&h->not_identity, 1);
@@ -400,7 +413,95 @@ __global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
   if (h->abort) return;
   const int64_t n = h->n;
   const int sh = 2 * (h->l_max - h->l_deep);
-  TJ_GRID_STRIDE(i, n) d.okey[0][i] = d.zmap[d.code[i] >> sh] & kPayloadMask;
+  if (h->key_sorted) {  // keyed lists: the objects enter the stable leaf sort in id order
+    TJ_GRID_STRIDE(j, n) d.okey[0][j] = d.zmap[d.code[d.order[j]] >> sh] & kPayloadMask;
+  } else {
+    TJ_GRID_STRIDE(i, n) d.okey[0][i] = d.zmap[d.code[i] >> sh] & kPayloadMask;
+  }
+}
+
+// ---- keyed lists (object ids that are not the input rows) ------------------
+// The reference sorts every result list by id (decode.py:117, np.sort in
+// merge_results).  When ids are not the rows, the device instead keeps every
+// leaf block in id order and stores each block position's id as a 32-bit
+// offset from the smallest id (loff): every run of a query is then id-sorted,
+// and the decode merges runs of offsets exactly like the monotone path merges
+// runs of rows, reading them leaf-locally.  Ids that do not increase with the
+// row are put in id order by a counting sort over a presence bitmap of the
+// offsets (one bit per possible id: rank = popcounts below it), and the stable
+// leaf sort then takes the objects in that order.  Eligible when the ids'
+// range is below 2^28 (the bitmap; the decode's packed merge heads) and, for
+// non-increasing ids, no two objects share an id (set bits == n); otherwise
+// lists are sorted per query (k_merge_big, which raises DuplicateResult).
+// Within a leaf the reference keeps input order (directory.py:128); the
+// introspection entry points restore it.
+constexpr int kKeyBits = 28;
+__global__ void k_key_decide(DevHdr* h) {
+  h->key_mode = 0;
+  h->key_sorted = 0;
+  h->pres_words = 0;
+  if (h->abort || !h->key_req || !h->not_identity || h->n == 0) return;
+  if (((h->id_kmax - h->id_kmin) >> kKeyBits) != 0) return;
+  h->id_min = (int64_t)(h->id_kmin ^ 0x8000000000000000ull);
+  h->key_mode = 1;
+  if (h->not_monotone) h->pres_words = (int64_t)((h->id_kmax - h->id_kmin) >> 5) + 1;
+}
+
+__global__ void __launch_bounds__(256) k_key_zero(const Dev d) {
+  DevHdr* h = d.h;
+  TJ_GRID_STRIDE(w, h->pres_words) d.presence[w] = 0u;
+}
+__global__ void __launch_bounds__(256) k_key_presence(const Dev d) {
+  DevHdr* h = d.h;
+  if (!h->pres_words) return;
+  const int64_t id_min = h->id_min;
+  TJ_GRID_STRIDE(i, h->n) {
+    const uint32_t off = (uint32_t)(d.ids[i] - id_min);
+    atomicOr(&d.presence[off >> 5], 1u << (off & 31));  // no return value: reductions
+  }
+}
+struct PopIn {
+  const uint32_t* w;
+  __device__ int64_t operator()(int64_t i) const { return __popc(w[i]); }
+};
+__global__ void k_key_close(DevHdr* h) {
+  if (!h->pres_words) return;
+  if (h->pres_total != h->n) {  // a shared id: per-list sorts (and DuplicateResult where a list has both)
+    h->dup_ids = 1;
+    h->key_mode = 0;
+    return;
+  }
+  h->key_sorted = 1;
+}
+// id rank of every object (popcounts of the presence bits below its id): order[rank] = row
+__global__ void __launch_bounds__(256) k_key_order(const Dev d) {
+  DevHdr* h = d.h;
+  if (!h->key_sorted) return;
+  const int64_t id_min = h->id_min;
+  TJ_GRID_STRIDE(i, h->n) {
+    const uint32_t off = (uint32_t)(d.ids[i] - id_min);
+    const uint32_t w = off >> 5;
+    const int32_t rank = d.pres_pre[w] + __popc(d.presence[w] & ((1u << (off & 31)) - 1u));
+    d.order[rank] = (int32_t)i;
+  }
+}
+// every leaf position's id offset, after the leaf sort
+__global__ void __launch_bounds__(256) k_key_loff(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort || !h->key_mode) return;
+  const int64_t n = h->n, id_min = h->id_min;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
+    int32_t r[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) r[u] = p0 + u * stride < n ? d.sidx[p0 + u * stride] : 0;
+    int64_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = p0 + u * stride < n ? __ldcg(reinterpret_cast<const long long*>(d.ids) + r[u]) : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (p0 + u * stride < n) d.loff[p0 + u * stride] = (uint32_t)(v[u] - id_min);
+  }
 }
 
 // Payload gather into leaf order, one array per launch: each launch's random
@@ -697,7 +798,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
   const int64_t L = h->L;
-  unsigned long long act = 0, s1 = 0, s2 = 0, tasks = 0, tests = 0, si = 0, sc = 0, pa = 0, sa = 0;
+  unsigned long long act = 0, s1 = 0, s2 = 0, tasks = 0, tests = 0, si = 0, sc = 0, pa = 0, sa = 0, wr = 0;
   TJ_GRID_STRIDE(r, L) {
     const int4 c = d.leaf_cnt[r];
     const int32_t nisq = c.x + c.z, ncov = c.y + c.w;
@@ -717,6 +818,7 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
         tests += no * ni;
         pa += no;
         sa += ni;
+        if (leaf_on(d.leaf_active, r)) wr += ni * ((no + 31) / 32);
       }
     }
   }
@@ -729,7 +831,9 @@ __global__ void __launch_bounds__(256) k_leaf_stats(const Dev d) {
   sc = warp_sum(sc);
   pa = warp_sum(pa);
   sa = warp_sum(sa);
+  wr = warp_sum(wr);
   if (lane_id() == 0) {
+    if (wr) atomicAdd(&h->W_ref, wr);
     if (pa) atomicAdd(&h->task_obj, pa);
     if (sa) atomicAdd(&h->task_isq, sa);
     if (si) atomicAdd(&h->sum_isq, si);
@@ -786,7 +890,24 @@ constexpr int kQC = TJ_QC;                    // subqueries per chunk
 #define TJ_TMQ 12
 #endif
 constexpr int kTableMinQ = TJ_TMQ;            // table path from this many subqueries
+#ifndef TJ_JOIN_TPS
+#define TJ_JOIN_TPS 1
+#endif
+constexpr bool kJoinTPS = TJ_JOIN_TPS != 0;   // table path: one thread per subquery (0: per (subquery, block))
 
+
+// Optional row padding (TJ_ROW_PAD=8: bitmap rows padded to whole 32-byte
+// sectors, pad words written as zeros by the join): the decode reads each
+// subquery's row at a random place, and an unaligned 28-byte row spans two
+// sectors.  Measured at config C5: the decode is unchanged (it is not bound
+// by those sectors) and the join 18% slower, so rows are unpadded by default.
+// Statistics and the introspection always use the reference's unpadded word
+// counts (bitmap.py:105-111).
+#ifndef TJ_ROW_PAD
+#define TJ_ROW_PAD 1  // 8: sector-padded rows (measured: the decode unchanged, the join 18% slower)
+#endif
+constexpr int kRowPad = TJ_ROW_PAD;
+__host__ __device__ __forceinline__ int row_words(int nb) { return (nb + kRowPad - 1) / kRowPad * kRowPad; }
 
 struct WordsIn {
   const int32_t* nobj;
@@ -794,7 +915,7 @@ struct WordsIn {
   const uint8_t* active;
   __device__ int64_t operator()(int64_t r) const {
     const int64_t no = nobj[r], ni = nisq[r];
-    return (no > 0 && ni > 0 && leaf_on(active, r)) ? ni * ((no + 31) / 32) : 0;
+    return (no > 0 && ni > 0 && leaf_on(active, r)) ? ni * row_words((int)((no + 31) / 32)) : 0;
   }
 };
 struct UnitsIn {
@@ -909,8 +1030,10 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
     const int P = min(nobj - b0 * 32, nbt * 32);
     const int32_t ob = li.x + b0 * 32;
     const int64_t woff = d.leaf_woff[r];
+    const int nbp = row_words(nb);  // row stride (sector-padded)
     const int32_t sbase = li.z;
     const bool table = nisq >= kTableMinQ;
+    const int nbs = kJoinTPS ? (nbt + 1) & ~1 : nbt;  // table row stride (even: paired 8-byte lookups)
     // ---- stage the tile's objects -------------------------------------------
     for (int i = tid; i < nbt * 32; i += kJT) {
       double x = kNaN, y = kNaN;
@@ -934,27 +1057,27 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       scx = sxm * f;
       scy = sym * f;
       static_assert((2 * kRows) % 4 == 0, "table rows must allow 16-byte zeroing");
-      for (int i = tid; i < 2 * kRows * nbt / 4; i += kJT) reinterpret_cast<uint4*>(S.tab)[i] = make_uint4(0u, 0u, 0u, 0u);
+      for (int i = tid; i < 2 * kRows * nbs / 4; i += kJT) reinterpret_cast<uint4*>(S.tab)[i] = make_uint4(0u, 0u, 0u, 0u);
       __syncthreads();
       // bucket scatter: Bk[axis][k][b] |= bit of each object
       for (int i = tid; i < P; i += kJT) {
         const int kx = bucket(S.ox[i], bx, scx), ky = bucket(S.oy[i], by, scy);
         const uint32_t bit = 1u << (i & 31);
-        atomicOr(&S.tab[kx * nbt + (i >> 5)], bit);
-        atomicOr(&S.tab[(kRows + ky) * nbt + (i >> 5)], bit);
+        atomicOr(&S.tab[kx * nbs + (i >> 5)], bit);
+        atomicOr(&S.tab[(kRows + ky) * nbs + (i >> 5)], bit);
       }
       __syncthreads();
       // exclusive prefix-OR down every (axis, block) column: Pre_k = OR_{k' < k} Bk_k'
       constexpr int kPer = (kRows + 31) / 32;
       for (int task = wp; task < 2 * nbt; task += kJW) {
         const int ax = task >= nbt ? 1 : 0, b = task - ax * nbt;
-        uint32_t* col = S.tab + ax * kRows * nbt + b;
+        uint32_t* col = S.tab + ax * kRows * nbs + b;
         uint32_t v[kPer];
         uint32_t acc = 0;
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
           const int k = lane * kPer + j;
-          v[j] = k < kRows ? col[k * nbt] : 0u;
+          v[j] = k < kRows ? col[k * nbs] : 0u;
           acc |= v[j];
         }
         uint32_t pre = acc;  // inclusive OR-scan of the lane totals
@@ -968,7 +1091,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
 #pragma unroll
         for (int j = 0; j < kPer; ++j) {
           const int k = lane * kPer + j;
-          if (k < kRows) col[k * nbt] = run;
+          if (k < kRows) col[k * nbs] = run;
           run |= v[j];
         }
       }
@@ -976,6 +1099,52 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
     __syncthreads();
     const uint32_t divm = (65536u + (uint32_t)nbt - 1u) / (uint32_t)nbt;  // it / nbt for it < 65536 / 16
     const Rect4* erect = d.erect + sbase;
+    if (kJoinTPS && table) {
+      // ---- one thread per subquery: its row of the tile, two blocks per step (paired 8-byte table
+      // lookups of rows k and k + 1), its popcount in a register; no shared-memory staging, no atomics
+      const uint2* TX = reinterpret_cast<const uint2*>(S.tab);
+      const uint2* TY = reinterpret_cast<const uint2*>(S.tab + kRows * nbs);
+      const int hs = nbs >> 1;
+      const bool last_tile = b0 + nbt == nb;
+      for (int t = tid; t < nisq; t += kJT) {
+        const Rect4 R = erect[t];
+        const int kxa = bucket(R.xa, bx, scx) * hs, kxb = bucket(R.xb, bx, scx) * hs;
+        const int kya = bucket(R.ya, by, scy) * hs, kyb = bucket(R.yb, by, scy) * hs;
+        uint32_t* orow = d.bitmap + woff + (int64_t)t * nbp + b0;
+        int cnt = 0;
+        for (int b2 = 0; b2 < hs; ++b2) {
+          const uint2 xa0 = TX[kxa + b2], xa1 = TX[kxa + hs + b2], xb0 = TX[kxb + b2], xb1 = TX[kxb + hs + b2];
+          const uint2 ya0 = TY[kya + b2], ya1 = TY[kya + hs + b2], yb0 = TY[kyb + b2], yb1 = TY[kyb + hs + b2];
+          uint32_t D[2], A[2];
+          D[0] = (xb0.x & ~xa1.x) & (yb0.x & ~ya1.x);
+          D[1] = (xb0.y & ~xa1.y) & (yb0.y & ~ya1.y);
+          A[0] = (xb1.x & ~xa0.x) & (yb1.x & ~ya0.x) & ~D[0];
+          A[1] = (xb1.y & ~xa0.y) & (yb1.y & ~ya0.y) & ~D[1];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int b = 2 * b2 + e;
+            uint32_t a = A[e];
+            while (a) {
+              const int bit = __ffs(a) - 1;
+              a &= a - 1;
+              const int o = (b << 5) + bit;
+              if (in_rect(S.ox[o], S.oy[o], R)) D[e] |= 1u << bit;
+            }
+            if (b < nbt) {
+              orow[b] = D[e];
+              cnt += __popc(D[e]);
+            }
+          }
+        }
+        if (kRowPad > 1 && last_tile)  // the row's pad words: whole-sector stores
+          for (int b = nb - b0; b < nbp - b0; ++b) orow[b] = 0u;
+        int32_t* ec = d.ecount + sbase + t;
+        if (n_ot == 1) *ec = cnt;
+        else if (cnt) atomicAdd(ec, cnt);
+      }
+      __syncthreads();  // the tile's shared memory is reused by the next unit
+      continue;
+    }
     // ---- subquery chunks ------------------------------------------------------
     for (int c0 = 0; c0 < nisq; c0 += kQC) {
       const int nq = min(kQC, nisq - c0);
@@ -988,18 +1157,18 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
         }
       }
       __syncthreads();
-      uint32_t* out = d.bitmap + woff + (int64_t)c0 * nb + b0;
+      uint32_t* out = d.bitmap + woff + (int64_t)c0 * nbp + b0;
       if (table) {
         const uint32_t* TX = S.tab;
-        const uint32_t* TY = S.tab + kRows * nbt;
+        const uint32_t* TY = S.tab + kRows * nbs;
         const int items = nq * nbt;
         for (int it = tid; it < items; it += kJT) {
           const int s = (int)(((uint32_t)it * divm) >> 16), b = it - s * nbt;
           const ushort4 k4 = S.kb[s];
-          const uint32_t xa0 = TX[k4.x * nbt + b], xa1 = TX[(k4.x + 1) * nbt + b];
-          const uint32_t xb0 = TX[k4.y * nbt + b], xb1 = TX[(k4.y + 1) * nbt + b];
-          const uint32_t ya0 = TY[k4.z * nbt + b], ya1 = TY[(k4.z + 1) * nbt + b];
-          const uint32_t yb0 = TY[k4.w * nbt + b], yb1 = TY[(k4.w + 1) * nbt + b];
+          const uint32_t xa0 = TX[k4.x * nbs + b], xa1 = TX[(k4.x + 1) * nbs + b];
+          const uint32_t xb0 = TX[k4.y * nbs + b], xb1 = TX[(k4.y + 1) * nbs + b];
+          const uint32_t ya0 = TY[k4.z * nbs + b], ya1 = TY[(k4.z + 1) * nbs + b];
+          const uint32_t yb0 = TY[k4.w * nbs + b], yb1 = TY[(k4.w + 1) * nbs + b];
           uint32_t D = (xb0 & ~xa1) & (yb0 & ~ya1);
           uint32_t A = (xb1 & ~xa0) & (yb1 & ~ya0) & ~D;
           if (A) {
@@ -1011,7 +1180,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
               if (in_rect(S.ox[o], S.oy[o], R)) D |= 1u << bit;
             } while (A);
           }
-          out[(int64_t)s * nb + b] = D;
+          out[(int64_t)s * nbp + b] = D;
           if (D) atomicAdd(&S.cnt[s], __popc(D));
         }
       } else {
@@ -1031,9 +1200,16 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
             if (in_rect(S.ox[o], S.oy[o], R)) w |= 1u << k;
           }
           if (s < nq) {
-            out[(int64_t)s * nb + b] = w;
+            out[(int64_t)s * nbp + b] = w;
             if (w) atomicAdd(&S.cnt[s], __popc(w));
           }
+        }
+      }
+      if (kRowPad > 1 && b0 + nbt == nb && nbp > nb) {  // the row's pad words: whole-sector stores
+        const int np = nbp - nb;
+        for (int it = tid; it < nq * np; it += kJT) {
+          const int s = it / np;
+          out[(int64_t)s * nbp + (nb - b0) + (it - s * np)] = 0u;
         }
       }
       __syncthreads();
@@ -1242,19 +1418,35 @@ __device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, in
 // by the whole warp and rank-merged there (<= 32 runs); lists that need a
 // sort by id (ids not monotone) or oversized lists of more than 32 runs go to
 // the CTA-wide k_merge_big.
+// Id modes of the decode (one instantiation each; the two that do not match
+// the tick's ids return at once): merge keys and ids of a leaf position are
+//  kIdsRows:   key = input row, id = the row (ids are the rows);
+//  kIdsKeyed:  key = the block's id offset (keyed lists), id = id_min + key;
+//  kIdsLookup: key = input row, id = ids[row] (lists sorted per query by
+//              k_merge_big unless the ids increase with the row).
+enum { kIdsRows = 0, kIdsKeyed = 1, kIdsLookup = 2 };
+__device__ __forceinline__ int id_mode_of(const DevHdr* h) {
+  return !h->not_identity ? kIdsRows : (h->key_mode ? kIdsKeyed : kIdsLookup);
+}
+
+template <int kMode>
 __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const Dev d) {
   DevHdr* h = d.h;
-  if (h->abort) return;
+  if (h->abort || id_mode_of(h) != kMode) return;
   __shared__ int32_t sbuf[kDQWarps][kDQStage];
-  const bool mono = !h->not_monotone, ident = !h->not_identity;
+  const bool mono = kMode != kIdsLookup || !h->not_monotone;
   const int64_t m = h->m;
   const int lane = lane_id(), wp = threadIdx.x >> 5;
   const int64_t nwarp = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t* __restrict__ ids = d.ids;
-  const int32_t* __restrict__ sidx = d.sidx;
+  // leaf position -> merge key
+  const int32_t* __restrict__ sidx = kMode == kIdsKeyed ? reinterpret_cast<const int32_t*>(d.loff) : d.sidx;
   int32_t* sa = sbuf[wp];
   int bad = 0;
-  auto idof = [&](int32_t row) -> int64_t { return ident ? (int64_t)row : ids[row]; };
+  auto idof = [&](int32_t v) -> int64_t {
+    if constexpr (kMode == kIdsRows) return (int64_t)v;
+    else if constexpr (kMode == kIdsKeyed) return h->id_min + (int64_t)(uint32_t)v;
+    else return d.ids[v];
+  };
   for (int64_t q0 = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; q0 < m; q0 += nwarp * 32) {
     const int64_t ql = q0 + lane;
     int k = 0;
@@ -1294,7 +1486,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
           const int nbw = (nobj + 31) >> 5;
           const int row = le.y - li.z;
           const bool cov = row >= li.w;
-          const uint32_t* wpt = cov ? nullptr : d.bitmap + d.leaf_woff[leaf] + (int64_t)row * nbw;
+          const uint32_t* wpt = cov ? nullptr : d.bitmap + d.leaf_woff[leaf] + (int64_t)row * row_words(nbw);
           const uint32_t tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
           int64_t got = 0;
           for (int b0 = 0; b0 < nbw; b0 += 32) {
@@ -1344,12 +1536,13 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
           obase = li.x;
           nbw = (nobj + 31) >> 5;
           tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
-          wof = row >= li.w ? -1 : d.leaf_woff[leaf] + (int64_t)row * nbw;
+          wof = row >= li.w ? -1 : d.leaf_woff[leaf] + (int64_t)row * row_words(nbw);
         }
+        const int pos0 = (int)(d.slot_off[c0] - base);  // output offset of the chunk's first run
         const int winc = warp_incl_scan(nbw);
         const int wexc = winc - nbw;
         const int TW = __shfl_sync(0xffffffffu, winc, 31);
-        int64_t pos = d.slot_off[c0] - base;  // output offset of the chunk's first run
+        int pos = 0;  // prefix of the flattened popcounts
         for (int t0 = 0; t0 < TW; t0 += 32 * TJ_DQ_WPL) {
           // TJ_DQ_WPL words per lane per step: independent loads in flight (8 measured slower: registers)
           uint32_t w[TJ_DQ_WPL];
@@ -1378,7 +1571,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
             uint32_t x = w[u];
             const int c = __popc(x);
             const int inc = warp_incl_scan(c);
-            int p = (int)pos + (inc - c);
+            int p = pos0 + pos + (inc - c);
             while (x) {
               const int bit = __ffs(x) - 1;
               x &= x - 1;
@@ -1389,7 +1582,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         }
         // the runs' popcounts must add up to the counts the offsets came from
         const int32_t cend = c0 + 32 < shi ? c0 + 32 : shi;
-        bad |= (lane == 0) && (pos != d.slot_off[cend] - base);  // CountMismatch (bitmap.py:131-132)
+        bad |= (lane == 0) && (pos0 + pos != d.slot_off[cend] - base);  // CountMismatch (bitmap.py:131-132)
       }
       __syncwarp();
       // ---- B: leaf positions -> input rows (independent loads, 4 in flight per lane)

@@ -293,7 +293,9 @@ k_radix_upsweep(KeySrc keys, const int64_t* n_ptr, const DevHdr* h, int shift,
   }
 }
 
-// vals_in == nullptr: the value of item i is i (first pass over input rows).
+// vals_in == nullptr: the value of item i is i (first pass over input rows);
+// gate: vals_in is used only when the tick's objects enter in id order
+// (DevHdr::key_sorted), else item i's value is i.
 // keys_out == nullptr: the keys are not written (last pass).
 // Payload (x, y) doubles (xin != nullptr): item i's payload is xin[i], yin[i]
 // (the input arrays on the first pass, the previous pass's output after);
@@ -318,8 +320,9 @@ __global__ void __launch_bounds__(kRadixThreads, TJ_RADIX_MINB)
 k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
                   const double* __restrict__ xin, const double* __restrict__ yin, double* __restrict__ xout,
                   double* __restrict__ yout, const int64_t* n_ptr, const DevHdr* h, int shift,
-                  const int64_t* offs /* [digits][G] exclusive */) {
+                  const int64_t* offs /* [digits][G] exclusive */, int gate) {
   if (h->abort) return;
+  if (gate && !h->key_sorted) vals_in = nullptr;
   extern __shared__ __align__(16) unsigned char radix_smem[];
   RadixSmem& S = *reinterpret_cast<RadixSmem*>(radix_smem);
   double* sx = XY ? reinterpret_cast<RadixSmemXY*>(radix_smem)->sx : nullptr;

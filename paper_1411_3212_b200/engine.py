@@ -136,6 +136,10 @@ class TickStats:
     l_deep: int = 0
     rebuilt: bool = True  # rebuild="adaptive": False when the previous tick's index was reused
     device_ms: dict = field(default_factory=dict)
+    # how the device put result lists in id order: "monotone" (ids increase with the input row),
+    # "keyed" (leaf blocks in id order with 32-bit id offsets), "sorted" (per-list sorts;
+    # see tj_stats.id_order)
+    id_order: str = "monotone"
 
 
 @dataclass
@@ -162,6 +166,7 @@ def _fill_stats(stats: TickStats, st: "_native.TjStats") -> None:
     stats.n_leaves = int(st.n_leaves)
     stats.l_deep = int(st.l_deep)
     stats.rebuilt = bool(st.rebuilt)
+    stats.id_order = ("monotone", "keyed", "sorted")[int(st.id_order)]
     if stats.results_total:
         stats.covering_result_fraction = stats.covering_results / stats.results_total
     a = int(st.active_cells)

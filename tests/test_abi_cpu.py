@@ -41,7 +41,7 @@ def test_library_loads_and_exports_every_symbol():
     for s in declared_symbols():
         assert hasattr(lib, s), s
     assert set(_native.EXPORTED) == set(declared_symbols())
-    assert lib.tj_abi_version() == 3
+    assert lib.tj_abi_version() == 4
     # loading the .so must not need a GPU; creating a context must fail loudly without one
     n = ctypes.c_int(-1)
     lib.tj_device_count(ctypes.byref(n))
