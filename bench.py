@@ -398,35 +398,32 @@ def run_reference_port(args):
 
 
 class Shard:
-    """This rank's slice of one tick (1/G of the updates and queries, device
-    resident) and the all-gathered full tick it ingests each step (SURVEY.md
-    §8e: NCCL all-gather of the position updates over NVLink, then every rank
-    builds the same index and joins only its contiguous leaf range)."""
+    """This rank's slice of one tick: a contiguous 1/G of the objects and of the queries
+    (device resident, or pinned host memory for the end-to-end leg).  tj_tick_sharded
+    gathers the slices into the full tick on every rank (NCCL), runs the rank's Morton range
+    of leaves, routes every query's partial lists to its home rank and merges them there."""
 
     def __init__(self, tick, rank, world, dev, pinned=False):
+        import numpy as np
         import torch
 
-        self.n, self.m = int(tick.n_objects), int(tick.n_queries)
-        self.cn, self.cm = -(-self.n // world), -(-self.m // world)
-        self.world = world
+        n, m = int(tick.n_objects), int(tick.n_queries)
+        o0, o1 = rank * n // world, (rank + 1) * n // world
+        q0, q1 = rank * m // world, (rank + 1) * m // world
+        self.n, self.m, self.n_total, self.m_total = o1 - o0, q1 - q0, n, m
 
-        def part(a, c):
-            t = torch.zeros(c, dtype=torch.from_numpy(a[:0]).dtype)
-            lo = min(rank * c, len(a))
-            hi = min(lo + c, len(a))
-            t[: hi - lo] = torch.from_numpy(a[lo:hi])
+        def part(a, lo, hi):
+            t = torch.from_numpy(np.ascontiguousarray(a[lo:hi]))
             return t.pin_memory() if pinned else t.to(dev)
 
-        cols = (tick.ids, tick.xs, tick.ys, tick.qids, tick.qxa, tick.qya, tick.qxb, tick.qyb)
-        self.mine = [part(a, self.cn if i < 3 else self.cm) for i, a in enumerate(cols)]
-        self.full = [torch.empty(world * (self.cn if i < 3 else self.cm), dtype=t.dtype, device=dev)
-                     for i, t in enumerate(self.mine)]
+        self.cols = [part(a, o0, o1) for a in (tick.ids, tick.xs, tick.ys)] + \
+                    [part(a, q0, q1) for a in (tick.qxa, tick.qya, tick.qxb, tick.qyb)]
 
-    def gather(self, dev_slices=None):
-        import torch.distributed as dist
+    def ptrs(self):
+        return [x.data_ptr() if x.numel() else 0 for x in self.cols]
 
-        for f, p in zip(self.full, dev_slices or self.mine):
-            dist.all_gather_into_tensor(f, p)
+    def nbytes(self):
+        return sum(x.numel() * x.element_size() for x in self.cols)
 
 
 def run_ours(args):
@@ -460,24 +457,28 @@ def run_ours(args):
     def new_ctx():
         return _native.NativeContext(384, 12, True, 0, local, sf)
     stream = torch.cuda.ExternalStream(ctx.stream(), device=dev)
-    if sharded:
-        ctx.set_shard(rank, world)
+    if sharded:  # NCCL communicator inside the library; rank 0's unique id shared over torch.distributed
+        import torch.distributed as dist
+
+        uid = [_native.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        ctx.comm_init(uid[0], rank, world)
         shards = [Shard(t, rank, world, dev) for t in ticks]
-    else:
-        dticks = [[torch.from_numpy(a).to(dev) for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb, t.qyb)]
-                  for t in ticks]
+    dticks = [[torch.from_numpy(a).to(dev) for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb, t.qyb)]
+              for t in ticks] if (not sharded or rank == 0) else None
 
     def tick_dev(k):
-        if sharded:
+        if sharded:  # this rank's slice in, the complete lists of this rank's queries out
             sh = shards[k % pool]
-            with torch.cuda.stream(stream):  # the collectives order before the tick on the library stream
-                sh.gather()
-            a, n, m = sh.full, sh.n, sh.m
-        else:
-            a = dticks[k % pool]
-            n, m = a[0].numel(), a[3].numel()
-        return ctx.tick_ptrs(n, *(x.data_ptr() for x in a[:3]), m, *(x.data_ptr() for x in a[3:]),
-                             _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
+            p = sh.ptrs()
+            out, st = ctx.tick_sharded_ptrs(sh.n, *p[:3], sh.m, *p[3:], _native.TJ_MEM_DEVICE,
+                                            _native.TJ_MEM_DEVICE)
+            return out, st, sh.m_total
+        a = dticks[k % pool]
+        n, m = a[0].numel(), a[3].numel()
+        out, st = ctx.tick_ptrs(n, *(x.data_ptr() for x in a[:3]), m, *(x.data_ptr() for x in a[3:]),
+                                _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
+        return out, st, m
 
     # the clock sampler starts before the warm-up (its start-up otherwise leaves the GPU idle,
     # clocks ramp down, and the first timed tick pays the ramp); samples are kept from the
@@ -498,10 +499,10 @@ def run_ours(args):
     stats = []
     queries = 0
     for k in range(args.steps):
-        _, st = tick_dev(args.warmup + k)
+        _, st, mq = tick_dev(args.warmup + k)
         ev[k + 1].record(stream)
         stats.append(st)
-        queries += int(st.n_queries)  # every rank sees the whole tick: count once
+        queries += mq  # whole-job queries of the step (every rank's queries, each answered completely)
     torch.cuda.synchronize()
     gc.enable()
     clk = clocks.stop()
@@ -539,23 +540,22 @@ def run_ours(args):
     # index build (K0 + K1) against its compulsory bytes 44n + 4Z + 12L.  In the
     # tick the object sort overlaps the query scatter on a side stream, so K1 alone is timed on a
     # second context with the sort kept on the main stream (TJ_SERIAL_SORT=1), a few ticks
-    os.environ["TJ_SERIAL_SORT"] = "1"
-    sctx = new_ctx()
-    os.environ.pop("TJ_SERIAL_SORT")
-    sst = []
-    for k in range(4):
-        a_ = shards[k % pool].full if sharded else dticks[k % pool]
-        n_, m_ = (shards[k % pool].n, shards[k % pool].m) if sharded else (a_[0].numel(), a_[3].numel())
-        if sharded:
-            with torch.cuda.stream(stream):
-                shards[k % pool].gather()
-            torch.cuda.synchronize()
-        _, s_ = sctx.tick_ptrs(n_, *(x.data_ptr() for x in a_[:3]), m_, *(x.data_ptr() for x in a_[3:]),
-                               _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
-        sst.append(s_)
-    sctx.close()
-    build_ms = statistics.mean(s_.t_build_ms + s_.t_sort_ms for s_ in sst[1:])
-    build_bytes = 44 * n + 4 * (4 ** int(st0.l_deep)) + 12 * int(st0.n_leaves)
+    # (rank 0 alone, on the full tick, when sharded)
+    build_ms = None
+    if dticks is not None:
+        os.environ["TJ_SERIAL_SORT"] = "1"
+        sctx = new_ctx()
+        os.environ.pop("TJ_SERIAL_SORT")
+        sst = []
+        for k in range(4):
+            a_ = dticks[k % pool]
+            _, s_ = sctx.tick_ptrs(a_[0].numel(), *(x.data_ptr() for x in a_[:3]), a_[3].numel(),
+                                   *(x.data_ptr() for x in a_[3:]), _native.TJ_MEM_DEVICE, _native.TJ_MEM_DEVICE)
+            sst.append(s_)
+        sctx.close()
+        build_ms = statistics.mean(s_.t_build_ms + s_.t_sort_ms for s_ in sst[1:])
+        st_full = sst[-1]
+        build_bytes = 44 * n + 4 * (4 ** int(st_full.l_deep)) + 12 * int(st_full.n_leaves)
 
     # end to end through the C ABI with pinned host buffers: H2D inputs + D2H CSR per step.
     # tj_tick uploads ids, x, y and the four rect columns; issuer ids stay on the host
@@ -570,18 +570,14 @@ def run_ours(args):
         idb, idbs = 8, set()
         if sharded:
             hsh = [Shard(t, rank, world, dev, pinned=True) for t in ticks]
-            dsl = [[torch.empty_like(x, device=dev) for x in hsh[0].mine] for _ in range(1)][0]
 
-            def tick_host(k):
+            def tick_host(k):  # this rank's slice from pinned host memory, its queries' lists back to it
                 sh = hsh[k % pool]
-                with torch.cuda.stream(stream):
-                    for d_, h_ in zip(dsl, sh.mine):
-                        d_.copy_(h_, non_blocking=True)
-                    sh.gather(dsl)
-                a = sh.full
-                return ctx.tick_ptrs(sh.n, *(x.data_ptr() for x in a[:3]), sh.m, *(x.data_ptr() for x in a[3:]),
-                                     _native.TJ_MEM_DEVICE, _native.TJ_MEM_HOST | out_flag), \
-                    sum(x.numel() * x.element_size() for x in sh.mine)  # all 8 columns are copied and gathered
+                p = sh.ptrs()
+                out, st = ctx.tick_sharded_ptrs(sh.n, *p[:3], sh.m, *p[3:], _native.TJ_MEM_HOST,
+                                                _native.TJ_MEM_HOST | out_flag)
+                st.n_queries = sh.m_total  # whole-job queries of the step
+                return (out, st), sh.nbytes()
         else:
             hticks = [[torch.from_numpy(a).pin_memory() for a in (t.ids, t.xs, t.ys, t.qids, t.qxa, t.qya, t.qxb,
                                                                     t.qyb)] for t in ticks]
@@ -661,7 +657,7 @@ def run_ours(args):
                "id_bytes": idb,
                "api": ("tj_tick (C ABI): pinned host inputs -> device, results CSR -> pinned host"
                        + (" (TJ_OUT_IDS32: int32 ids and offsets, every id and offset < 2^31)" if idb == 4 else " (int64 ids)")
-                       + ("; per rank: H2D of its 1/G slice, NCCL all-gather, D2H of its leaf-range CSR"
+                       + ("; per rank (tj_tick_sharded): H2D of its 1/G slice, NCCL gather, its leaf range, partial lists routed to home ranks and merged, D2H of the complete CSR of its own queries"
                           if sharded else ""))}
 
     cpu = None
@@ -683,8 +679,11 @@ def run_ours(args):
                               "object_ids": ("a random permutation of 0..n-1 per tick" if args.shuffle_ids
                                              else "arange(n)"),
                               "id_order": ("monotone", "keyed", "sorted")[int(st0.id_order)],
-                              "parallelism": (f"leaf-range sharding over {world} GPUs: NCCL all-gather of each "
-                                              f"tick's updates, per-rank join/decode of its Morton leaf range"
+                              "parallelism": (f"leaf-range sharding over {world} GPUs (tj_tick_sharded): NCCL "
+                                              f"gather of the ranks' slices, per-rank join/decode of its Morton "
+                                              f"leaf range, partial lists routed to the queries' home ranks "
+                                              f"(NCCL send/recv) and merged there on the device; every query's "
+                                              f"complete list inside the timed region"
                                               if sharded else "1 GPU")},
             "roofline": {"bound": "hbm", "achieved": dec_bytes / (dec_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": dec_bytes / (dec_ms / 1e3) / 1e9 / peak, "traffic": dec_traffic,

@@ -208,6 +208,25 @@ int tj_get_staging_flushes(tj_ctx* ctx, int32_t staging_capacity, int64_t* flush
  * their per-query merge is the full result.  nranks == 1 (default): off. */
 int tj_set_shard(tj_ctx* ctx, int32_t rank, int32_t nranks);
 
+/* ---- multi-GPU data plane (one process or thread per GPU) ---------------
+ * tj_tick_sharded takes this rank's slice of the tick's objects and queries
+ * (any sizes per rank) and returns the complete result lists of this rank's
+ * queries: the slices are gathered into the full tick on every rank, the
+ * tick runs on the rank's contiguous Morton range of leaves (tj_set_shard),
+ * each query's partial lists go to its home rank (all-to-all), and the home
+ * rank merges them on the device.  Concatenating the ranks' outputs in rank
+ * order gives tj_tick's output for the concatenated slices.  Transports:
+ * NCCL (the caller shares one tj_nccl_unique_id among the ranks, e.g. over
+ * its own bootstrap; libnccl.so.2 is loaded at run time) or an in-process
+ * group of contexts driven from one thread each. */
+typedef struct tj_group tj_group;
+int tj_nccl_unique_id(void* id, int32_t bytes); /* bytes >= 128 (ncclUniqueId) */
+int tj_comm_init(tj_ctx* ctx, const void* nccl_unique_id, int32_t rank, int32_t nranks);
+int tj_group_create(int32_t nranks, tj_group** out);
+int tj_group_destroy(tj_group* group);
+int tj_comm_init_local(tj_ctx* ctx, tj_group* group, int32_t rank);
+int tj_tick_sharded(tj_ctx* ctx, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats);
+
 /* The context's CUDA stream (cudaStream_t), for callers that time or order
  * work against the tick with their own events. */
 int tj_get_stream(tj_ctx* ctx, void** stream);

@@ -78,6 +78,7 @@ EXPORTED = (
     "tj_abi_version", "tj_device_count", "tj_create", "tj_destroy", "tj_last_error", "tj_tick",
     "tj_get_index", "tj_get_object_cells", "tj_get_subqueries", "tj_get_directory", "tj_get_bitmaps",
     "tj_get_imbalance", "tj_get_occupancy", "tj_get_staging_flushes", "tj_set_shard", "tj_get_stream", "tj_host_alloc", "tj_host_free",
+    "tj_nccl_unique_id", "tj_comm_init", "tj_group_create", "tj_group_destroy", "tj_comm_init_local", "tj_tick_sharded",
 )
 
 _lib: Optional[ctypes.CDLL] = None
@@ -112,6 +113,12 @@ def load_library() -> ctypes.CDLL:
     lib.tj_set_shard.argtypes = [c_void_p, c_int32, c_int32]
     lib.tj_host_alloc.argtypes = [c_int64, POINTER(c_void_p)]
     lib.tj_host_free.argtypes = [c_void_p]
+    lib.tj_nccl_unique_id.argtypes = [c_void_p, c_int32]
+    lib.tj_comm_init.argtypes = [c_void_p, c_void_p, c_int32, c_int32]
+    lib.tj_group_create.argtypes = [c_int32, POINTER(c_void_p)]
+    lib.tj_group_destroy.argtypes = [c_void_p]
+    lib.tj_comm_init_local.argtypes = [c_void_p, c_void_p, c_int32]
+    lib.tj_tick_sharded.argtypes = [c_void_p, POINTER(TjTickIn), POINTER(TjTickOut), POINTER(TjStats)]
     _lib = lib
     return lib
 
@@ -120,6 +127,32 @@ def device_count() -> int:
     n = c_int(0)
     load_library().tj_device_count(ctypes.byref(n))
     return n.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for tj_comm_init; rank 0 makes it, the caller shares it."""
+    lib = load_library()
+    buf = ctypes.create_string_buffer(128)
+    rc = lib.tj_nccl_unique_id(buf, 128)
+    if rc != 0:
+        raise _ERRORS.get(rc, errors.DeviceError)(lib.tj_last_error(None).decode(errors="replace"))
+    return buf.raw
+
+
+class LocalGroup:
+    """In-process group of G contexts (one host thread each) for tj_tick_sharded without NCCL."""
+
+    def __init__(self, nranks: int):
+        self.lib = load_library()
+        self.h = c_void_p()
+        if self.lib.tj_group_create(nranks, ctypes.byref(self.h)) != 0:
+            raise errors.DeviceError("tj_group_create failed")
+        self.nranks = nranks
+
+    def close(self) -> None:
+        if getattr(self, "h", None):
+            self.lib.tj_group_destroy(self.h)
+            self.h = None
 
 
 def _ptr(a: np.ndarray) -> int:
@@ -191,6 +224,43 @@ class NativeContext:
         tout = TjTickOut()
         st = TjStats()
         self._check(self.lib.tj_tick(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
+        return tout, st
+
+    def comm_init(self, unique_id: bytes, rank: int, nranks: int) -> None:
+        """NCCL communicator for tj_tick_sharded (collective: every rank calls it)."""
+        buf = ctypes.create_string_buffer(bytes(unique_id), 128)
+        self._check(self.lib.tj_comm_init(self.h, buf, rank, nranks))
+
+    def comm_init_local(self, group: "LocalGroup", rank: int) -> None:
+        self._check(self.lib.tj_comm_init_local(self.h, group.h, rank))
+
+    def tick_sharded_host(self, ids, xs, ys, qxa, qya, qxb, qyb, ids32: bool = False):
+        """This rank's slice in (host arrays), the complete CSR of this rank's queries out."""
+        arrs = [np.ascontiguousarray(ids, np.int64), np.ascontiguousarray(xs, np.float64),
+                np.ascontiguousarray(ys, np.float64), np.ascontiguousarray(qxa, np.float64),
+                np.ascontiguousarray(qya, np.float64), np.ascontiguousarray(qxb, np.float64),
+                np.ascontiguousarray(qyb, np.float64)]
+        tin = TjTickIn(len(arrs[0]), _ptr(arrs[0]), _ptr(arrs[1]), _ptr(arrs[2]), len(arrs[3]), 0,
+                       _ptr(arrs[3]), _ptr(arrs[4]), _ptr(arrs[5]), _ptr(arrs[6]),
+                       TJ_MEM_HOST, TJ_MEM_HOST | (TJ_OUT_IDS32 if ids32 else 0))
+        tout = TjTickOut()
+        st = TjStats()
+        self._check(self.lib.tj_tick_sharded(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
+        m = tout.n_q
+        osrc, otyp = (tout.offsets32, c_int32) if tout.offset_bytes == 4 else (tout.offsets, c_int64)
+        offs = np.ctypeslib.as_array(ctypes.cast(osrc, POINTER(otyp)), shape=(m + 1,)).copy()
+        res = np.zeros(0, np.int32 if tout.id_bytes == 4 else np.int64)
+        if tout.n_results:
+            src, typ = (tout.ids32, c_int32) if tout.id_bytes == 4 else (tout.ids, c_int64)
+            res = np.ctypeslib.as_array(ctypes.cast(src, POINTER(typ)), shape=(tout.n_results,)).copy()
+        return offs, res, st
+
+    def tick_sharded_ptrs(self, n, ids, xs, ys, m, qxa, qya, qxb, qyb, mem: int, out_mem: int):
+        """Raw-pointer sharded tick (device tensors or pinned host buffers); returns (TjTickOut, TjStats)."""
+        tin = TjTickIn(n, ids, xs, ys, m, 0, qxa, qya, qxb, qyb, mem, out_mem)
+        tout = TjTickOut()
+        st = TjStats()
+        self._check(self.lib.tj_tick_sharded(self.h, ctypes.byref(tin), ctypes.byref(tout), ctypes.byref(st)))
         return tout, st
 
     def set_shard(self, rank: int, nranks: int) -> None:

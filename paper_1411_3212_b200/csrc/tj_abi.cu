@@ -27,6 +27,8 @@ struct DBuf {
 
 }  // namespace
 
+struct Transport;  // multi-GPU exchange (tj_shard.cuh)
+
 // One instantiated CUDA graph of the tick's launch sequence.  Every size
 // after the index build lives on the device, so a graph is valid for any
 // tick with the same host-side launch shape: input/arena pointers (all in
@@ -66,7 +68,7 @@ struct tj_ctx {
   // index
   DBuf linfo, pyr, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
-  DBuf qpos, qwin, crect, nsub, qsbase, biglist, leafcnt;
+  DBuf qpos, qwin, nsub, qsbase, biglist, leafcnt;
   // subqueries
   DBuf sqle, sqcount, ecount, erect, slotoff, leafcur, unitleaf;
   // join / outputs
@@ -109,6 +111,9 @@ struct tj_ctx {
   bool use_graphs = true;
   std::vector<TickGraph> graphs;
   DBuf lactive, lwpre;
+  // multi-GPU data plane (tj_comm_init / tj_comm_init_local, tj_tick_sharded)
+  Transport* comm = nullptr;
+  DBuf pcnt, rcnt, sstart, moff, sconst, rids, mids, mscratch;
 };
 
 namespace {
@@ -227,7 +232,6 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(qsbase, m * 4);
   ENS(qpos, m * sizeof(int4));
   ENS(qwin, m * sizeof(int4));
-  ENS(crect, m * sizeof(Rect4));
   ENS(biglist, m * 4);
   ENS(outoff, (m + 1) * 8);
   ENS(partial, 1024 * 8);
@@ -303,7 +307,6 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.qsbase = P<int32_t>(c->qsbase);
   d.qpos = P<int4>(c->qpos);
   d.qwin = P<int4>(c->qwin);
-  d.crect = P<Rect4>(c->crect);
   d.sq_le = P<int2>(c->sqle);
   d.sq_count = P<int32_t>(c->sqcount);
   d.erect = P<Rect4>(c->erect);
@@ -655,176 +658,14 @@ int run_tick(tj_ctx* c, int64_t* launches) {
   return check_launch(c);
 }
 
-}  // namespace
-
-// ===========================================================================
-// C ABI
-// ===========================================================================
-extern "C" {
-
-int tj_abi_version(void) { return TJ_ABI_VERSION; }
-
-int tj_device_count(int* count) {
-  int n = 0;
-  cudaError_t e = cudaGetDeviceCount(&n);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    n = 0;
-  }
-  if (count) *count = n;
-  return TJ_OK;
-}
-
-const char* tj_last_error(const tj_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
-
-int tj_create(const tj_config* cfg, tj_ctx** out) {
-  tj_ctx* c = nullptr;
-  if (!cfg || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
-  // MethodConfig.validate (engine.py:73-88)
-  if (cfg->split_factor < 0) return fail(c, TJ_E_BAD_CONFIG, "split_factor must be >= 1");
-  if (cfg->split_factor > (1 << kMaxLevel))
-    return fail(c, TJ_E_BAD_CONFIG, "split factors above 4096 are not supported on the device path");
-  if (cfg->split_factor == 0) {
-    if (cfg->th_quad < 1) return fail(c, TJ_E_BAD_CONFIG, "th_quad must be >= 1");
-    if (cfg->l_max < 1 || cfg->l_max > kMaxLevel) return fail(c, TJ_E_BAD_CONFIG, "l_max must be in [1, 12]");
-  }
-  if (cfg->rebuild != TJ_REBUILD_EVERY_TICK && cfg->rebuild != TJ_REBUILD_ADAPTIVE)
-    return fail(c, TJ_E_BAD_CONFIG, "unknown rebuild policy");
-  int ndev = 0;
-  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
-    cudaGetLastError();
-    return fail(c, TJ_E_NO_DEVICE, "no CUDA device visible");
-  }
-  if (cfg->device < 0 || cfg->device >= ndev) return fail(c, TJ_E_NO_DEVICE, "device ordinal out of range");
-  c = new tj_ctx();
-  c->cfg = *cfg;
-  if (cfg->split_factor > 0) {  // method "ug": the grid as the leaf level of a 2^L x 2^L cell map
-    c->ug_sf = cfg->split_factor;
-    int L = 1;
-    while ((1 << L) < cfg->split_factor) ++L;
-    c->cfg.l_max = L;
-    c->cfg.th_quad = 1;
-    c->cfg.rebuild = TJ_REBUILD_EVERY_TICK;
-  }
-  c->device = cfg->device;
-  if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
-  if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
-  if (const char* ss = std::getenv("TJ_SERIAL_SORT")) c->serial_sort = std::atoi(ss) != 0;
-  if (const char* sx = std::getenv("TJ_SORT_XY")) c->sort_xy = std::atoi(sx) != 0;
-  if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
-  if (const char* fp = std::getenv("TJ_FUSED_PYR")) c->fused_pyr = std::atoi(fp) != 0;
-  if (const char* ky = std::getenv("TJ_KEYED")) c->key_auto = std::atoi(ky) != 0;
-  cudaSetDevice(c->device);
-  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
-  // side-stream priority (TJ_SIDE_PRIO=1: the object sort's blocks go first) measured no gain:
-  // the sort branch is latency-bound, not starved of SMs; default priority
-  int prio_lo = 0, prio_hi = 0;
-  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
-  int side_prio = prio_lo;
-  if (const char* sp = std::getenv("TJ_SIDE_PRIO")) side_prio = std::atoi(sp) ? prio_hi : prio_lo;
-  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
-      cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
-      cudaMalloc(&c->d_hdr, sizeof(DevHdr)) != cudaSuccess ||
-      cudaMallocHost(&c->h_hdr, sizeof(DevHdr)) != cudaSuccess ||
-      cudaMalloc(&c->d_consts, 8 * sizeof(int64_t)) != cudaSuccess) {
-    std::string msg = std::string("context setup: ") + cudaGetErrorString(cudaGetLastError());
-    tj_destroy(c);
-    return fail(nullptr, TJ_E_CUDA, msg);
-  }
-  for (auto& e : c->ev) cudaEventCreate(&e);
-  cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
-  cudaFuncSetAttribute(k_radix_downsweep<ArrKey, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)radix_smem_bytes<true>());
-  cudaFuncSetAttribute(k_radix_downsweep<ArrKey, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)radix_smem_bytes<false>());
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->join_blocks, k_join, kJT, sizeof(JoinSmem));
-  if (c->join_blocks < 1) c->join_blocks = 1;
-
-  int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
-  cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
-  *out = c;
-  return TJ_OK;
-}
-
-int tj_destroy(tj_ctx* c) {
-  if (!c) return TJ_OK;
-  cudaSetDevice(c->device);
-  if (c->st) cudaStreamSynchronize(c->st);
-  drop_graphs(c);
-  DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
-                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->loff, &c->presence, &c->prespre, &c->order, &c->pyr, &c->clev,
-                 &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
-                 &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qpos, &c->qwin, &c->crect, &c->biglist, &c->sqle,
-                 &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
-                 &c->outids, &c->outoff, &c->scratch, &c->outoff32, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2};
-  for (DBuf* b : all)
-    if (b->p) cudaFree(b->p);
-  if (c->h_off) cudaFreeHost(c->h_off);
-  if (c->h_ids) cudaFreeHost(c->h_ids);
-  if (c->d_hdr) cudaFree(c->d_hdr);
-  if (c->h_hdr) cudaFreeHost(c->h_hdr);
-  if (c->d_consts) cudaFree(c->d_consts);
-  for (auto& e : c->ev)
-    if (e) cudaEventDestroy(e);
-  if (c->st) cudaStreamDestroy(c->st);
-  if (c->side) cudaStreamDestroy(c->side);
-  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
-  if (c->ev_join) cudaEventDestroy(c->ev_join);
-  delete c;
-  return TJ_OK;
-}
-
-int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) {
-  if (!c || !in || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
-  const int64_t n = in->n_obj, m = in->n_q;
-  const bool want32 = (in->out_mem & TJ_OUT_IDS32) != 0;
-  const int out_space = in->out_mem & ~TJ_OUT_IDS32;
-  if (out_space != TJ_MEM_HOST && out_space != TJ_MEM_DEVICE)
-    return fail(c, TJ_E_INVALID_ARG, "unknown output memory space");
-  if (n < 0 || m < 0) return fail(c, TJ_E_INVALID_ARG, "negative size");
-  if (n > INT32_MAX / 2 || m > INT32_MAX / 2) return fail(c, TJ_E_INVALID_ARG, "tick too large for 32-bit rows");
-  if (n >= (int64_t(1) << 28)) return fail(c, TJ_E_INVALID_ARG, "more than 2^28 objects per tick is not supported");
-  if ((n && (!in->obj_id || !in->obj_x || !in->obj_y)) ||
-      (m && (!in->q_issuer || !in->q_xa || !in->q_ya || !in->q_xb || !in->q_yb)))
-    return fail(c, TJ_E_INVALID_ARG, "null input array");
-  TJ_CUDA(cudaSetDevice(c->device));
-  c->have = false;
-  tj_stats S{};
-  S.n_objects = n;
-  S.n_queries = m;
+// The device tick on device-resident inputs: leaves the query-order CSR in c->outoff / c->outids
+// and the tick's statistics in S.
+int compute_tick(tj_ctx* c, int64_t n, int64_t m, const int64_t* ids, const double* xs, const double* ys,
+                 const double* qxa, const double* qya, const double* qxb, const double* qyb, tj_stats& S,
+                 int64_t& R) {
   int rc;
-
-  // ---- inputs to device ---------------------------------------------------
-  const int64_t* ids = in->obj_id;
-  const double *xs = in->obj_x, *ys = in->obj_y;
-  const double *qxa = in->q_xa, *qya = in->q_ya, *qxb = in->q_xb, *qyb = in->q_yb;
-  if (in->mem == TJ_MEM_HOST) {
-    if ((rc = ensure(c, c->ids, n * 8)) || (rc = ensure(c, c->xs, n * 8)) || (rc = ensure(c, c->ys, n * 8)) ||
-        (rc = ensure(c, c->qxa, m * 8)) || (rc = ensure(c, c->qya, m * 8)) || (rc = ensure(c, c->qxb, m * 8)) ||
-        (rc = ensure(c, c->qyb, m * 8)))
-      return rc;
-    TJ_CUDA(cudaMemcpyAsync(c->ids.p, ids, n * 8, cudaMemcpyHostToDevice, c->st));
-    TJ_CUDA(cudaMemcpyAsync(c->xs.p, xs, n * 8, cudaMemcpyHostToDevice, c->st));
-    TJ_CUDA(cudaMemcpyAsync(c->ys.p, ys, n * 8, cudaMemcpyHostToDevice, c->st));
-    TJ_CUDA(cudaMemcpyAsync(c->qxa.p, qxa, m * 8, cudaMemcpyHostToDevice, c->st));
-    TJ_CUDA(cudaMemcpyAsync(c->qya.p, qya, m * 8, cudaMemcpyHostToDevice, c->st));
-    TJ_CUDA(cudaMemcpyAsync(c->qxb.p, qxb, m * 8, cudaMemcpyHostToDevice, c->st));
-    TJ_CUDA(cudaMemcpyAsync(c->qyb.p, qyb, m * 8, cudaMemcpyHostToDevice, c->st));
-    ids = P<int64_t>(c->ids);
-    xs = P<double>(c->xs);
-    ys = P<double>(c->ys);
-    qxa = P<double>(c->qxa);
-    qya = P<double>(c->qya);
-    qxb = P<double>(c->qxb);
-    qyb = P<double>(c->qyb);
-  } else if (in->mem != TJ_MEM_DEVICE) {
-    return fail(c, TJ_E_INVALID_ARG, "unknown memory space");
-  }
-
+  R = 0;
   if ((rc = ensure(c, c->outoff, (m + 1) * 8))) return rc;
-  int64_t R = 0;
   if (n == 0) {  // engine.py:188-190: every issued query gets []
     TJ_CUDA(cudaMemsetAsync(c->outoff.p, 0, (m + 1) * 8, c->st));
     TJ_CUDA(cudaStreamSynchronize(c->st));
@@ -958,7 +799,17 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     S.mbr[3] = H.yb;
   }
 
-  // ---- deliver results ----------------------------------------------------
+  return TJ_OK;
+}
+
+// Result delivery (device pointers or pinned host copies; TJ_OUT_IDS32 narrows ids and offsets on the
+// device when they fit) of a query-order CSR: offsets (m + 1, int64) and ids (R, int64); `scratch`
+// holds the narrowed ids.
+int deliver(tj_ctx* c, int out_mem, tj_tick_out* out, int64_t m, int64_t R, bool have_ids, const DBuf& offbuf,
+            const DBuf& idsbuf, DBuf& scratch, tj_stats& S) {
+  int rc;
+  const bool want32 = (out_mem & TJ_OUT_IDS32) != 0;
+  const int out_space = out_mem & ~TJ_OUT_IDS32;
   out->n_q = m;
   out->n_results = R;
   // TJ_OUT_IDS32: narrow the ids on the device (into the idle merge scratch) when they all fit
@@ -966,7 +817,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
   if (want32) {
     use32 = true;
     if (R > 0) {
-      k_narrow_ids<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(c->outids), P<int32_t>(c->scratch), R, c->d_hdr);
+      k_narrow_ids<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(idsbuf), P<int32_t>(scratch), R, c->d_hdr);
       ++S.kernel_launches;
       TJ_CUDA(cudaMemcpyAsync(&c->h_hdr->ids_wide, &c->d_hdr->ids_wide, sizeof(int32_t), cudaMemcpyDeviceToHost,
                               c->st));
@@ -979,7 +830,7 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
   const int64_t ob = off32 ? 4 : 8;
   if (off32) {
     if ((rc = ensure(c, c->outoff32, (size_t)(m + 1) * 4))) return rc;
-    k_narrow_offsets<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(c->outoff), P<int32_t>(c->outoff32), m + 1);
+    k_narrow_offsets<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(offbuf), P<int32_t>(c->outoff32), m + 1);
     ++S.kernel_launches;
   }
   out->id_bytes = (int32_t)idb;
@@ -990,16 +841,16 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
   out->offsets32 = nullptr;
   if (out_space == TJ_MEM_DEVICE) {
     if (off32) out->offsets32 = P<int32_t>(c->outoff32);
-    else out->offsets = P<int64_t>(c->outoff);
-    if (use32) out->ids32 = R ? P<int32_t>(c->scratch) : nullptr;
-    else out->ids = n ? P<int64_t>(c->outids) : nullptr;
+    else out->offsets = P<int64_t>(offbuf);
+    if (use32) out->ids32 = R ? P<int32_t>(scratch) : nullptr;
+    else out->ids = have_ids ? P<int64_t>(idsbuf) : nullptr;
     out->mem = TJ_MEM_DEVICE;
   } else {
     if ((rc = ensure_host(c, c->h_off, c->h_off_bytes, (m + 1) * ob))) return rc;
     if ((rc = ensure_host(c, c->h_ids, c->h_ids_bytes, R * idb))) return rc;
-    TJ_CUDA(cudaMemcpyAsync(c->h_off, off32 ? c->outoff32.p : c->outoff.p, (m + 1) * ob, cudaMemcpyDeviceToHost,
+    TJ_CUDA(cudaMemcpyAsync(c->h_off, off32 ? c->outoff32.p : offbuf.p, (m + 1) * ob, cudaMemcpyDeviceToHost,
                             c->st));
-    if (R) TJ_CUDA(cudaMemcpyAsync(c->h_ids, use32 ? c->scratch.p : c->outids.p, R * idb, cudaMemcpyDeviceToHost,
+    if (R) TJ_CUDA(cudaMemcpyAsync(c->h_ids, use32 ? scratch.p : idsbuf.p, R * idb, cudaMemcpyDeviceToHost,
                                    c->st));
     TJ_CUDA(cudaStreamSynchronize(c->st));
     if (off32) out->offsets32 = (const int32_t*)c->h_off;
@@ -1008,6 +859,185 @@ int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) 
     else out->ids = (const int64_t*)c->h_ids;
     out->mem = TJ_MEM_HOST;
   }
+  return TJ_OK;
+}
+
+
+}  // namespace
+
+#include "tj_shard.cuh"
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+int tj_abi_version(void) { return TJ_ABI_VERSION; }
+
+int tj_device_count(int* count) {
+  int n = 0;
+  cudaError_t e = cudaGetDeviceCount(&n);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (count) *count = n;
+  return TJ_OK;
+}
+
+const char* tj_last_error(const tj_ctx* ctx) { return ctx ? ctx->err.c_str() : g_last_error.c_str(); }
+
+int tj_create(const tj_config* cfg, tj_ctx** out) {
+  tj_ctx* c = nullptr;
+  if (!cfg || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
+  // MethodConfig.validate (engine.py:73-88)
+  if (cfg->split_factor < 0) return fail(c, TJ_E_BAD_CONFIG, "split_factor must be >= 1");
+  if (cfg->split_factor > (1 << kMaxLevel))
+    return fail(c, TJ_E_BAD_CONFIG, "split factors above 4096 are not supported on the device path");
+  if (cfg->split_factor == 0) {
+    if (cfg->th_quad < 1) return fail(c, TJ_E_BAD_CONFIG, "th_quad must be >= 1");
+    if (cfg->l_max < 1 || cfg->l_max > kMaxLevel) return fail(c, TJ_E_BAD_CONFIG, "l_max must be in [1, 12]");
+  }
+  if (cfg->rebuild != TJ_REBUILD_EVERY_TICK && cfg->rebuild != TJ_REBUILD_ADAPTIVE)
+    return fail(c, TJ_E_BAD_CONFIG, "unknown rebuild policy");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(c, TJ_E_NO_DEVICE, "no CUDA device visible");
+  }
+  if (cfg->device < 0 || cfg->device >= ndev) return fail(c, TJ_E_NO_DEVICE, "device ordinal out of range");
+  c = new tj_ctx();
+  c->cfg = *cfg;
+  if (cfg->split_factor > 0) {  // method "ug": the grid as the leaf level of a 2^L x 2^L cell map
+    c->ug_sf = cfg->split_factor;
+    int L = 1;
+    while ((1 << L) < cfg->split_factor) ++L;
+    c->cfg.l_max = L;
+    c->cfg.th_quad = 1;
+    c->cfg.rebuild = TJ_REBUILD_EVERY_TICK;
+  }
+  c->device = cfg->device;
+  if (const char* ng = std::getenv("TJ_NO_GRAPH")) c->use_graphs = std::atoi(ng) == 0;
+  if (const char* lb = std::getenv("TJ_SCAN_LB")) c->lb_scan = std::atoi(lb) != 0;
+  if (const char* ss = std::getenv("TJ_SERIAL_SORT")) c->serial_sort = std::atoi(ss) != 0;
+  if (const char* sx = std::getenv("TJ_SORT_XY")) c->sort_xy = std::atoi(sx) != 0;
+  if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
+  if (const char* fp = std::getenv("TJ_FUSED_PYR")) c->fused_pyr = std::atoi(fp) != 0;
+  if (const char* ky = std::getenv("TJ_KEYED")) c->key_auto = std::atoi(ky) != 0;
+  cudaSetDevice(c->device);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
+  // side-stream priority (TJ_SIDE_PRIO=1: the object sort's blocks go first) measured no gain:
+  // the sort branch is latency-bound, not starved of SMs; default priority
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  int side_prio = prio_lo;
+  if (const char* sp = std::getenv("TJ_SIDE_PRIO")) side_prio = std::atoi(sp) ? prio_hi : prio_lo;
+  if (cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, side_prio) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaMalloc(&c->d_hdr, sizeof(DevHdr)) != cudaSuccess ||
+      cudaMallocHost(&c->h_hdr, sizeof(DevHdr)) != cudaSuccess ||
+      cudaMalloc(&c->d_consts, 8 * sizeof(int64_t)) != cudaSuccess) {
+    std::string msg = std::string("context setup: ") + cudaGetErrorString(cudaGetLastError());
+    tj_destroy(c);
+    return fail(nullptr, TJ_E_CUDA, msg);
+  }
+  for (auto& e : c->ev) cudaEventCreate(&e);
+  cudaFuncSetAttribute(k_join, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(JoinSmem));
+  cudaFuncSetAttribute(k_radix_downsweep<ArrKey, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)radix_smem_bytes<true>());
+  cudaFuncSetAttribute(k_radix_downsweep<ArrKey, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)radix_smem_bytes<false>());
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->join_blocks, k_join, kJT, sizeof(JoinSmem));
+  if (c->join_blocks < 1) c->join_blocks = 1;
+
+  int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
+  cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
+  *out = c;
+  return TJ_OK;
+}
+
+int tj_destroy(tj_ctx* c) {
+  if (!c) return TJ_OK;
+  cudaSetDevice(c->device);
+  if (c->st) cudaStreamSynchronize(c->st);
+  drop_graphs(c);
+  DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->loff, &c->presence, &c->prespre, &c->order, &c->pyr, &c->clev,
+                 &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
+                 &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qpos, &c->qwin, &c->biglist, &c->sqle,
+                 &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
+                 &c->outids, &c->outoff, &c->scratch, &c->outoff32, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2,
+                 &c->pcnt, &c->rcnt, &c->sstart, &c->moff, &c->sconst, &c->rids, &c->mids, &c->mscratch};
+  delete c->comm;
+  c->comm = nullptr;
+  for (DBuf* b : all)
+    if (b->p) cudaFree(b->p);
+  if (c->h_off) cudaFreeHost(c->h_off);
+  if (c->h_ids) cudaFreeHost(c->h_ids);
+  if (c->d_hdr) cudaFree(c->d_hdr);
+  if (c->h_hdr) cudaFreeHost(c->h_hdr);
+  if (c->d_consts) cudaFree(c->d_consts);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->st) cudaStreamDestroy(c->st);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  delete c;
+  return TJ_OK;
+}
+
+int tj_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) {
+  if (!c || !in || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
+  const int64_t n = in->n_obj, m = in->n_q;
+  const int out_space = in->out_mem & ~TJ_OUT_IDS32;
+  if (out_space != TJ_MEM_HOST && out_space != TJ_MEM_DEVICE)
+    return fail(c, TJ_E_INVALID_ARG, "unknown output memory space");
+  if (n < 0 || m < 0) return fail(c, TJ_E_INVALID_ARG, "negative size");
+  if (n > INT32_MAX / 2 || m > INT32_MAX / 2) return fail(c, TJ_E_INVALID_ARG, "tick too large for 32-bit rows");
+  if (n >= (int64_t(1) << 28)) return fail(c, TJ_E_INVALID_ARG, "more than 2^28 objects per tick is not supported");
+  if ((n && (!in->obj_id || !in->obj_x || !in->obj_y)) ||
+      (m && (!in->q_issuer || !in->q_xa || !in->q_ya || !in->q_xb || !in->q_yb)))
+    return fail(c, TJ_E_INVALID_ARG, "null input array");
+  TJ_CUDA(cudaSetDevice(c->device));
+  c->have = false;
+  tj_stats S{};
+  S.n_objects = n;
+  S.n_queries = m;
+  int rc;
+
+  // ---- inputs to device ---------------------------------------------------
+  const int64_t* ids = in->obj_id;
+  const double *xs = in->obj_x, *ys = in->obj_y;
+  const double *qxa = in->q_xa, *qya = in->q_ya, *qxb = in->q_xb, *qyb = in->q_yb;
+  if (in->mem == TJ_MEM_HOST) {
+    if ((rc = ensure(c, c->ids, n * 8)) || (rc = ensure(c, c->xs, n * 8)) || (rc = ensure(c, c->ys, n * 8)) ||
+        (rc = ensure(c, c->qxa, m * 8)) || (rc = ensure(c, c->qya, m * 8)) || (rc = ensure(c, c->qxb, m * 8)) ||
+        (rc = ensure(c, c->qyb, m * 8)))
+      return rc;
+    TJ_CUDA(cudaMemcpyAsync(c->ids.p, ids, n * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->xs.p, xs, n * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->ys.p, ys, n * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qxa.p, qxa, m * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qya.p, qya, m * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qxb.p, qxb, m * 8, cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaMemcpyAsync(c->qyb.p, qyb, m * 8, cudaMemcpyHostToDevice, c->st));
+    ids = P<int64_t>(c->ids);
+    xs = P<double>(c->xs);
+    ys = P<double>(c->ys);
+    qxa = P<double>(c->qxa);
+    qya = P<double>(c->qya);
+    qxb = P<double>(c->qxb);
+    qyb = P<double>(c->qyb);
+  } else if (in->mem != TJ_MEM_DEVICE) {
+    return fail(c, TJ_E_INVALID_ARG, "unknown memory space");
+  }
+
+  int64_t R = 0;
+  if ((rc = compute_tick(c, n, m, ids, xs, ys, qxa, qya, qxb, qyb, S, R))) return rc;
+  if ((rc = deliver(c, in->out_mem, out, m, R, n > 0, c->outoff, c->outids, c->scratch, S))) return rc;
   if (stats) *stats = S;
   return TJ_OK;
 }
@@ -1362,6 +1392,84 @@ int tj_set_shard(tj_ctx* c, int32_t rank, int32_t nranks) {
   c->shard_rank = rank;
   c->shard_n = nranks;
   c->have = false;
+  return TJ_OK;
+}
+
+int tj_nccl_unique_id(void* id, int32_t bytes) {
+  if (!id || bytes < (int32_t)sizeof(ncclUniqueId)) return fail(nullptr, TJ_E_INVALID_ARG, "need 128 bytes");
+  NcclApi* api = nccl_api();
+  if (!api) return fail(nullptr, TJ_E_NCCL, "NCCL unavailable");
+  ncclResult_t r = api->GetUniqueId(static_cast<ncclUniqueId*>(id));
+  if (r != ncclSuccess) return fail(nullptr, TJ_E_NCCL, std::string("ncclGetUniqueId: ") + api->GetErrorString(r));
+  return TJ_OK;
+}
+
+int tj_comm_init(tj_ctx* c, const void* unique_id, int32_t rank, int32_t nranks) {
+  if (!c || !unique_id || nranks < 1 || rank < 0 || rank >= nranks) return fail(c, TJ_E_INVALID_ARG, "bad comm");
+  NcclApi* api = nccl_api();
+  if (!api) return fail(c, TJ_E_NCCL, "NCCL unavailable");
+  TJ_CUDA(cudaSetDevice(c->device));
+  auto* t = new NcclTransport();
+  t->api = api;
+  t->rank = rank;
+  t->nranks = nranks;
+  ncclUniqueId uid;
+  std::memcpy(&uid, unique_id, sizeof(uid));
+  ncclResult_t r = api->CommInitRank(&t->comm, nranks, uid, rank);
+  if (r != ncclSuccess) {
+    t->comm = nullptr;
+    delete t;
+    return fail(c, TJ_E_NCCL, std::string("ncclCommInitRank: ") + api->GetErrorString(r));
+  }
+  delete c->comm;
+  c->comm = t;
+  return TJ_OK;
+}
+
+int tj_group_create(int32_t nranks, tj_group** out) {
+  if (nranks < 1 || !out) return fail(nullptr, TJ_E_INVALID_ARG, "bad group");
+  auto* g = new tj_group();
+  g->n = nranks;
+  g->ptr.assign(nranks, nullptr);
+  g->cnt.assign(nranks, nullptr);
+  g->displ.assign(nranks, nullptr);
+  *out = g;
+  return TJ_OK;
+}
+
+int tj_group_destroy(tj_group* g) {
+  delete g;
+  return TJ_OK;
+}
+
+int tj_comm_init_local(tj_ctx* c, tj_group* g, int32_t rank) {
+  if (!c || !g || rank < 0 || rank >= g->n) return fail(c, TJ_E_INVALID_ARG, "bad local comm");
+  auto* t = new LocalTransport();
+  t->g = g;
+  t->rank = rank;
+  t->nranks = g->n;
+  delete c->comm;
+  c->comm = t;
+  return TJ_OK;
+}
+
+int tj_tick_sharded(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats* stats) {
+  if (!c || !in || !out) return fail(c, TJ_E_INVALID_ARG, "null argument");
+  if (!c->comm) return fail(c, TJ_E_INVALID_ARG, "no communicator: tj_comm_init / tj_comm_init_local first");
+  const int64_t n = in->n_obj, m = in->n_q;
+  const int out_space = in->out_mem & ~TJ_OUT_IDS32;
+  if (out_space != TJ_MEM_HOST && out_space != TJ_MEM_DEVICE)
+    return fail(c, TJ_E_INVALID_ARG, "unknown output memory space");
+  if (in->mem != TJ_MEM_HOST && in->mem != TJ_MEM_DEVICE) return fail(c, TJ_E_INVALID_ARG, "unknown memory space");
+  if (n < 0 || m < 0) return fail(c, TJ_E_INVALID_ARG, "negative size");
+  if ((n && (!in->obj_id || !in->obj_x || !in->obj_y)) || (m && (!in->q_xa || !in->q_ya || !in->q_xb || !in->q_yb)))
+    return fail(c, TJ_E_INVALID_ARG, "null input array");
+  TJ_CUDA(cudaSetDevice(c->device));
+  c->have = false;
+  tj_stats S{};
+  int rc = sharded_tick(c, in, out, S);
+  if (rc) return rc;
+  if (stats) *stats = S;
   return TJ_OK;
 }
 

@@ -73,7 +73,6 @@ struct Dev {
   int4* leaf_cnt;          // per leaf: intersecting / covering pairs of small windows, of large windows
   int4* qpos;              // per small-window query: each pair's place in its leaf block
   int4* qwin;              // per query: deepest-cell window of its clipped rect (count pass -> fill pass)
-  Rect4* crect;            // per query: clipped rect (count pass -> fill pass)
   int32_t* unit_leaf;      // join work unit -> leaf
   uint8_t* leaf_active;    // multi-GPU leaf-range sharding: leaf owned by this rank (nullptr: all)
   int64_t* leaf_wpre;      // exclusive prefix of the per-leaf work weight (sharding)
@@ -727,7 +726,6 @@ __global__ void __launch_bounds__(256) k_query_count(const Dev d) {
     }
     d.nsub[q] = cnt;
     d.qwin[q] = w;
-    d.crect[q] = r;
   }
 }
 
@@ -746,10 +744,21 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
   const int64_t m = h->m;
   const int ld = h->l_deep;
   const int cov_on = h->covering;
+  const double xa = h->xa, ya = h->ya, xb = h->xb, yb = h->yb;
   TJ_GRID_STRIDE(q, m) {
     const int n = d.nsub[q];
     if (n == 0) continue;
-    const Rect4 r = d.crect[q];  // clip from the count pass
+    // the clip again (geometry.py:80-88): re-reading the query costs what reading a stored clip
+    // would, and the count pass then writes no per-query rect
+    Rect4 r;
+    r.xa = d.qxa[q];
+    r.ya = d.qya[q];
+    r.xb = d.qxb[q];
+    r.yb = d.qyb[q];
+    r.xa = r.xa < xa ? xa : r.xa;  // exactly clip_window's max / min
+    r.ya = r.ya < ya ? ya : r.ya;
+    r.xb = r.xb > xb ? xb : r.xb;
+    r.yb = r.yb > yb ? yb : r.yb;
     const int4 p4 = d.qpos[q];
     const int4 w = d.qwin[q];  // small window: its leaves as found by the count pass; else the window
     const int32_t base = d.qsbase[q];
@@ -883,7 +892,7 @@ constexpr int kTileObj = kTileBlocks * 32;
 constexpr int kNK = TJ_NK;                    // buckets per axis
 constexpr int kRows = kNK + 2;                // prefix rows k = 0 .. kNK + 1
 #ifndef TJ_QC
-#define TJ_QC 512
+#define TJ_QC 256
 #endif
 constexpr int kQC = TJ_QC;                    // subqueries per chunk
 #ifndef TJ_TMQ
@@ -982,13 +991,61 @@ __global__ void __launch_bounds__(256) k_zero_counts(const Dev d) {
   TJ_GRID_STRIDE(e, h->S) d.ecount[e] = 0;
 }
 
+// Tile objects arrive by bulk copy (cp.async.bulk, the TMA engine's 1-D
+// copy), double-buffered: while a CTA joins unit u, the copy engine stages
+// unit u + gridDim's x / y into the other buffer, completion tracked by an
+// mbarrier per buffer.  A bulk copy needs 16-byte aligned addresses and sizes,
+// so a tile is copied from the 16-byte boundary at or below its first object
+// (lead = 0 or 1 doubles) and rounded up (the coordinate arrays carry 16
+// bytes of slack); objects past the tile's end are never read unmasked.
+constexpr int kTileBuf = kTileObj + 4;    // lead + round-up
 struct JoinSmem {
-  double ox[kTileObj];                    // tile objects (NaN padding never matches)
-  double oy[kTileObj];
+  double ox[2][kTileBuf];                 // tile objects, two stages
+  double oy[2][kTileBuf];
+  unsigned long long bar[2];              // mbarriers of the two stages
   uint32_t tab[2 * kRows * kTileBlocks];  // [axis][k][b], row stride = tile blocks
   ushort4 kb[kQC];                        // bucket of xa, xb, ya, yb
   int32_t cnt[kQC];
 };
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "TJ_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra TJ_WAIT_%=;\n}"
+      ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+// The tile of unit u: first object (global index), object count, 16-byte lead
+struct TileRef {
+  int32_t ob;
+  int P;
+};
+__device__ __forceinline__ TileRef tile_of(const Dev& d, int64_t u) {
+  const int64_t r = d.unit_leaf[u];
+  const int4 li = d.linfo[r];
+  const int nb = (li.y + 31) >> 5;
+  const int b0 = (int)(u - d.leaf_ubase[r]) * kTileBlocks, nbt = min(kTileBlocks, nb - b0);
+  return TileRef{li.x + b0 * 32, min(li.y - b0 * 32, nbt * 32)};
+}
+// issue the bulk copies of a tile's x / y into stage buffers (one thread)
+__device__ __forceinline__ void stage_tile(const Dev& d, JoinSmem& S, int st, TileRef t) {
+  const int lead = t.ob & 1;  // doubles before the tile in its 16-byte line
+  const uint32_t bytes = (uint32_t)(((t.P + lead) * 8 + 15) & ~15);
+  mbar_expect_tx(&S.bar[st], 2 * bytes);
+  bulk_g2s(S.ox[st], d.sx + (t.ob - lead), bytes, &S.bar[st]);
+  bulk_g2s(S.oy[st], d.sy + (t.ob - lead), bytes, &S.bar[st]);
+}
 
 // Monotone bucket map of one axis of a leaf.  Any base and positive scale
 // keep it monotone (fl(v - base), the product, the clamps and the
@@ -1015,11 +1072,24 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
   JoinSmem& S = *reinterpret_cast<JoinSmem*>(join_smem);
   const int tid = threadIdx.x, lane = lane_id(), wp = tid >> 5;
   const int64_t U = h->U;
-  const double kNaN = __longlong_as_double(0x7ff8000000000000ll);
   const double gxa = h->xa, gya = h->ya, gw = h->width, gh = h->height;
   const double sxm = h->sx_max, sym = h->sy_max;  // 2^l_max / extent (0 for an empty extent)
   const int lmax = h->l_max;
-  for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+  if (tid == 0) {
+    mbar_init(&S.bar[0]);
+    mbar_init(&S.bar[1]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x < U) stage_tile(d, S, 0, tile_of(d, blockIdx.x));
+  }
+  __syncthreads();
+  int iter = 0;
+  for (int64_t u = blockIdx.x; u < U; u += gridDim.x, ++iter) {
+    const int stg = iter & 1;
+    // the next unit's objects into the other stage (free: the previous unit ended with a barrier)
+    if (tid == 0 && u + gridDim.x < U) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // the stage's generic reads before the copy
+      stage_tile(d, S, stg ^ 1, tile_of(d, u + gridDim.x));
+    }
     const int64_t r = d.unit_leaf[u];
     const int4 li = d.linfo[r];  // object base, object count, entry base, intersecting count
     const int nobj = li.y, nisq = li.w;
@@ -1034,16 +1104,10 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
     const int32_t sbase = li.z;
     const bool table = nisq >= kTableMinQ;
     const int nbs = kJoinTPS ? (nbt + 1) & ~1 : nbt;  // table row stride (even: paired 8-byte lookups)
-    // ---- stage the tile's objects -------------------------------------------
-    for (int i = tid; i < nbt * 32; i += kJT) {
-      double x = kNaN, y = kNaN;
-      if (i < P) {
-        x = d.sx[ob + i];
-        y = d.sy[ob + i];
-      }
-      S.ox[i] = x;
-      S.oy[i] = y;
-    }
+    // ---- this unit's objects (bulk-copied into stage stg) ----------------------
+    mbar_wait(&S.bar[stg], (uint32_t)((iter >> 1) & 1));
+    const double* ox = S.ox[stg] + (ob & 1);
+    const double* oy = S.oy[stg] + (ob & 1);
     float bx = 0.0f, by = 0.0f, scx = 0.0f, scy = 0.0f;
     if (table) {
       const uint32_t code = d.leaf_code[r];
@@ -1061,7 +1125,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       __syncthreads();
       // bucket scatter: Bk[axis][k][b] |= bit of each object
       for (int i = tid; i < P; i += kJT) {
-        const int kx = bucket(S.ox[i], bx, scx), ky = bucket(S.oy[i], by, scy);
+        const int kx = bucket(ox[i], bx, scx), ky = bucket(oy[i], by, scy);
         const uint32_t bit = 1u << (i & 31);
         atomicOr(&S.tab[kx * nbs + (i >> 5)], bit);
         atomicOr(&S.tab[(kRows + ky) * nbs + (i >> 5)], bit);
@@ -1106,8 +1170,11 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
       const uint2* TY = reinterpret_cast<const uint2*>(S.tab + kRows * nbs);
       const int hs = nbs >> 1;
       const bool last_tile = b0 + nbt == nb;
+      Rect4 Rn;
+      if (tid < nisq) Rn = erect[tid];
       for (int t = tid; t < nisq; t += kJT) {
-        const Rect4 R = erect[t];
+        const Rect4 R = Rn;
+        if (t + kJT < nisq) Rn = erect[t + kJT];  // the next subquery's rect in flight
         const int kxa = bucket(R.xa, bx, scx) * hs, kxb = bucket(R.xb, bx, scx) * hs;
         const int kya = bucket(R.ya, by, scy) * hs, kyb = bucket(R.yb, by, scy) * hs;
         uint32_t* orow = d.bitmap + woff + (int64_t)t * nbp + b0;
@@ -1128,7 +1195,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
               const int bit = __ffs(a) - 1;
               a &= a - 1;
               const int o = (b << 5) + bit;
-              if (in_rect(S.ox[o], S.oy[o], R)) D[e] |= 1u << bit;
+              if (in_rect(ox[o], oy[o], R)) D[e] |= 1u << bit;
             }
             if (b < nbt) {
               orow[b] = D[e];
@@ -1177,7 +1244,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
               const int bit = __ffs(A) - 1;
               A &= A - 1;
               const int o = (b << 5) + bit;
-              if (in_rect(S.ox[o], S.oy[o], R)) D |= 1u << bit;
+              if (in_rect(ox[o], oy[o], R)) D |= 1u << bit;
             } while (A);
           }
           out[(int64_t)s * nbp + b] = D;
@@ -1197,8 +1264,10 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
 #pragma unroll 8
           for (int k = 0; k < 32; ++k) {
             const int o = (b << 5) + k;
-            if (in_rect(S.ox[o], S.oy[o], R)) w |= 1u << k;
+            if (in_rect(ox[o], oy[o], R)) w |= 1u << k;
           }
+          const int valid = P - (b << 5);  // objects past the tile hold other leaves' coordinates
+          if (valid < 32) w &= (1u << valid) - 1u;
           if (s < nq) {
             out[(int64_t)s * nbp + b] = w;
             if (w) atomicAdd(&S.cnt[s], __popc(w));

@@ -1,14 +1,21 @@
 """Multi-GPU leaf-range sharding of the QUAD tick.
 
-One process per GPU.  Each rank ingests 1/G of the tick's position updates
-and queries; an all-gather (NCCL over NVLink on GPUs, gloo on CPU) gives every
-rank the full tick; every rank builds the bit-identical index (the index
-build is integer-exact), then scatters, joins, decodes and assembles only the
-(query, leaf) pairs of its contiguous Morton range of leaves, balanced by the
-per-leaf object count (device side: `tj_set_shard`, `k_shard_mark` in
-csrc/tj_kernels.cuh, run right after the index build).  A rank's per-query lists are the restriction of the
-full lists to its leaves: disjoint across ranks and each sorted, so the
-per-query union (merge) is the full result.
+One process per GPU.  Each rank passes its slice of the tick's position
+updates and queries; the ranks' slices are gathered into the full tick on
+every rank, every rank builds the bit-identical index (the index build is
+integer-exact), then scatters, joins and decodes only the (query, leaf) pairs
+of its contiguous Morton range of leaves, balanced by the per-leaf object
+count (device side: `k_shard_mark` in csrc/tj_kernels.cuh).  A rank's
+per-query lists are the restriction of the full lists to its leaves: disjoint
+across ranks and each sorted.  Each query's partial lists go to its home
+rank (the rank whose slice issued it) and are merged there, so every rank
+ends with the complete lists of its own queries.
+
+The product path is the native library's `tj_tick_sharded` over NCCL
+(csrc/tj_shard.cuh: NCCL broadcasts / send-recv on the library stream, merge
+on the device).  `ShardedEngine(..., partial_tick=f)` runs the same protocol
+with torch.distributed collectives and a caller-supplied partial tick — the
+host restatement the CPU tests drive over gloo with a stubbed device tick.
 
 The reference has no distributed path (multi-GPU / distributed
 execution is a non-goal); this module is B200-side plumbing only.
@@ -79,13 +86,23 @@ def all_gather_var(t, group=None):
     return torch.cat([b[:s] for b, s in zip(bufs, sizes)]), sizes
 
 
+def split_bounds(total: int, world: int) -> np.ndarray:
+    """Contiguous 1/G slices: rank r owns [b[r], b[r + 1])."""
+    return np.array([r * total // world for r in range(world + 1)], np.int64)
+
+
 class ShardedEngine:
-    """One rank of a G-GPU QUAD tick (torch.distributed process group already initialised)."""
+    """One rank of a G-GPU QUAD tick (torch.distributed process group already initialised).
 
-    def __init__(self, cfg, device: Optional[int] = None, group=None):
+    partial_tick=None: the native `tj_tick_sharded` over an NCCL communicator the ranks set
+    up here (rank 0's unique id broadcast over the process group).  Otherwise
+    partial_tick(ids, xs, ys, qxa, qya, qxb, qyb, rank, world) -> (offsets[m + 1], ids) must
+    return the full tick's per-query lists restricted to the rank's leaves (what the device
+    computes after `k_shard_mark`), and the gather / routing / merge run on the host with
+    torch.distributed (the restatement of csrc/tj_shard.cuh the gloo tests exercise)."""
+
+    def __init__(self, cfg, device: Optional[int] = None, group=None, partial_tick=None):
         import torch.distributed as dist
-
-        from . import _native
 
         cfg.validate()
         self.cfg = cfg
@@ -93,30 +110,60 @@ class ShardedEngine:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = cfg.device if device is None else device
-        self.ctx = _native.NativeContext(cfg.th_quad, cfg.l_max, cfg.covering_optimization, 0, self.device)
-        if self.world > 1:
-            self.ctx.set_shard(self.rank, self.world)
+        self.partial_tick = partial_tick
+        self.ctx = None
+        if partial_tick is None:
+            from . import _native
 
-    def process_shard(self, ids, xs, ys, qids, qxa, qya, qxb, qyb):
-        """This rank's share of the tick in (host arrays); the full CSR out on every rank."""
+            self.ctx = _native.NativeContext(cfg.th_quad, cfg.l_max, cfg.covering_optimization, 0, self.device)
+            uid = [_native.nccl_unique_id() if self.rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0, group=group)
+            self.ctx.comm_init(uid[0], self.rank, self.world)
+
+    def process_shard(self, ids, xs, ys, qxa, qya, qxb, qyb):
+        """This rank's slice of the tick in (host arrays); the complete CSR of this rank's
+        queries out: (offsets, ids), stats (None on the host path)."""
+        if self.ctx is not None:
+            offs, res, st = self.ctx.tick_sharded_host(ids, xs, ys, qxa, qya, qxb, qyb)
+            return (offs, res), st
+        return self._host_protocol(ids, xs, ys, qxa, qya, qxb, qyb), None
+
+    def _host_protocol(self, ids, xs, ys, qxa, qya, qxb, qyb):
         import torch
+        import torch.distributed as dist
 
-        dev = torch.device("cuda", self.device) if torch.cuda.is_available() else torch.device("cpu")
-        cols = [torch.as_tensor(np.ascontiguousarray(a)).to(dev) for a in (ids, xs, ys, qids, qxa, qya, qxb, qyb)]
-        full = [all_gather_var(c, self.group)[0].cpu().numpy() for c in cols]
-        offs, res, st = self.ctx.tick_host(*full)
-        counts = torch.as_tensor(np.diff(offs)).to(dev)
-        all_counts, _ = all_gather_var(counts, self.group)
-        all_ids, sizes = all_gather_var(torch.as_tensor(res).to(dev), self.group)
-        m = len(full[3])
-        all_counts = all_counts.cpu().numpy().reshape(self.world, m)
-        all_ids = all_ids.cpu().numpy()
+        G, r, grp = self.world, self.rank, self.group
+        cols = [torch.as_tensor(np.ascontiguousarray(a)) for a in (ids, xs, ys, qxa, qya, qxb, qyb)]
+        # 1. the full tick on every rank (slices concatenated in rank order)
+        full = [all_gather_var(c, grp)[0].numpy() for c in cols]
+        msz = torch.tensor([len(qxa)], dtype=torch.int64)
+        msizes = [torch.zeros_like(msz) for _ in range(G)]
+        dist.all_gather(msizes, msz, group=grp)
+        M = [int(x.item()) for x in msizes]
+        md = np.concatenate([[0], np.cumsum(M)]).astype(np.int64)
+        # 2. this rank's leaves
+        poffs, pids = self.partial_tick(*full, r, G)
+        poffs = np.asarray(poffs, np.int64)
+        # 3. partial lists to the home ranks: per-query counts, then the id runs
+        counts = torch.as_tensor(np.diff(poffs))
+        rcnt = torch.empty(G * M[r], dtype=torch.int64)
+        dist.all_to_all_single(rcnt, counts, output_split_sizes=[M[r]] * G, input_split_sizes=M, group=grp)
+        bounds = poffs[md]
+        scnt = torch.as_tensor(np.diff(bounds))
+        rsz = torch.empty(G, dtype=torch.int64)
+        dist.all_to_all_single(rsz, scnt, group=grp)
+        rids = torch.empty(int(rsz.sum()), dtype=torch.int64)
+        dist.all_to_all_single(rids, torch.as_tensor(np.asarray(pids, np.int64)[bounds[0]:bounds[-1]]),
+                               output_split_sizes=rsz.tolist(), input_split_sizes=scnt.tolist(), group=grp)
+        # 4. merge the G sorted partial lists of every own query
+        rcnt = rcnt.numpy().reshape(G, M[r])
         parts, base = [], 0
-        for r in range(self.world):
-            o = np.concatenate([[0], np.cumsum(all_counts[r])]).astype(np.int64)
-            parts.append((o, all_ids[base:base + sizes[r]]))
-            base += sizes[r]
-        return merge_partials(parts), st
+        for j in range(G):
+            o = np.concatenate([[0], np.cumsum(rcnt[j])]).astype(np.int64)
+            parts.append((o, rids.numpy()[base:base + int(o[-1])]))
+            base += int(o[-1])
+        return merge_partials(parts)
 
     def close(self):
-        self.ctx.close()
+        if self.ctx is not None:
+            self.ctx.close()

@@ -1,9 +1,11 @@
 """Leaf-range sharding across ranks.
 
-CPU: ownership math, partial merging, and a world_size-2 gloo run of the
-host path (all-gather of per-rank updates, per-rank partial results, gather +
-merge) with the oracle standing in for each rank's device tick.
-GPU: two sharded contexts on one device reproduce the unsharded tick.
+CPU: ownership math, partial merging, and world_size-2 gloo runs of
+ShardedEngine's host protocol (gather of the ranks' slices, per-rank partial
+lists, routing to the queries' home ranks, merge) with the oracle restricted
+to the rank's leaves standing in for the device tick.
+GPU: sharded contexts on one device reproduce the unsharded tick (the native
+data plane itself: tests/test_gpu_sharded.py).
 """
 
 from __future__ import annotations
@@ -72,35 +74,41 @@ def _small_tick(seed=3):
     return dict(ids=tk.ids, xs=tk.xs, ys=tk.ys, qids=tk.qids, rects=(tk.qxa, tk.qya, tk.qxb, tk.qyb))
 
 
+def _stub_partial_tick(ids, xs, ys, qxa, qya, qxb, qyb, rank, world):
+    """Stubbed device tick: the full tick's lists restricted to the rank's Morton leaf range."""
+    tick = dict(ids=ids, xs=xs, ys=ys, qids=np.arange(len(qxa), dtype=np.int64), rects=(qxa, qya, qxb, qyb))
+    offs, pids, _ = _partial_for_rank(tick, rank, world)
+    return offs, pids
+
+
 def _gloo_worker(rank, world, port, out):
-    import torch
     import torch.distributed as dist
 
-    from paper_1411_3212_b200.sharding import all_gather_var
+    from paper_1411_3212_b200 import MethodConfig
+    from paper_1411_3212_b200.sharding import ShardedEngine
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         full = _small_tick()
         n, m = len(full["ids"]), len(full["qids"])
-        # this rank ingests 1/G of the updates and queries (interleaved split)
-        osl, qsl = slice(rank, n, world), slice(rank, m, world)
-        mine = [full["ids"][osl], full["xs"][osl], full["ys"][osl], full["qids"][qsl],
-                *(r[qsl] for r in full["rects"])]
-        gathered = [all_gather_var(torch.as_tensor(np.ascontiguousarray(a)))[0].numpy() for a in mine]
-        tick = dict(ids=gathered[0], xs=gathered[1], ys=gathered[2], qids=gathered[3], rects=tuple(gathered[4:]))
-        # every rank now holds the same (reordered) tick: identical index on all ranks
-        offs, ids, (foffs, fids) = _partial_for_rank(tick, rank, world)
-        counts, _ = all_gather_var(torch.as_tensor(np.diff(offs)))
-        allids, sizes = all_gather_var(torch.as_tensor(ids))
-        counts = counts.numpy().reshape(world, -1)
-        parts, base = [], 0
-        for r in range(world):
-            parts.append((np.concatenate([[0], np.cumsum(counts[r])]), allids.numpy()[base:base + sizes[r]]))
-            base += sizes[r]
-        moffs, mids = merge_partials(parts)
-        ok = np.array_equal(moffs, foffs) and np.array_equal(mids, fids)
-        ok = ok and all(len(p[1]) > 0 for p in parts)  # both ranks did real work
+        # uneven contiguous slices of the updates and the queries (rank 0 issues more queries)
+        ob = [0, n // 3, n] if world == 2 else [r * n // world for r in range(world + 1)]
+        qb = [0, 2 * m // 3, m] if world == 2 else [r * m // world for r in range(world + 1)]
+        o0, o1, q0, q1 = ob[rank], ob[rank + 1], qb[rank], qb[rank + 1]
+        eng = ShardedEngine(MethodConfig(method="quad", th_quad=64), partial_tick=_stub_partial_tick)
+        (offs, ids), _ = eng.process_shard(full["ids"][o0:o1], full["xs"][o0:o1], full["ys"][o0:o1],
+                                           *(r_[q0:q1] for r_ in full["rects"]))
+        eng.close()
+        # the complete lists of this rank's queries: the unsharded tick's rows q0..q1
+        ref = qo.run_tick(full["ids"], full["xs"], full["ys"], full["qids"], *full["rects"], th_quad=64)
+        want_off = ref.offsets[q0:q1 + 1] - ref.offsets[q0]
+        want_ids = ref.result_ids[ref.offsets[q0]:ref.offsets[q1]]
+        ok = np.array_equal(offs, want_off) and np.array_equal(ids, want_ids)
+        # the routing really moved lists: some of this rank's results came from the other rank's leaves
+        mine = _partial_for_rank(dict(full), rank, world)
+        local = np.diff(mine[0])[q0:q1].sum()
+        ok = ok and 0 < local < len(want_ids)
         out.put((rank, bool(ok)))
     finally:
         dist.destroy_process_group()
