@@ -122,9 +122,11 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
   unsigned long long imn = ~0ull, imx = 0ull;  // id range (rank mode keys)
   int bad = 0, notid = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += 4 * stride) {
+  // warp-uniform trip count (the next-id shuffle below needs every lane of the warp)
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 - lane_id() < n; i0 += 4 * stride) {
     double x[4], y[4];
     int64_t v[4], nx[4];
+    const bool last_lane = lane_id() == 31;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int64_t i = i0 + u * stride;
@@ -132,7 +134,13 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {
       x[u] = ok ? d.xs[i] : 0.0;
       y[u] = ok ? d.ys[i] : 0.0;
       v[u] = ok ? d.ids[i] : 0;
-      nx[u] = (i + 1 < n) ? d.ids[i + 1] : 0x7fffffffffffffffll;
+      // the next row's id: the next lane's (consecutive rows per warp); the warp's last lane loads it
+      nx[u] = (last_lane && i + 1 < n) ? d.ids[i + 1] : 0x7fffffffffffffffll;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t nb = __shfl_down_sync(0xffffffffu, v[u], 1);
+      if (!last_lane) nx[u] = nb;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -335,6 +343,7 @@ __global__ void __launch_bounds__(256) k_cell_level(const Dev d) {
   const int ld = h->l_deep, lmax = h->l_max, F = h->F;
   const uint32_t th = (uint32_t)h->th;
   TJ_GRID_STRIDE(c, Z) {
+    // (loading every ancestor's count at once measured slower: most cells stop well above l_deep)
     int lev = ld;
     for (int l = 1; l <= ld; ++l) {
       const uint32_t cnt = node_count(d, F, l, (uint32_t)(c >> (2 * (ld - l))));
@@ -412,10 +421,21 @@ __global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
   if (h->abort) return;
   const int64_t n = h->n;
   const int sh = 2 * (h->l_max - h->l_deep);
-  if (h->key_sorted) {  // keyed lists: the objects enter the stable leaf sort in id order
-    TJ_GRID_STRIDE(j, n) d.okey[0][j] = d.zmap[d.code[d.order[j]] >> sh] & kPayloadMask;
-  } else {
-    TJ_GRID_STRIDE(i, n) d.okey[0][i] = d.zmap[d.code[i] >> sh] & kPayloadMask;
+  const bool keyed = h->key_sorted;  // keyed lists: the objects enter the stable leaf sort in id order
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j0 < n; j0 += 4 * stride) {
+    uint32_t cd[4];  // four code -> zmap chains in flight
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = j0 + u * stride;
+      cd[u] = j < n ? d.code[keyed ? d.order[j] : j] : 0u;
+    }
+    uint32_t z[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) z[u] = j0 + u * stride < n ? d.zmap[cd[u] >> sh] : 0u;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (j0 + u * stride < n) d.okey[0][j0 + u * stride] = z[u] & kPayloadMask;
   }
 }
 
@@ -749,7 +769,8 @@ __global__ void __launch_bounds__(256) k_query_fill(const Dev d) {
     const int n = d.nsub[q];
     if (n == 0) continue;
     // the clip again (geometry.py:80-88): re-reading the query costs what reading a stored clip
-    // would, and the count pass then writes no per-query rect
+    // would, and the count pass then writes no per-query rect.  (Prefetching the next query's
+    // count, rect and handoff while placing this one's pairs measured 6% slower: 64 registers.)
     Rect4 r;
     r.xa = d.qxa[q];
     r.ya = d.qya[q];
@@ -1593,11 +1614,15 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
       // ---- A: bits -> leaf positions, at their output positions in sa
       for (int32_t c0 = slo; c0 < shi; c0 += 32) {
         const int32_t s = c0 + lane;
-        int nbw = 0, obase = 0;
+        int nbw = 0, obase = 0, cs = 0;
         int64_t wof = -1;
         uint32_t tail = 0;
-        if (s < shi && d.sq_count[s] > 0) {
-          const int2 le = d.sq_le[s];
+        int2 le = make_int2(0, 0);
+        if (s < shi) {  // count and slot loaded together (no dependent round trip)
+          cs = d.sq_count[s];
+          le = d.sq_le[s];
+        }
+        if (cs > 0) {
           const int32_t leaf = le.x;
           const int4 li = d.linfo[leaf];
           const int nobj = li.y;

@@ -8,9 +8,9 @@ import csv
 import sys
 
 
-def main():
-    path = sys.argv[1]
-    back = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+def one_tick(path, back=6):
+    """[(kernel, launches, us, dram MB)] of the tick that starts at the back-th k_mbr from the end
+    (the bench's last launches are the serial-sort context's ticks)."""
     rows = list(csv.reader(ln for ln in open(path) if ln.startswith('"')))
     hdr, rows = rows[0], rows[1:]
     ki, mi, vi, ii = (hdr.index(k) for k in ("Kernel Name", "Metric Name", "Metric Value", "ID"))
@@ -28,10 +28,18 @@ def main():
         e[0] += 1
         e[1] += v.get("gpu__time_duration.sum", 0.0) / 1e3
         e[2] += (v.get("dram__bytes_read.sum", 0.0) + v.get("dram__bytes_write.sum", 0.0)) / 1e6
+    return b - a, [(k, e[0], e[1], e[2]) for k, e in agg.items()]
+
+
+def main():
+    path = sys.argv[1]
+    back = int(sys.argv[2]) if len(sys.argv) > 2 else 6
+    n, rows = one_tick(path, back)
+    agg = {k: [c, us, mb] for k, c, us, mb in rows}
     tot = sum(e[1] for e in agg.values())
-    print(f"one tick: {b - a} launches, {tot:.1f} us serialised")
+    print(f"one tick: {n} launches, {tot:.1f} us serialised")
     for k, e in sorted(agg.items(), key=lambda x: -x[1][1])[:30]:
-        print(f"{k[:58]:58s} n={e[0]:2d} {e[1]:8.1f} us {100 * e[1] / tot:5.1f}%  {e[2]:8.1f} MB  {e[2] / e[1] / 1e3 if e[1] else 0:5.2f} TB/s")
+        print(f"{k[:58]:58s} n={e[0]:2d} {e[1]:8.1f} us {100 * e[1] / tot:5.1f}%  {e[2]:8.1f} MB  {e[2] / e[1] if e[1] else 0:5.2f} TB/s")
 
 
 if __name__ == "__main__":

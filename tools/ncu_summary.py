@@ -77,23 +77,18 @@ def summarize_rep(rep: str) -> dict:
 
 
 def summarize_launches(path: str) -> dict:
-    rows = list(csv.reader(open(path)))
-    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
-    h = rows[hi]
-    ki, vi = h.index("Kernel Name"), h.index("Metric Value")
-    seq = [(r[ki].split("(")[0].replace("void ", "").strip(), float(r[vi].replace(",", "")))
-           for r in rows[hi + 1:] if len(r) > vi]
-    starts = [i for i, (n, _) in enumerate(seq) if n.endswith("k_mbr")]
-    last = seq[starts[-1]:] if starts else seq
-    tot = sum(v for _, v in last)
-    agg = collections.defaultdict(float)
-    cnt = collections.Counter()
-    for n, v in last:
-        agg[n] += v
-        cnt[n] += 1
-    return {"tick_total_us": tot / 1e3, "launches": len(last),
-            "kernels": [{"kernel": n, "us": v / 1e3, "share": v / tot, "launches": cnt[n]}
-                        for n, v in sorted(agg.items(), key=lambda x: -x[1])]}
+    """Per-kernel time share of one tick of the bench's timed ticks (tools/launch_table.py)."""
+    import os
+    import sys
+
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from launch_table import one_tick
+
+    n, rows = one_tick(path)
+    tot = sum(us for _, _, us, _ in rows)
+    return {"tick_total_us": tot, "launches": n,
+            "kernels": [{"kernel": k, "us": us, "share": us / tot, "launches": c, "dram_mb": mb}
+                        for k, c, us, mb in sorted(rows, key=lambda x: -x[2])]}
 
 
 def main():
