@@ -65,6 +65,7 @@ struct tj_ctx {
   // objects
   DBuf code, okey0, okey1, oval0, oval1, sx, sy, tx, ty;
   DBuf loff, presence, prespre, order;  // keyed lists (ids that are not the rows)
+  DBuf crow;                            // sharded ticks: compacted rows of own-leaf objects
   // index
   DBuf linfo, pyr, clev, zmap, lcode, lnobj, lobase, lnisq, lncov, lsbase, lwoff, lubase;
   // queries
@@ -205,6 +206,7 @@ int prepare_static(tj_ctx* c, int64_t n, int64_t m) {
   ENS(sy, n * 8 + 16);
   ENS(tx, n * 8);
   ENS(ty, n * 8);
+  if (c->shard_n > 1) ENS(crow, n * 4);
   if (c->key_req) {
     ENS(loff, n * 4);
     ENS(presence, (int64_t(1) << (kKeyBits - 5)) * 4 + 64);
@@ -321,6 +323,7 @@ void fill_dev(tj_ctx* c, const int64_t* ids, const double* xs, const double* ys,
   d.presence = P<uint32_t>(c->presence);
   d.pres_pre = P<int32_t>(c->prespre);
   d.order = P<int32_t>(c->order);
+  d.crow = P<int32_t>(c->crow);
   d.leaf_cur = P<int32_t>(c->leafcur);
   d.leaf_cnt = P<int4>(c->leafcnt);
   d.unit_leaf = P<int32_t>(c->unitleaf);
@@ -364,7 +367,14 @@ int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
     k_key_order<<<Gn, 256, 0, st>>>(d);
     launched += 8;
   }
-  k_obj_keys<<<Gn, 256, 0, st>>>(d);
+  const bool compact = c->shard_n > 1 && !c->sort_xy;
+  if (compact) {  // sharded: own-leaf objects only, compacted in order (keys + rows)
+    scan_launch(sp, OwnObjIn{d}, OwnObjOut{d}, &h->n, h, &h->n_sort, st);
+    launched += 3;
+  } else {
+    k_obj_keys<<<Gn, 256, 0, st>>>(d);
+    launched += 1;
+  }
   double* bx[2] = {P<double>(c->sx), P<double>(c->tx)};
   double* by[2] = {P<double>(c->sy), P<double>(c->ty)};
   const double *xin = d.xs, *yin = d.ys;
@@ -374,8 +384,9 @@ int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
     const int ob = (P_ - 1 - p) & 1;  // the last pass lands in (sx, sy)
     uint32_t* kout = last ? nullptr : d.okey[dst];
     // first pass: the input rows, or (keyed lists, ids not increasing) the rows in id order
-    const int32_t* vin = p == 0 ? (c->key_req ? (const int32_t*)d.order : nullptr) : d.oval[src];
-    const int gate = p == 0 && c->key_req ? 1 : 0;
+    const int32_t* vin = p == 0 ? (compact ? (const int32_t*)d.crow : (c->key_req ? (const int32_t*)d.order : nullptr))
+                                : d.oval[src];
+    const int gate = p == 0 && c->key_req && !compact ? 1 : 0;
     if (c->sort_xy) {
       radix_pass<true>(c, st, sp, ArrKey{d.okey[src]}, vin, kout, d.oval[dst], xin, yin, bx[ob], by[ob], &h->n,
                        kRadixBits * p, gate);
@@ -383,7 +394,7 @@ int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
       yin = by[ob];
     } else {
       radix_pass<false>(c, st, sp, ArrKey{d.okey[src]}, vin, kout, d.oval[dst], nullptr, nullptr, nullptr, nullptr,
-                        &h->n, kRadixBits * p, gate);
+                        &h->n_sort, kRadixBits * p, gate);
     }
   }
   if (c->key_req) {  // keyed lists: every leaf position's id offset
@@ -395,7 +406,7 @@ int sort_objects(tj_ctx* c, cudaStream_t st, const ScanPlan& sp) {
     k_gather<double><<<Gn, 256, 0, st>>>(d, d.ys, d.sy);
   }
   // 5 launches per radix pass (upsweep + 3-kernel scan + downsweep)
-  return launched + 1 + 5 * P_ + (c->sort_xy ? 0 : 2);
+  return launched + 5 * P_ + (c->sort_xy ? 0 : 2);
 }
 
 // The per-tick launch sequence, in stages (index build, query scatter, join
@@ -421,11 +432,14 @@ int launch_stage(tj_ctx* c, int stage) {
       cudaMemsetAsync(d.leaf_cur, 0, c->cap_L * 2 * 4, st);
       cudaMemsetAsync(d.leaf_cnt, 0, c->cap_L * sizeof(int4), st);
       if (c->reuse) {  // adaptive: the old tree, leaf counts recounted by the check pass
-        scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
-                    st);
-        if (c->shard_n > 1) {
+        if (c->shard_n > 1) {  // own leaves first: their blocks are the only ones sorted
           scan_launch(sp, LeafWeightIn{d.leaf_nobj}, PrefOut{d.leaf_wpre}, &h->L, h, &h->shard_total, st);
           k_shard_mark<<<Gbig, 256, 0, st>>>(d);
+          scan_launch(sp, OwnNobjIn{d.leaf_nobj, d.leaf_active}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h,
+                      (int64_t*)nullptr, st);
+        } else {
+          scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
+                      st);
         }
         return 3 + (c->shard_n > 1 ? 4 : 0);
       }
@@ -450,11 +464,15 @@ int launch_stage(tj_ctx* c, int stage) {
       }
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
-      scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
-                  st);
-      if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range, before the scatter
+      if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range, before the scatter,
+                             // and block bases over its own leaves (only their objects are sorted)
         scan_launch(sp, LeafWeightIn{d.leaf_nobj}, PrefOut{d.leaf_wpre}, &h->L, h, &h->shard_total, st);
         k_shard_mark<<<Gbig, 256, 0, st>>>(d);
+        scan_launch(sp, OwnNobjIn{d.leaf_nobj, d.leaf_active}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h,
+                    (int64_t*)nullptr, st);
+      } else {
+        scan_launch(sp, ArrIn<int32_t>{d.leaf_nobj}, ExclOut<int32_t>{d.leaf_obase}, &h->L, h, (int64_t*)nullptr,
+                    st);
       }
       // 3 launches per scan
       return (c->ug_sf ? 11 : 12 + (c->fused_pyr ? (F + kPyrSpan - 1) / kPyrSpan : F)) + (c->shard_n > 1 ? 4 : 0);
@@ -530,6 +548,7 @@ void init_hdr(tj_ctx* c, int64_t n, int64_t m) {
   H.grid_sf = c->ug_sf;
   H.shard_rank = c->shard_rank;
   H.shard_n = c->shard_n;
+  H.n_sort = n;  // (sharded: the own-leaf compaction overwrites it)
   H.id_kmin = ~0ull;
   H.id_kmax = 0ull;
   H.key_req = c->key_req ? 1 : 0;
@@ -964,7 +983,7 @@ int tj_destroy(tj_ctx* c) {
   if (c->st) cudaStreamSynchronize(c->st);
   drop_graphs(c);
   DBuf* all[] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb, &c->code, &c->okey0, &c->okey1,
-                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->loff, &c->presence, &c->prespre, &c->order, &c->pyr, &c->clev,
+                 &c->oval0, &c->oval1, &c->sx, &c->sy, &c->tx, &c->ty, &c->loff, &c->presence, &c->prespre, &c->order, &c->crow, &c->pyr, &c->clev,
                  &c->zmap, &c->lcode, &c->lnobj, &c->lobase, &c->lnisq, &c->lncov, &c->lsbase, &c->lwoff,
                  &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qpos, &c->qwin, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,

@@ -44,6 +44,7 @@ struct Dev {
   uint32_t* presence;   // one bit per id offset (2^28 bits): duplicate detection and id ranks
   int32_t* pres_pre;    // exclusive prefix of the presence words' popcounts
   int32_t* order;       // id rank -> input row (key_sorted ticks)
+  int32_t* crow;        // sharded ticks: the rows of the objects in own leaves, compacted in sort order
   double* sx;
   double* sy;
   // index
@@ -439,6 +440,36 @@ __global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {
   }
 }
 
+// Sharded ticks (§8e): only the objects in this rank's leaves are sorted.  A
+// scan over the objects (in input order, or id order for keyed lists) flags
+// those whose leaf is owned and compacts their leaf keys and rows, in order, so
+// the stable sort sees them as the unsharded sort would.
+struct OwnObjIn {
+  Dev d;
+  __device__ int64_t operator()(int64_t j) const {
+    const DevHdr* h = d.h;
+    const int32_t row = h->key_sorted ? d.order[j] : (int32_t)j;
+    const uint32_t leaf = d.zmap[d.code[row] >> (2 * (h->l_max - h->l_deep))] & kPayloadMask;
+    return d.leaf_active[leaf] ? 1 : 0;
+  }
+};
+struct OwnObjOut {
+  Dev d;
+  __device__ void operator()(int64_t j, int64_t ex, int64_t v) const {
+    if (!v) return;
+    const DevHdr* h = d.h;
+    const int32_t row = h->key_sorted ? d.order[j] : (int32_t)j;
+    d.okey[0][ex] = d.zmap[d.code[row] >> (2 * (h->l_max - h->l_deep))] & kPayloadMask;
+    d.crow[ex] = row;
+  }
+};
+// leaf object counts of own leaves only (the compacted blocks' bases)
+struct OwnNobjIn {
+  const int32_t* nobj;
+  const uint8_t* active;
+  __device__ int64_t operator()(int64_t r) const { return active[r] ? nobj[r] : 0; }
+};
+
 // ---- keyed lists (object ids that are not the input rows) ------------------
 // The reference sorts every result list by id (decode.py:117, np.sort in
 // merge_results).  When ids are not the rows, the device instead keeps every
@@ -508,7 +539,7 @@ __global__ void __launch_bounds__(256) k_key_order(const Dev d) {
 __global__ void __launch_bounds__(256) k_key_loff(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort || !h->key_mode) return;
-  const int64_t n = h->n, id_min = h->id_min;
+  const int64_t n = h->n_sort, id_min = h->id_min;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
     int32_t r[4];
@@ -530,7 +561,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_gather(const Dev d, const T* __restrict__ src, T* __restrict__ dst) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  const int64_t n = h->n;
+  const int64_t n = h->n_sort;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t p0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p0 < n; p0 += 4 * stride) {
     int32_t r[4];  // four independent gathers in flight per thread
@@ -1184,7 +1215,10 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
     __syncthreads();
     const uint32_t divm = (65536u + (uint32_t)nbt - 1u) / (uint32_t)nbt;  // it / nbt for it < 65536 / 16
     const Rect4* erect = d.erect + sbase;
-    if (kJoinTPS && table) {
+    // (multi-tile leaves — objects pinned at l_max, many per bucket — keep one thread per (subquery,
+    // block) item: their many ambiguous bits serialise a subquery's fix-ups in one lane; at config E
+    // the per-subquery mapping made the join 2x slower)
+    if (kJoinTPS && table && n_ot == 1) {
       // ---- one thread per subquery: its row of the tile, two blocks per step (paired 8-byte table
       // lookups of rows k and k + 1), its popcount in a register; no shared-memory staging, no atomics
       const uint2* TX = reinterpret_cast<const uint2*>(S.tab);
@@ -1339,7 +1373,9 @@ __global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
   if (lane == 0 && covres) atomicAdd(&h->cov_results, covres);
 }
 
-// per-slot result counts in slot (= output) order
+// per-slot result counts in slot (= output) order.  (Reading them straight inside the slot-offset
+// scan instead — its reduce and down-sweep passes each doing the random entry lookups — measured
+// 0.11 ms slower per tick at C5.)
 __global__ void __launch_bounds__(256) k_slot_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
