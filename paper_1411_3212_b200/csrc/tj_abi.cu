@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <functional>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -52,6 +53,7 @@ struct tj_ctx {
   bool fused_pyr = true;  // TJ_FUSED_PYR=0: one launch per pyramid level
   int ug_sf = 0;  // method "ug": cells per side (cfg.l_max then holds ceil(log2) of it)
   int join_blocks = 4;  // resident k_join CTAs per SM (occupancy API)
+  int decode_blocks = TJ_DQ_MINB;  // resident k_decode_query CTAs per SM (occupancy API)
   cudaStream_t st = nullptr;
   cudaStream_t side = nullptr;             // object sort, concurrent with the query scatter
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
@@ -115,6 +117,9 @@ struct tj_ctx {
   // multi-GPU data plane (tj_comm_init / tj_comm_init_local, tj_tick_sharded)
   Transport* comm = nullptr;
   DBuf pcnt, rcnt, sstart, moff, sconst, rids, mids, mscratch;
+  // query routing: own queries, their destination masks / places, send and receive rects
+  DBuf oq[4], qmask, packpos, dcnt, sq[4], rq[4], gcnt, gstart;
+  std::function<int()> after_build;  // run between the index build and the rest of a tick
 };
 
 namespace {
@@ -515,9 +520,9 @@ int launch_stage(tj_ctx* c, int stage) {
       return 7;
     case 5:  // ---- K4: decode + canonical lists (its own stage: timed alone) ----
       // the CTAs its register budget lets reside; the instantiations for the other id modes return at once
-      k_decode_query<kIdsRows><<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);
-      k_decode_query<kIdsKeyed><<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);
-      k_decode_query<kIdsLookup><<<c->num_sms * TJ_DQ_MINB, kDQThreads, 0, st>>>(d);
+      k_decode_query<kIdsRows><<<c->num_sms * c->decode_blocks, kDQThreads, 0, st>>>(d);
+      k_decode_query<kIdsKeyed><<<c->num_sms * c->decode_blocks, kDQThreads, 0, st>>>(d);
+      k_decode_query<kIdsLookup><<<c->num_sms * c->decode_blocks, kDQThreads, 0, st>>>(d);
       return 3;
     default:  // ---- lists that need a sort by id ----------------------------
       k_merge_big<<<c->num_sms * 2, 256, 0, st>>>(d);
@@ -670,9 +675,16 @@ int run_tick(tj_ctx* c, int64_t* launches) {
       if ((rc = stage(kSortStage, ss))) return rc;
       cudaEventRecord(c->ev[8], ss);
     }
-    if (s == 2) cudaStreamWaitEvent(c->st, c->ev[8], 0);  // join: the join needs both
+    // the join needs the sorted objects; its preparation (stage 2: word / unit offsets from the
+    // directory) does not, so it runs while the sort finishes.  Stage 2's event is recorded once
+    // the sort has joined, so it marks the join's start.
+    if (s == 3) {
+      cudaStreamWaitEvent(c->st, c->ev[8], 0);
+      cudaEventRecord(c->ev[kStageEvent[2]], c->st);
+    }
     if ((rc = stage(s, c->st))) return rc;
-    cudaEventRecord(c->ev[kStageEvent[s]], c->st);
+    if (s != 2) cudaEventRecord(c->ev[kStageEvent[s]], c->st);
+    if (s == 0 && c->after_build && (rc = c->after_build())) return rc;  // sharded: route the queries
   }
   return check_launch(c);
 }
@@ -970,6 +982,11 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
                        (int)radix_smem_bytes<false>());
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->join_blocks, k_join, kJT, sizeof(JoinSmem));
   if (c->join_blocks < 1) c->join_blocks = 1;
+  // the decode's grid: exactly its resident CTAs (a persistent grid-stride kernel)
+  // (no shared-memory carveout preference: asking for the maximum shrank L1, which the decode's
+  // leaf-position lookups live in — 40% slower at C5)
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c->decode_blocks, k_decode_query<kIdsRows>, kDQThreads, 0);
+  if (c->decode_blocks < 1) c->decode_blocks = 1;
 
   int64_t consts[8] = {(int64_t)kRadixDigits * 2 * c->num_sms, 0, 0, 0, 0, 0, 0, 0};
   cudaMemcpy(c->d_consts, consts, sizeof(consts), cudaMemcpyHostToDevice);
@@ -988,7 +1005,9 @@ int tj_destroy(tj_ctx* c) {
                  &c->lubase, &c->leafcnt, &c->nsub, &c->qsbase, &c->qpos, &c->qwin, &c->biglist, &c->sqle,
                  &c->sqcount, &c->ecount, &c->erect, &c->slotoff, &c->linfo, &c->leafcur, &c->unitleaf, &c->lactive, &c->lwpre, &c->bitmap,
                  &c->outids, &c->outoff, &c->scratch, &c->outoff32, &c->partial, &c->partial2, &c->rhist, &c->roffs, &c->sstate, &c->sstate2,
-                 &c->pcnt, &c->rcnt, &c->sstart, &c->moff, &c->sconst, &c->rids, &c->mids, &c->mscratch};
+                 &c->pcnt, &c->rcnt, &c->sstart, &c->moff, &c->sconst, &c->rids, &c->mids, &c->mscratch,
+                 &c->oq[0], &c->oq[1], &c->oq[2], &c->oq[3], &c->qmask, &c->packpos, &c->dcnt, &c->sq[0], &c->sq[1],
+                 &c->sq[2], &c->sq[3], &c->rq[0], &c->rq[1], &c->rq[2], &c->rq[3], &c->gcnt, &c->gstart};
   delete c->comm;
   c->comm = nullptr;
   for (DBuf* b : all)

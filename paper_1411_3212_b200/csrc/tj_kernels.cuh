@@ -1403,6 +1403,9 @@ constexpr int32_t kRowEnd = 0x7fffffff;
 #ifndef TJ_DQ_MINB
 #define TJ_DQ_MINB 10  // resident decode CTAs per SM the register budget is cut for
 #endif
+#ifndef TJ_DQ_SMEM_TMP
+#define TJ_DQ_SMEM_TMP 0  // 1: the warp merge's second buffer in shared memory (16 KB more per CTA: fewer resident CTAs; measured no faster at C20)
+#endif
 constexpr int kDQThreads = 128;
 constexpr int kDQWarps = kDQThreads / 32;
 constexpr int kDQStage = 1024;   // results staged per warp window
@@ -1485,6 +1488,75 @@ __device__ __forceinline__ void warp_bitonic(int32_t* a, int cnt) {
   __syncwarp();
 }
 
+// Warp merge of one list's k sorted runs (k <= 32; rs[j] = start of run j in
+// the list `a` of cq elements, rs[k] = cq): pairwise rounds, each a segmented
+// merge path — lane L produces outputs [L*cq/32, (L+1)*cq/32) of the round,
+// finding its place by a binary search on the merge diagonal of the pair it
+// starts in, then merging serially (one load per output, continuing into the
+// next pairs).  A merged pair occupies exactly its two inputs' range, so runs
+// only change their starts.  Rounds ping-pong between `a` and `tmp`; the last
+// one stores the ids to `out`.  O(n log k) work against O(n log^2 n) for a
+// bitonic sort of the concatenation (config C @20u: lists of 129..1024
+// results with ~6.5 runs, where the bitonic sort was 78% of the decode).
+template <typename IdOf>
+__device__ __forceinline__ void warp_merge_runs(int32_t* a, int32_t* tmp, int32_t* rs, int cq, int k,
+                                                int64_t* out, IdOf idof) {
+  const int lane = lane_id();
+  int32_t* src = a;
+  int32_t* dst = tmp;
+  int nr = k;
+  auto run_start = [&](int j) -> int { return j < nr ? rs[j] : cq; };
+  while (nr > 1) {
+    const int np = (nr + 1) >> 1;
+    const bool last = np == 1;
+    const int lo = (int)(((int64_t)lane * cq) >> 5), hi = (int)(((int64_t)(lane + 1) * cq) >> 5);
+    if (lo < hi) {
+      // the pair holding output lo: the last pair starting at or before it
+      int q = 0;
+      for (int step = 16; step > 0; step >>= 1)
+        if (q + step < np && rs[2 * (q + step)] <= lo) q += step;
+      int sA = rs[2 * q], eA = run_start(2 * q + 1), eB = run_start(2 * q + 2);
+      // merge path: l outputs from A among the first d of the pair
+      const int d = lo - sA, nA = eA - sA, nB = eB - eA;
+      int l = d > nB ? d - nB : 0, r = d < nA ? d : nA;
+      while (l < r) {
+        const int mid = (l + r) >> 1;
+        if (src[sA + mid] < src[eA + d - 1 - mid]) l = mid + 1;
+        else r = mid;
+      }
+      int ia = sA + l, ib = eA + (d - l);
+      int32_t ha = ia < eA ? src[ia] : 0x7fffffff, hb = ib < eB ? src[ib] : 0x7fffffff;
+      for (int p = lo; p < hi; ++p) {
+        while (p == eB) {  // into the next (non-empty) pair: both its runs start at their heads
+          ++q;
+          sA = eB;
+          eA = run_start(2 * q + 1);
+          eB = run_start(2 * q + 2);
+          ia = sA;
+          ib = eA;
+          ha = ia < eA ? src[ia] : 0x7fffffff;
+          hb = ib < eB ? src[ib] : 0x7fffffff;
+        }
+        const bool ta = ha < hb;
+        const int32_t v = ta ? ha : hb;
+        if (last) st_out(out + p, idof(v));
+        else dst[p] = v;
+        if (ta) ha = ++ia < eA ? src[ia] : 0x7fffffff;
+        else hb = ++ib < eB ? src[ib] : 0x7fffffff;
+      }
+    }
+    // the merged pairs' starts: run q of the next round starts where run 2q did
+    const int ns = 2 * lane < nr ? rs[2 * lane] : cq;
+    __syncwarp();
+    if (lane <= 32 - 1) rs[lane] = lane < np ? ns : cq;
+    __syncwarp();
+    nr = np;
+    int32_t* t = src;
+    src = dst;
+    dst = t;
+  }
+}
+
 template <typename T, typename Emit>
 __device__ __forceinline__ void warp_rank_merge(const T* src, int cnt, int k, int c, Emit emit) {
   const int lane = lane_id();
@@ -1560,6 +1632,10 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
   DevHdr* h = d.h;
   if (h->abort || id_mode_of(h) != kMode) return;
   __shared__ int32_t sbuf[kDQWarps][kDQStage];
+  __shared__ int32_t rsb[kDQWarps][33];  // run starts of the list a warp merges
+#if TJ_DQ_SMEM_TMP
+  __shared__ int32_t tmpb[kDQWarps][kDQStage];  // the merge rounds' second buffer
+#endif
   const bool mono = kMode != kIdsLookup || !h->not_monotone;
   const int64_t m = h->m;
   const int lane = lane_id(), wp = threadIdx.x >> 5;
@@ -1734,7 +1810,9 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
       for (int i = lane; i < (int)T; i += 32) st_out(d.out_ids + base + i, idof(sa[i]));
       __syncwarp();
       // ---- D: per query with 2..4 runs and <= 128 results, merge the runs by head (one lane per query)
-      if (act && cnt > 1) {
+      // (TJ_DEBUG bit 8: skip the merges — wrong lists, for timing the other phases only)
+      const bool merge_on = !(h->dbg & 8);
+      if (act && cnt > 1 && merge_on) {
         const int qs = (int)(qo - base);
         if (!mono) {  // ids not increasing with the input row: sorted by id in k_merge_big
           const int idx = atomicAdd(&h->n_big, 1);
@@ -1777,7 +1855,8 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         }
       }
       // other multi-run lists: the warp sorts them one at a time
-      unsigned rq = __ballot_sync(0xffffffffu, act && cnt > 1 && mono && k > 1 && (k > kLaneRuns || cnt > kLaneList));
+      unsigned rq = __ballot_sync(0xffffffffu, merge_on && act && cnt > 1 && mono && k > 1 &&
+                                                   (k > kLaneRuns || cnt > kLaneList));
       while (rq) {
         const int src = __ffs(rq) - 1;
         rq &= rq - 1;
@@ -1785,7 +1864,20 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         const int cq = (int)__shfl_sync(0xffffffffu, cnt, src);
         int64_t* out = d.out_ids + qoq;
         int32_t* lst = sa + (qoq - base);
-        if (cq <= 512) {  // sort in registers, then store
+        const int kq = __shfl_sync(0xffffffffu, k, src);
+        if (kq <= 32) {  // merge the runs (starts from the slot counts; empty runs are harmless)
+          const int32_t sq0 = __shfl_sync(0xffffffffu, s0, src);
+          const int c = lane < kq ? d.sq_count[sq0 + lane] : 0;
+          const int inc = warp_incl_scan(c);
+          int32_t* rs = rsb[wp];
+          rs[lane] = lane < kq ? inc - c : cq;
+          __syncwarp();
+#if TJ_DQ_SMEM_TMP
+          warp_merge_runs(lst, tmpb[wp], rs, cq, kq, out, idof);
+#else
+          warp_merge_runs(lst, reinterpret_cast<int32_t*>(d.scratch + qoq), rs, cq, kq, out, idof);
+#endif
+        } else if (cq <= 512) {  // sort in registers, then store
           if (cq <= 64) warp_bitonic<2>(lst, cq);
           else if (cq <= 128) warp_bitonic<4>(lst, cq);
           else if (cq <= 256) warp_bitonic<8>(lst, cq);

@@ -248,7 +248,7 @@ struct ExclOut {
 #define TJ_RADIX_BITS 8
 #endif
 constexpr int kRadixBits = TJ_RADIX_BITS;           // 8: 2 passes cover 16-bit keys (leaf ranks)
-constexpr int kRadixDigits = 1 << kRadixBits;       // 512
+constexpr int kRadixDigits = 1 << kRadixBits;       // 256 digits per pass
 constexpr int kRadixThreads = 256;
 constexpr int kRadixWarps = kRadixThreads / 32;
 constexpr int kRadixDPT = kRadixDigits > kRadixThreads ? kRadixDigits / kRadixThreads : 1;  // digits per thread

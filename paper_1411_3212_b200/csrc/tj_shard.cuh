@@ -106,6 +106,87 @@ __global__ void __launch_bounds__(256) k_merge_partials(int G, int64_t M, const 
   }
 }
 
+// Query routing (after the index build, which every rank builds identically):
+// each own query goes to the owners of the leaves its window touches — the
+// same clip, window and leaf enumeration the scatter does, with the owner of
+// a leaf from the weight prefix k_shard_mark uses.  Its ORIGINAL rect is
+// written into each destination's segment of the send buffers (segment j at
+// j * mr, the place from a per-destination counter, kept in packpos for the
+// merge); a query disjoint from the MBR goes nowhere (its list is empty).
+__device__ __forceinline__ int leaf_owner(const Dev& d, uint32_t r, int G) {
+  const DevHdr* h = d.h;
+  const int64_t T = h->shard_total > 0 ? h->shard_total : 1;
+  const int64_t mid = 2 * d.leaf_wpre[r] + (int64_t)d.leaf_nobj[r] + 1;
+  const int64_t o = (mid * G) / (2 * T);
+  return o < G ? (int)o : G - 1;
+}
+__global__ void __launch_bounds__(256) k_route(const Dev d, int64_t mr, int G, const double* __restrict__ qxa,
+                                               const double* __restrict__ qya, const double* __restrict__ qxb,
+                                               const double* __restrict__ qyb, double* sxa, double* sya,
+                                               double* sxb, double* syb, int32_t* packpos,
+                                               unsigned long long* dcnt, uint64_t* qmask) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const double xa = h->xa, ya = h->ya, xb = h->xb, yb = h->yb;
+  const double sx = h->sx_deep, sy = h->sy_deep;
+  const int wpos = h->wpos, hpos = h->hpos, ld = h->l_deep;
+  const uint32_t side = h->side_deep;
+  TJ_GRID_STRIDE(q, mr) {
+    const double a = qxa[q], b = qya[q], c = qxb[q], e = qyb[q];
+    double cxa = a < xa ? xa : a, cya = b < ya ? ya : b, cxb = c > xb ? xb : c, cyb = e > yb ? yb : e;
+    uint64_t mask = 0;
+    if (!(cxa > cxb || cya > cyb)) {
+      int4 w;
+      w.x = (int)cell_of(cxa, xa, sx, wpos, side);
+      w.y = (int)cell_of(cxb, xa, sx, wpos, side);
+      w.z = (int)cell_of(cya, ya, sy, hpos, side);
+      w.w = (int)cell_of(cyb, ya, sy, hpos, side);
+      if (is_small(w)) {
+        uint32_t key[4], rank[4];
+        const int ne = enum_small(w, ld, d.zmap, key, rank);
+        for (int k = 0; k < ne; ++k) mask |= 1ull << leaf_owner(d, rank[k], G);
+      } else {
+        enum_window(w.x, w.y, w.z, w.w, ld, d.zmap,
+                    [&](int, uint32_t, uint32_t rank) { mask |= 1ull << leaf_owner(d, rank, G); });
+      }
+    }
+    qmask[q] = mask;
+    for (uint64_t mm = mask; mm; mm &= mm - 1) {
+      const int j = __ffsll((long long)mm) - 1;
+      const int64_t pp = (int64_t)atomicAdd(&dcnt[j], 1ull);
+      packpos[(int64_t)j * mr + q] = (int32_t)pp;
+      const int64_t o = (int64_t)j * mr + pp;
+      sxa[o] = a;
+      sya[o] = b;
+      sxb[o] = c;
+      syb[o] = e;
+    }
+  }
+}
+
+// the returned partial lists of own query q, indexed like the merge wants them:
+// cnt[j][q], start[j][q] (0 where q was not routed to j)
+__global__ void __launch_bounds__(256) k_route_gather(int64_t mr, int G, const uint64_t* __restrict__ qmask,
+                                                      const int32_t* __restrict__ packpos,
+                                                      const int32_t* __restrict__ rcnt,
+                                                      const int64_t* __restrict__ rstart, int32_t* gcnt,
+                                                      int64_t* gstart) {
+  TJ_GRID_STRIDE(q, mr) {
+    const uint64_t mask = qmask[q];
+    for (int j = 0; j < G; ++j) {
+      const int64_t o = (int64_t)j * mr + q;
+      if ((mask >> j) & 1ull) {
+        const int64_t p = (int64_t)j * mr + packpos[o];
+        gcnt[o] = rcnt[p];
+        gstart[o] = rstart[p];
+      } else {
+        gcnt[o] = 0;
+        gstart[o] = 0;
+      }
+    }
+  }
+}
+
 }  // namespace tj
 
 // ---------------------------------------------------------------------------
@@ -309,11 +390,13 @@ struct LocalTransport : Transport {
   }
 };
 
-// the sharded tick: gather -> sharded device tick -> partials to home ranks -> device merge
+// the sharded tick: gather the objects -> index build -> route the queries to the owners of
+// their leaves -> the rank's leaf range -> partial lists back to the home ranks -> device merge
 int sharded_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats& S) {
   Transport& T = *c->comm;
   const int G = T.nranks, r = T.rank;
   int rc;
+  if (G > 31) return fail(c, TJ_E_INVALID_ARG, "at most 31 ranks");
   const int64_t mine[2] = {in->n_obj, in->n_q};
   std::vector<int64_t> all(2 * G), N(G), M(G), nd(G + 1, 0), md(G + 1, 0);
   if ((rc = T.exchange_host(c, mine, 2, all.data()))) return rc;
@@ -326,93 +409,149 @@ int sharded_tick(tj_ctx* c, const tj_tick_in* in, tj_tick_out* out, tj_stats& S)
   const int64_t n = nd[G], m = md[G], Mr = M[r];
   if (n >= (int64_t(1) << 28) || m > INT32_MAX / 2)
     return fail(c, TJ_E_INVALID_ARG, "sharded tick too large for 32-bit rows");
-  // 1. the full tick on every rank
-  if ((rc = ensure(c, c->ids, n * 8)) || (rc = ensure(c, c->xs, n * 8)) || (rc = ensure(c, c->ys, n * 8)) ||
-      (rc = ensure(c, c->qxa, m * 8)) || (rc = ensure(c, c->qya, m * 8)) || (rc = ensure(c, c->qxb, m * 8)) ||
-      (rc = ensure(c, c->qyb, m * 8)))
-    return rc;
-  DBuf* full[7] = {&c->ids, &c->xs, &c->ys, &c->qxa, &c->qya, &c->qxb, &c->qyb};
-  const void* src[7] = {in->obj_id, in->obj_x, in->obj_y, in->q_xa, in->q_ya, in->q_xb, in->q_yb};
-  for (int a = 0; a < 7; ++a) {
-    const bool obj = a < 3;
-    const int64_t cnt = obj ? N[r] : Mr, off = obj ? nd[r] : md[r];
-    char* slot = static_cast<char*>(full[a]->p) + off * 8;
-    const void* send = src[a];
+  // 1. every rank's objects gathered into the full set (the index is built on all of them)
+  if ((rc = ensure(c, c->ids, n * 8)) || (rc = ensure(c, c->xs, n * 8)) || (rc = ensure(c, c->ys, n * 8))) return rc;
+  DBuf* full[3] = {&c->ids, &c->xs, &c->ys};
+  const void* osrc[3] = {in->obj_id, in->obj_x, in->obj_y};
+  for (int a = 0; a < 3; ++a) {
+    char* slot = static_cast<char*>(full[a]->p) + nd[r] * 8;
+    const void* send = osrc[a];
     if (in->mem == TJ_MEM_HOST) {  // this rank's slice lands in its place of the full array first
-      if (cnt) TJ_CUDA(cudaMemcpyAsync(slot, src[a], cnt * 8, cudaMemcpyHostToDevice, c->st));
+      if (N[r]) TJ_CUDA(cudaMemcpyAsync(slot, osrc[a], N[r] * 8, cudaMemcpyHostToDevice, c->st));
       send = slot;
     }
-    if ((rc = T.allgatherv(c, send, full[a]->p, obj ? N.data() : M.data(), obj ? nd.data() : md.data(), 8)))
+    if ((rc = T.allgatherv(c, send, full[a]->p, N.data(), nd.data(), 8))) return rc;
+  }
+  // this rank's own queries on the device
+  const double* oq[4] = {in->q_xa, in->q_ya, in->q_xb, in->q_yb};
+  if (in->mem == TJ_MEM_HOST)
+    for (int a = 0; a < 4; ++a) {
+      if ((rc = ensure(c, c->oq[a], (size_t)Mr * 8 + 8))) return rc;
+      if (Mr) TJ_CUDA(cudaMemcpyAsync(c->oq[a].p, oq[a], Mr * 8, cudaMemcpyHostToDevice, c->st));
+      oq[a] = P<double>(c->oq[a]);
+    }
+  if (n == 0 || G == 1) {  // nothing to route: every list is complete on this rank (or empty)
+    c->shard_rank = 0;
+    c->shard_n = 1;
+    int64_t R = 0;
+    if ((rc = compute_tick(c, n, Mr, P<int64_t>(c->ids), P<double>(c->xs), P<double>(c->ys), oq[0], oq[1], oq[2],
+                           oq[3], S, R)))
       return rc;
+    S.n_objects = n;
+    S.n_queries = Mr;
+    return deliver(c, in->out_mem, out, Mr, R, n > 0, c->outoff, c->outids, c->scratch, S);
   }
   c->shard_rank = r;
   c->shard_n = G;
+  // 2. the queries go to the owners of the leaves their windows touch, right after the index build
+  //    (a rank receives at most every query of the tick once)
+  for (int a = 0; a < 4; ++a)
+    if ((rc = ensure(c, c->rq[a], (size_t)m * 8 + 8)) || (rc = ensure(c, c->sq[a], (size_t)G * Mr * 8 + 8)))
+      return rc;
+  if ((rc = ensure(c, c->packpos, (size_t)G * Mr * 4 + 4)) || (rc = ensure(c, c->qmask, (size_t)Mr * 8 + 8)) ||
+      (rc = ensure(c, c->dcnt, (size_t)G * 8)) || (rc = ensure(c, c->sconst, 64 * 8)))
+    return rc;
+  std::vector<int64_t> dc(G), sdq(G), rcq(G), rdq(G + 1, 0), mat((size_t)G * G);
+  for (int j = 0; j < G; ++j) sdq[j] = (int64_t)j * Mr;
+  int64_t m_recv = 0;
+  bool routed = false;
+  c->after_build = [&]() -> int {
+    // Collectives run once per tick on every rank: a capacity replay of one rank's tick (its own
+    // queries' sizes) reuses the queries it received, and an index build that aborted (identical
+    // on every rank: the index is) routes nothing — the replay that builds the index does.
+    int32_t ab = 0;
+    TJ_CUDA(cudaMemcpyAsync(&ab, &c->d_hdr->abort, sizeof(int32_t), cudaMemcpyDeviceToHost, c->st));
+    TJ_CUDA(cudaStreamSynchronize(c->st));
+    if (ab) return TJ_OK;
+    if (routed) {
+      TJ_CUDA(cudaMemcpyAsync(&c->d_hdr->m, &m_recv, sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+      TJ_CUDA(cudaStreamSynchronize(c->st));
+      return TJ_OK;
+    }
+    routed = true;
+    TJ_CUDA(cudaMemsetAsync(c->dcnt.p, 0, G * 8, c->st));
+    if (Mr)
+      k_route<<<grid_for(c, Mr), 256, 0, c->st>>>(c->dv, Mr, G, oq[0], oq[1], oq[2], oq[3], P<double>(c->sq[0]),
+                                                 P<double>(c->sq[1]), P<double>(c->sq[2]), P<double>(c->sq[3]),
+                                                 P<int32_t>(c->packpos), P<unsigned long long>(c->dcnt),
+                                                 P<uint64_t>(c->qmask));
+    TJ_CUDA(cudaMemcpyAsync(dc.data(), c->dcnt.p, G * 8, cudaMemcpyDeviceToHost, c->st));
+    TJ_CUDA(cudaStreamSynchronize(c->st));
+    int rc2;
+    if ((rc2 = T.exchange_host(c, dc.data(), G, mat.data()))) return rc2;
+    rdq[0] = 0;
+    for (int j = 0; j < G; ++j) {
+      rcq[j] = mat[(size_t)j * G + r];
+      rdq[j + 1] = rdq[j] + rcq[j];
+    }
+    m_recv = rdq[G];
+    for (int a = 0; a < 4; ++a)
+      if ((rc2 = T.alltoallv(c, c->sq[a].p, dc.data(), sdq.data(), c->rq[a].p, rcq.data(), rdq.data(), 8)))
+        return rc2;
+    // the rest of the tick runs on the received queries
+    TJ_CUDA(cudaMemcpyAsync(&c->d_hdr->m, &m_recv, sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    TJ_CUDA(cudaStreamSynchronize(c->st));
+    return TJ_OK;
+  };
   int64_t R = 0;
-  if ((rc = compute_tick(c, n, m, P<int64_t>(c->ids), P<double>(c->xs), P<double>(c->ys), P<double>(c->qxa),
-                         P<double>(c->qya), P<double>(c->qxb), P<double>(c->qyb), S, R)))
+  rc = compute_tick(c, n, m, P<int64_t>(c->ids), P<double>(c->xs), P<double>(c->ys), P<double>(c->rq[0]),
+                    P<double>(c->rq[1]), P<double>(c->rq[2]), P<double>(c->rq[3]), S, R);
+  c->after_build = nullptr;
+  if (rc) return rc;
+  // 3. each received query's partial list back to its home rank: counts, then the id runs
+  if ((rc = ensure(c, c->pcnt, (size_t)std::max<int64_t>(m_recv, 1) * 4)) ||
+      (rc = ensure(c, c->rcnt, (size_t)G * Mr * 4 + 4)) || (rc = ensure(c, c->sstart, (size_t)G * Mr * 8 + 8)) ||
+      (rc = ensure(c, c->gcnt, (size_t)G * Mr * 4 + 4)) || (rc = ensure(c, c->gstart, (size_t)G * Mr * 8 + 8)) ||
+      (rc = ensure(c, c->moff, (size_t)(Mr + 1) * 8)))
     return rc;
-  if (G == 1) {  // one rank: the tick's lists are already complete
-    S.n_objects = n;
-    S.n_queries = m;
-    return deliver(c, in->out_mem, out, m, R, n > 0, c->outoff, c->outids, c->scratch, S);
-  }
-  // 2. partial lists to the home ranks: per-query counts, then the id runs
-  if ((rc = ensure(c, c->pcnt, (size_t)std::max<int64_t>(m, 1) * 4)) ||
-      (rc = ensure(c, c->rcnt, (size_t)std::max<int64_t>(G * Mr, 1) * 4)) ||
-      (rc = ensure(c, c->sstart, (size_t)std::max<int64_t>(G * Mr, 1) * 8)) ||
-      (rc = ensure(c, c->moff, (size_t)(Mr + 1) * 8)) || (rc = ensure(c, c->sconst, 64 * 8)))
-    return rc;
-  if (m) k_partial_counts<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(c->outoff), P<int32_t>(c->pcnt), m);
-  std::vector<int64_t> bound(G + 1), scnt(G), sdis(G), rqc(G, Mr), rqd(G);
+  if (m_recv)
+    k_partial_counts<<<c->num_sms * 4, 256, 0, c->st>>>(P<int64_t>(c->outoff), P<int32_t>(c->pcnt), m_recv);
+  std::vector<int64_t> bound(G + 1), sid(G), sdid(G), rid(G), rdid(G + 1, 0);
   for (int j = 0; j <= G; ++j)
-    TJ_CUDA(cudaMemcpyAsync(&bound[j], P<int64_t>(c->outoff) + md[j], 8, cudaMemcpyDeviceToHost, c->st));
+    TJ_CUDA(cudaMemcpyAsync(&bound[j], P<int64_t>(c->outoff) + rdq[j], 8, cudaMemcpyDeviceToHost, c->st));
   TJ_CUDA(cudaStreamSynchronize(c->st));
   for (int j = 0; j < G; ++j) {
-    scnt[j] = bound[j + 1] - bound[j];
-    sdis[j] = bound[j];
-    rqd[j] = (int64_t)j * Mr;
+    sid[j] = bound[j + 1] - bound[j];
+    sdid[j] = bound[j];
   }
-  if ((rc = T.alltoallv(c, c->pcnt.p, M.data(), md.data(), c->rcnt.p, rqc.data(), rqd.data(), 4))) return rc;
-  std::vector<int64_t> mat((size_t)G * G), rc_ids(G), rd_ids(G + 1, 0);
-  if ((rc = T.exchange_host(c, scnt.data(), G, mat.data()))) return rc;
-  int64_t Rr = 0;
+  if ((rc = T.alltoallv(c, c->pcnt.p, rcq.data(), rdq.data(), c->rcnt.p, dc.data(), sdq.data(), 4))) return rc;
+  if ((rc = T.exchange_host(c, sid.data(), G, mat.data()))) return rc;
   for (int j = 0; j < G; ++j) {
-    rc_ids[j] = j == r ? 0 : mat[(size_t)j * G + r];  // (this rank's own lists are not sent)
-    rd_ids[j + 1] = rd_ids[j] + rc_ids[j];
-    Rr += mat[(size_t)j * G + r];
+    rid[j] = mat[(size_t)j * G + r];
+    rdid[j + 1] = rdid[j] + rid[j];
   }
-  if ((rc = ensure(c, c->rids, (size_t)std::max<int64_t>(rd_ids[G], 1) * 8)) ||
+  const int64_t Rr = rdid[G];
+  if ((rc = ensure(c, c->rids, (size_t)std::max<int64_t>(Rr, 1) * 8)) ||
       (rc = ensure(c, c->mids, (size_t)std::max<int64_t>(Rr, 1) * 8)) ||
       (rc = ensure(c, c->mscratch, (size_t)std::max<int64_t>(Rr, 1) * 4)))
     return rc;
-  // this rank's own partial lists stay where the tick wrote them (no self-copy)
-  const int64_t self_cnt = scnt[r];
-  scnt[r] = 0;
-  rc_ids[r] = 0;
-  if ((rc = T.alltoallv(c, c->outids.p, scnt.data(), sdis.data(), c->rids.p, rc_ids.data(), rd_ids.data(), 8)))
-    return rc;
-  // 3. merge on the device: per-source starts, query offsets, the union of the sorted runs
-  (void)self_cnt;
-  int64_t hconst[64] = {0};  // [0] = own queries, [1 + j] = where source j's runs are (device pointers)
+  if ((rc = T.alltoallv(c, c->outids.p, sid.data(), sdid.data(), c->rids.p, rid.data(), rdid.data(), 8))) return rc;
+  // 4. merge on the device: run starts per destination, own queries' offsets, the union
+  int64_t hconst[64] = {0};  // [0] own queries; [1 + j] source j's runs (device pointer); [32 + j] dc[j]
   hconst[0] = Mr;
-  if (G > 62) return fail(c, TJ_E_INVALID_ARG, "at most 62 ranks");
-  for (int j = 0; j < G; ++j)
-    hconst[1 + j] = j == r ? (int64_t)(uintptr_t)(P<int64_t>(c->outids) + bound[r])
-                           : (int64_t)(uintptr_t)(P<int64_t>(c->rids) + rd_ids[j]);
+  for (int j = 0; j < G; ++j) {
+    hconst[1 + j] = (int64_t)(uintptr_t)(P<int64_t>(c->rids) + rdid[j]);
+    hconst[32 + j] = dc[j];
+  }
   TJ_CUDA(cudaMemcpyAsync(c->sconst.p, hconst, sizeof(hconst), cudaMemcpyHostToDevice, c->st));
-  int64_t* d_M = P<int64_t>(c->sconst);
+  int64_t* dK = P<int64_t>(c->sconst);
   ScanPlan sp{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial), nullptr, c->scan_words};
   for (int j = 0; j < G; ++j)
     scan_launch(sp, ArrIn<int32_t>{P<int32_t>(c->rcnt) + (int64_t)j * Mr},
-                ExclOut<int64_t>{P<int64_t>(c->sstart) + (int64_t)j * Mr}, d_M, c->d_hdr, (int64_t*)nullptr, c->st);
-  scan_launch(sp, SumIn{P<int32_t>(c->rcnt), G, Mr}, ExclOut<int64_t>{P<int64_t>(c->moff)}, d_M, c->d_hdr,
+                ExclOut<int64_t>{P<int64_t>(c->sstart) + (int64_t)j * Mr}, dK + 32 + j, c->d_hdr, (int64_t*)nullptr,
+                c->st);
+  if (Mr)
+    k_route_gather<<<grid_for(c, Mr), 256, 0, c->st>>>(Mr, G, P<uint64_t>(c->qmask), P<int32_t>(c->packpos),
+                                                       P<int32_t>(c->rcnt), P<int64_t>(c->sstart),
+                                                       P<int32_t>(c->gcnt), P<int64_t>(c->gstart));
+  scan_launch(sp, SumIn{P<int32_t>(c->gcnt), G, Mr}, ExclOut<int64_t>{P<int64_t>(c->moff)}, dK, c->d_hdr,
               P<int64_t>(c->moff) + Mr, c->st);
   if (Mr)
-    k_merge_partials<<<c->num_sms * 8, 256, 0, c->st>>>(G, Mr, P<int32_t>(c->rcnt), P<int64_t>(c->sstart),
-                                                       reinterpret_cast<const int64_t* const*>(d_M + 1),
+    k_merge_partials<<<c->num_sms * 8, 256, 0, c->st>>>(G, Mr, P<int32_t>(c->gcnt), P<int64_t>(c->gstart),
+                                                       reinterpret_cast<const int64_t* const*>(dK + 1),
                                                        P<int64_t>(c->moff), P<int64_t>(c->mids));
   if ((rc = check_launch(c))) return rc;
-  S.kernel_launches += (m ? 1 : 0) + 3 * (G + 1) + (Mr ? 1 : 0);
+  S.kernel_launches += 2 + (m_recv ? 1 : 0) + 3 * (G + 1) + (Mr ? 2 : 0);
   S.n_objects = n;
   S.n_queries = Mr;
   S.results_total = Rr;

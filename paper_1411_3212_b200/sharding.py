@@ -95,13 +95,16 @@ class ShardedEngine:
     """One rank of a G-GPU QUAD tick (torch.distributed process group already initialised).
 
     partial_tick=None: the native `tj_tick_sharded` over an NCCL communicator the ranks set
-    up here (rank 0's unique id broadcast over the process group).  Otherwise
-    partial_tick(ids, xs, ys, qxa, qya, qxb, qyb, rank, world) -> (offsets[m + 1], ids) must
-    return the full tick's per-query lists restricted to the rank's leaves (what the device
-    computes after `k_shard_mark`), and the gather / routing / merge run on the host with
-    torch.distributed (the restatement of csrc/tj_shard.cuh the gloo tests exercise)."""
+    up here (rank 0's unique id broadcast over the process group).  Otherwise the protocol
+    runs on the host with torch.distributed (the restatement of csrc/tj_shard.cuh the gloo
+    tests exercise) around two caller-supplied device stand-ins:
+    route(ids, xs, ys, qxa, qya, qxb, qyb, rank, world) -> per own query a bit mask of the
+    ranks owning leaves it touches (`k_route`), and
+    partial_tick(ids, xs, ys, qxa, qya, qxb, qyb, rank, world) -> (offsets[m + 1], ids): the
+    lists of the given (received) queries restricted to the rank's leaves (what the device
+    computes after `k_shard_mark`)."""
 
-    def __init__(self, cfg, device: Optional[int] = None, group=None, partial_tick=None):
+    def __init__(self, cfg, device: Optional[int] = None, group=None, partial_tick=None, route=None):
         import torch.distributed as dist
 
         cfg.validate()
@@ -111,6 +114,7 @@ class ShardedEngine:
         self.world = dist.get_world_size(group)
         self.device = cfg.device if device is None else device
         self.partial_tick = partial_tick
+        self.route = route
         self.ctx = None
         if partial_tick is None:
             from . import _native
@@ -129,40 +133,57 @@ class ShardedEngine:
         return self._host_protocol(ids, xs, ys, qxa, qya, qxb, qyb), None
 
     def _host_protocol(self, ids, xs, ys, qxa, qya, qxb, qyb):
+        """The host restatement of csrc/tj_shard.cuh's sharded_tick (G > 1)."""
         import torch
         import torch.distributed as dist
 
         G, r, grp = self.world, self.rank, self.group
-        cols = [torch.as_tensor(np.ascontiguousarray(a)) for a in (ids, xs, ys, qxa, qya, qxb, qyb)]
-        # 1. the full tick on every rank (slices concatenated in rank order)
-        full = [all_gather_var(c, grp)[0].numpy() for c in cols]
-        msz = torch.tensor([len(qxa)], dtype=torch.int64)
-        msizes = [torch.zeros_like(msz) for _ in range(G)]
-        dist.all_gather(msizes, msz, group=grp)
-        M = [int(x.item()) for x in msizes]
-        md = np.concatenate([[0], np.cumsum(M)]).astype(np.int64)
-        # 2. this rank's leaves
-        poffs, pids = self.partial_tick(*full, r, G)
+        # 1. every rank's objects gathered into the full set (slices concatenated in rank order)
+        objs = [all_gather_var(torch.as_tensor(np.ascontiguousarray(a)), grp)[0].numpy() for a in (ids, xs, ys)]
+        own = [np.ascontiguousarray(a, np.float64) for a in (qxa, qya, qxb, qyb)]
+        mr = len(own[0])
+        # 2. every own query to the ranks owning the leaves it touches (k_route), grouped per destination
+        mask = np.asarray(self.route(*objs, *own, r, G), np.uint64) if mr else np.zeros(0, np.uint64)
+        dest = [np.flatnonzero((mask >> np.uint64(j)) & np.uint64(1)) for j in range(G)]
+        scnt = torch.tensor([len(x) for x in dest], dtype=torch.int64)
+        rcnt_q = torch.empty(G, dtype=torch.int64)
+        dist.all_to_all_single(rcnt_q, scnt, group=grp)
+        recv = []
+        for a in own:
+            send = torch.as_tensor(np.concatenate([a[x] for x in dest]) if mr else np.zeros(0))
+            out = torch.empty(int(rcnt_q.sum()), dtype=torch.float64)
+            dist.all_to_all_single(out, send, output_split_sizes=rcnt_q.tolist(), input_split_sizes=scnt.tolist(),
+                                   group=grp)
+            recv.append(out.numpy())
+        # 3. this rank's leaves, for the queries it received
+        poffs, pids = self.partial_tick(*objs, *recv, r, G)
         poffs = np.asarray(poffs, np.int64)
-        # 3. partial lists to the home ranks: per-query counts, then the id runs
-        counts = torch.as_tensor(np.diff(poffs))
-        rcnt = torch.empty(G * M[r], dtype=torch.int64)
-        dist.all_to_all_single(rcnt, counts, output_split_sizes=[M[r]] * G, input_split_sizes=M, group=grp)
-        bounds = poffs[md]
-        scnt = torch.as_tensor(np.diff(bounds))
-        rsz = torch.empty(G, dtype=torch.int64)
-        dist.all_to_all_single(rsz, scnt, group=grp)
-        rids = torch.empty(int(rsz.sum()), dtype=torch.int64)
+        # 4. each received query's partial list back to its home rank: counts, then the id runs
+        rq = rcnt_q.tolist()
+        rd = np.concatenate([[0], np.cumsum(rq)]).astype(np.int64)
+        back = torch.empty(int(scnt.sum()), dtype=torch.int64)
+        dist.all_to_all_single(back, torch.as_tensor(np.diff(poffs)), output_split_sizes=scnt.tolist(),
+                               input_split_sizes=rq, group=grp)
+        bounds = poffs[rd]
+        sid = torch.as_tensor(np.diff(bounds))
+        rid = torch.empty(G, dtype=torch.int64)
+        dist.all_to_all_single(rid, sid, group=grp)
+        rids = torch.empty(int(rid.sum()), dtype=torch.int64)
         dist.all_to_all_single(rids, torch.as_tensor(np.asarray(pids, np.int64)[bounds[0]:bounds[-1]]),
-                               output_split_sizes=rsz.tolist(), input_split_sizes=scnt.tolist(), group=grp)
-        # 4. merge the G sorted partial lists of every own query
-        rcnt = rcnt.numpy().reshape(G, M[r])
-        parts, base = [], 0
+                               output_split_sizes=rid.tolist(), input_split_sizes=sid.tolist(), group=grp)
+        # 5. merge: own query q's run from destination j is its place in what was sent to j
+        back = back.numpy()
+        rids = rids.numpy()
+        parts, cb, ib = [], 0, 0
         for j in range(G):
-            o = np.concatenate([[0], np.cumsum(rcnt[j])]).astype(np.int64)
-            parts.append((o, rids.numpy()[base:base + int(o[-1])]))
-            base += int(o[-1])
-        return merge_partials(parts)
+            c = back[cb:cb + len(dest[j])]
+            cb += len(dest[j])
+            counts = np.zeros(mr, np.int64)
+            counts[dest[j]] = c
+            o = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            parts.append((o, rids[ib:ib + int(c.sum())]))
+            ib += int(c.sum())
+        return merge_partials(parts) if mr else (np.zeros(1, np.int64), np.zeros(0, np.int64))
 
     def close(self):
         if self.ctx is not None:

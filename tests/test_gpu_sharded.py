@@ -149,6 +149,45 @@ def test_local_group_big_windows_many_ranks_per_query(native):
     assert np.array_equal(offs, f_offs) and np.array_equal(ids, f_ids)
 
 
+def test_local_group_repeated_ticks(native):
+    """Several ticks through the same three contexts (graphs replayed, routing per tick, capacity
+    replays of single ranks) keep matching the unsharded tick."""
+    G = 3
+    group = native.LocalGroup(G)
+    ctxs = [native.NativeContext(64, 12, True) for _ in range(G)]
+    for r, cx in enumerate(ctxs):
+        cx.comm_init_local(group, r)
+    full = native.NativeContext(64, 12, True)
+    for t, side in enumerate([(2.0, 40.0), (2.0, 40.0), (50.0, 250.0), (2.0, 40.0)]):
+        tick = _tick(300 + t, n=30_000, m=2_500, side=side)
+        ids, xs, ys, qxa, qya, qxb, qyb = tick
+        f_offs, f_ids, _ = full.tick_host(ids, xs, ys, np.arange(len(qxa)), qxa, qya, qxb, qyb)
+        rng = np.random.default_rng(t)
+        oc, qc = _cuts(len(ids), G, rng), _cuts(len(qxa), G, rng)
+        outs, errs = [None] * G, []
+
+        def worker(r):
+            try:
+                o0, o1, q0, q1 = oc[r], oc[r + 1], qc[r], qc[r + 1]
+                outs[r] = ctxs[r].tick_sharded_host(ids[o0:o1], xs[o0:o1], ys[o0:o1], qxa[q0:q1], qya[q0:q1],
+                                                    qxb[q0:q1], qyb[q0:q1])
+            except Exception as e:  # pragma: no cover
+                errs.append((r, repr(e)))
+
+        ths = [threading.Thread(target=worker, args=(r,)) for r in range(G)]
+        for x in ths:
+            x.start()
+        for x in ths:
+            x.join(timeout=600)
+        assert not errs, errs
+        offs, res = _concat(outs)
+        assert np.array_equal(offs, f_offs) and np.array_equal(res, f_ids), t
+    for cx in ctxs:
+        cx.close()
+    full.close()
+    group.close()
+
+
 def test_nccl_one_rank_equals_tick(native):
     tick = _tick(21)
     full = native.NativeContext(64, 12, True)

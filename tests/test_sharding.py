@@ -1,9 +1,10 @@
 """Leaf-range sharding across ranks.
 
 CPU: ownership math, partial merging, and world_size-2 gloo runs of
-ShardedEngine's host protocol (gather of the ranks' slices, per-rank partial
-lists, routing to the queries' home ranks, merge) with the oracle restricted
-to the rank's leaves standing in for the device tick.
+ShardedEngine's host protocol (gather of the ranks' objects, queries routed
+to the owners of their leaves, per-rank partial lists, back to the queries'
+home ranks, merge) with the oracle restricted to the rank's leaves standing in
+for the device tick and its routing.
 GPU: sharded contexts on one device reproduce the unsharded tick (the native
 data plane itself: tests/test_gpu_sharded.py).
 """
@@ -75,10 +76,22 @@ def _small_tick(seed=3):
 
 
 def _stub_partial_tick(ids, xs, ys, qxa, qya, qxb, qyb, rank, world):
-    """Stubbed device tick: the full tick's lists restricted to the rank's Morton leaf range."""
+    """Stubbed device tick: the given queries' lists restricted to the rank's Morton leaf range."""
     tick = dict(ids=ids, xs=xs, ys=ys, qids=np.arange(len(qxa), dtype=np.int64), rects=(qxa, qya, qxb, qyb))
     offs, pids, _ = _partial_for_rank(tick, rank, world)
     return offs, pids
+
+
+def _stub_route(ids, xs, ys, qxa, qya, qxb, qyb, rank, world):
+    """Stubbed k_route: the ranks owning the leaves that hold a query's results (the device routes
+    by every leaf the window touches; for the lists, the ranks holding results are what matters)."""
+    m = len(qxa)
+    mask = np.zeros(m, np.uint64)
+    for j in range(world):
+        tick = dict(ids=ids, xs=xs, ys=ys, qids=np.arange(m, dtype=np.int64), rects=(qxa, qya, qxb, qyb))
+        offs, _, _ = _partial_for_rank(tick, j, world)
+        mask |= np.where(np.diff(offs) > 0, np.uint64(1) << np.uint64(j), np.uint64(0))
+    return mask
 
 
 def _gloo_worker(rank, world, port, out):
@@ -96,7 +109,8 @@ def _gloo_worker(rank, world, port, out):
         ob = [0, n // 3, n] if world == 2 else [r * n // world for r in range(world + 1)]
         qb = [0, 2 * m // 3, m] if world == 2 else [r * m // world for r in range(world + 1)]
         o0, o1, q0, q1 = ob[rank], ob[rank + 1], qb[rank], qb[rank + 1]
-        eng = ShardedEngine(MethodConfig(method="quad", th_quad=64), partial_tick=_stub_partial_tick)
+        eng = ShardedEngine(MethodConfig(method="quad", th_quad=64), partial_tick=_stub_partial_tick,
+                            route=_stub_route)
         (offs, ids), _ = eng.process_shard(full["ids"][o0:o1], full["xs"][o0:o1], full["ys"][o0:o1],
                                            *(r_[q0:q1] for r_ in full["rects"]))
         eng.close()
