@@ -84,11 +84,14 @@ def ncu_traffic(kernel: str):
     """Per-launch dram bytes of `kernel` from the committed ncu summary (profiles/)."""
     import glob
 
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json")), reverse=True):
+    # the newest round first, its final capture before earlier ones
+    paths = glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json"))
+    for p in sorted(paths, key=lambda q: (os.path.basename(q)[:3], "final" in q, q), reverse=True):
         try:
             with open(p) as fp:
                 d = json.load(fp)
-            k = d.get("kernels", {}).get(kernel)
+            ks = d.get("kernels", {})
+            k = ks.get(kernel) or next((v for name, v in ks.items() if name.startswith(kernel + "<")), None)
             if k and k.get("dram_bytes_per_launch"):
                 return float(k["dram_bytes_per_launch"]), os.path.relpath(p, ROOT)
         except Exception:
