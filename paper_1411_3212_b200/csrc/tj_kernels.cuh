@@ -955,6 +955,10 @@ constexpr int kTableMinQ = TJ_TMQ;            // table path from this many subqu
 #define TJ_JOIN_TPS 1
 #endif
 constexpr bool kJoinTPS = TJ_JOIN_TPS != 0;   // table path: one thread per subquery (0: per (subquery, block))
+#ifndef TJ_JOIN_ODD
+#define TJ_JOIN_ODD 1
+#endif
+constexpr bool kJoinOdd = TJ_JOIN_ODD != 0;   // odd pair stride of the table rows (bank spread)
 
 
 // Optional row padding (TJ_ROW_PAD=8: bitmap rows padded to whole 32-byte
@@ -1055,7 +1059,7 @@ struct JoinSmem {
   double ox[2][kTileBuf];                 // tile objects, two stages
   double oy[2][kTileBuf];
   unsigned long long bar[2];              // mbarriers of the two stages
-  uint32_t tab[2 * kRows * kTileBlocks];  // [axis][k][b], row stride = tile blocks
+  uint32_t tab[2 * kRows * (kTileBlocks + 2)];  // [axis][k][b], row stride >= tile blocks
   ushort4 kb[kQC];                        // bucket of xa, xb, ya, yb
   int32_t cnt[kQC];
 };
@@ -1155,7 +1159,10 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
     const int nbp = row_words(nb);  // row stride (sector-padded)
     const int32_t sbase = li.z;
     const bool table = nisq >= kTableMinQ;
-    const int nbs = kJoinTPS ? (nbt + 1) & ~1 : nbt;  // table row stride (even: paired 8-byte lookups)
+    // table row stride in words: even for paired 8-byte lookups; with one thread per subquery its
+    // pairs per row are odd, so the random rows of a warp's subqueries spread over the banks
+    // (4 pairs per row put every row start on one of 4 bank pairs: 8-way conflicts)
+    const int nbs = (kJoinTPS && n_ot == 1) ? (kJoinOdd ? 2 * (((nbt + 1) >> 1) | 1) : (nbt + 1) & ~1) : nbt;
     // ---- this unit's objects (bulk-copied into stage stg) ----------------------
     mbar_wait(&S.bar[stg], (uint32_t)((iter >> 1) & 1));
     const double* ox = S.ox[stg] + (ob & 1);
@@ -1379,7 +1386,19 @@ __global__ void __launch_bounds__(256) k_cov_counts(const Dev d) {
 __global__ void __launch_bounds__(256) k_slot_counts(const Dev d) {
   DevHdr* h = d.h;
   if (h->abort) return;
-  TJ_GRID_STRIDE(s, h->S) d.sq_count[s] = d.ecount[d.sq_le[s].y];
+  const int64_t S = h->S;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t s0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s0 < S; s0 += 4 * stride) {
+    int32_t e[4];  // four slot -> entry -> count chains in flight
+#pragma unroll
+    for (int u = 0; u < 4; ++u) e[u] = s0 + u * stride < S ? d.sq_le[s0 + u * stride].y : 0;
+    int32_t c[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) c[u] = s0 + u * stride < S ? d.ecount[e[u]] : 0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (s0 + u * stride < S) d.sq_count[s0 + u * stride] = c[u];
+  }
 }
 
 __global__ void k_close_offsets(const Dev d) {
