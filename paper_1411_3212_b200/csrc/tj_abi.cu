@@ -81,6 +81,7 @@ struct tj_ctx {
   int64_t scan_words = 0;  // look-back scan state words (tile counter + tiles)
   bool lb_scan = false;       // single-pass look-back scan (measured slower here than reduce-then-scan)
   bool serial_sort = false;   // TJ_SERIAL_SORT=1: object sort on the main stream (for measuring K1 alone)
+  bool check_tiling = false;  // TJ_CHECK_TILING=1: the build_zmap tiling check on the device (TilingGap)
   bool sort_xy = false;       // TJ_SORT_XY=1: coordinates carried through the radix passes (no gathers)
   // adaptive rebuild: the last built index (header fields + the buffers it lives in)
   bool have_index = false;
@@ -471,6 +472,7 @@ int launch_stage(tj_ctx* c, int stage) {
       }
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
+      if (c->check_tiling) k_check_tiling<<<Gbig, 256, 0, st>>>(d);
       if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range, before the scatter,
                              // and block bases over its own leaves (only their objects are sorted)
         scan_launch(sp, LeafWeightIn{d.leaf_nobj}, PrefOut{d.leaf_wpre}, &h->L, h, &h->shard_total, st);
@@ -482,7 +484,8 @@ int launch_stage(tj_ctx* c, int stage) {
                     st);
       }
       // 3 launches per scan
-      return (c->ug_sf ? 11 : 12 + (c->fused_pyr ? (F + kPyrSpan - 1) / kPyrSpan : F)) + (c->shard_n > 1 ? 4 : 0);
+      return (c->ug_sf ? 11 : 12 + (c->fused_pyr ? (F + kPyrSpan - 1) / kPyrSpan : F)) + (c->shard_n > 1 ? 4 : 0) +
+             (c->check_tiling ? 1 : 0);
     case kSortStage: {  // ---- K1's last part: objects into leaf order (side stream) ----
       cudaStream_t ss = c->serial_sort ? c->st : c->side;
       ScanPlan sp2{std::min(1024, 4 * c->num_sms), P<int64_t>(c->partial2),
@@ -781,6 +784,7 @@ int compute_tick(tj_ctx* c, int64_t n, int64_t m, const int64_t* ids, const doub
     c->key_req = c->key_auto && !c->sort_xy && !c->dup_ids_seen && H.not_identity &&
                  ((H.id_kmax - H.id_kmin) >> kKeyBits) == 0;
     S.id_order = H.key_mode ? TJ_IDS_KEYED : (!H.not_monotone ? TJ_IDS_MONOTONE : TJ_IDS_SORTED);
+    if (H.tiling_gap) return fail(c, TJ_E_TILING_GAP, "leaves do not tile the deepest-level grid");
     if (H.dup) return fail(c, TJ_E_DUPLICATE_RESULT, "a (query, object) pair was produced twice");
     if (H.count_mismatch) return fail(c, TJ_E_COUNT_MISMATCH, "decoded counts disagree with popcounts");
     R = H.R;
@@ -957,6 +961,7 @@ int tj_create(const tj_config* cfg, tj_ctx** out) {
   if (const char* sp = std::getenv("TJ_SCATTER_PER_SM")) c->scatter_per_sm = std::max(1, std::atoi(sp));
   if (const char* fp = std::getenv("TJ_FUSED_PYR")) c->fused_pyr = std::atoi(fp) != 0;
   if (const char* ky = std::getenv("TJ_KEYED")) c->key_auto = std::atoi(ky) != 0;
+  if (const char* ct = std::getenv("TJ_CHECK_TILING")) c->check_tiling = std::atoi(ct) != 0;
   cudaSetDevice(c->device);
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
   // side-stream priority (TJ_SIDE_PRIO=1: the object sort's blocks go first) measured no gain:

@@ -63,6 +63,8 @@ struct DevHdr {
   int32_t shard_rank, shard_n;              // leaf-range sharding (n == 1: off)
   int64_t shard_total;                      // total leaf work weight
   int64_t n_sort;                           // objects the leaf sort orders: n, or (sharded) those in own leaves
+  int32_t tiling_gap;                       // TJ_CHECK_TILING: the leaves do not tile the deepest grid
+  int32_t pad2;
   // object ids that are not the input rows ("keyed" lists): every leaf block is put in id order on
   // the device and carries its ids as 32-bit offsets from id_min (Dev::loff), so the decode merges
   // runs and emits ids with leaf-local loads (no per-result random id lookups, no per-list sorts)

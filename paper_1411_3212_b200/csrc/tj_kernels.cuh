@@ -415,6 +415,33 @@ struct ZOut {
   }
 };
 
+// TJ_CHECK_TILING=1: the reference's internal check of build_zmap (quadtree.py:153-157) on the
+// device — leaves in Morton order must tile the 4^l_deep deepest cells without gaps or overlaps
+// (each leaf at level l spans 4^(l_deep - l) cells starting at z * span).  Holds by construction;
+// a debug check, off by default.
+__global__ void __launch_bounds__(256) k_check_tiling(const Dev d) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  const int64_t L = h->L, Z = h->Z;
+  const int ld = h->l_deep;
+  int gap = L == 0;
+  TJ_GRID_STRIDE(r, L) {
+    const uint32_t code = d.leaf_code[r];
+    const int lev = (int)(code >> kLevelShift);
+    const int64_t span = int64_t(1) << (2 * (ld - lev));
+    const int64_t start = (int64_t)(code & kPayloadMask) * span;
+    if (r == 0 && start != 0) gap = 1;
+    if (r + 1 < L) {
+      const uint32_t nc = d.leaf_code[r + 1];
+      const int nl = (int)(nc >> kLevelShift);
+      if ((int64_t)(nc & kPayloadMask) * (int64_t(1) << (2 * (ld - nl))) != start + span) gap = 1;
+    } else if (start + span != Z) {
+      gap = 1;
+    }
+  }
+  if (__any_sync(0xffffffffu, gap) && lane_id() == 0) atomicOr(&h->tiling_gap, 1);
+}
+
 // object -> leaf rank (quadtree.py:161-165) as the radix key; the value of
 // the first radix pass is the input row itself (implicit)
 __global__ void __launch_bounds__(256) k_obj_keys(const Dev d) {

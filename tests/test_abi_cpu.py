@@ -101,3 +101,17 @@ def test_rect_validation():
 
     with pytest.raises(ValueError):
         Rect(1.0, 0.0, 0.0, 1.0)
+
+
+def test_multi_gpu_entry_points_without_a_device():
+    """NCCL is loaded at run time (no link-time dependency): a unique id can be made on any
+    host, and the in-process group used for one-device runs of the sharded tick is plain host
+    state."""
+    from paper_1411_3212_b200 import _native
+
+    uid = _native.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128
+    assert uid != _native.nccl_unique_id()  # a fresh id per call
+    g = _native.LocalGroup(3)
+    assert g.nranks == 3
+    g.close()

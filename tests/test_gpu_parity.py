@@ -540,3 +540,14 @@ def test_device_pointer_tick_and_compact_device_delivery(pkg):
         res = _d2h(out.ids32 if flag else out.ids, out.n_results, np.int32 if flag else np.int64)
         assert np.array_equal(offs.astype(np.int64), o_ref) and np.array_equal(res.astype(np.int64), r_ref)
     ctx.close()
+
+
+@pytest.mark.parametrize("case", CASES[:6], ids=[c.name for c in CASES[:6]])
+def test_device_tiling_check_on_reference_cases(pkg, case, monkeypatch):
+    """TJ_CHECK_TILING=1 runs the reference's build_zmap TilingGap check (quadtree.py:153-157)
+    on the device; real ticks tile the deepest grid, so it passes and changes nothing."""
+    monkeypatch.setenv("TJ_CHECK_TILING", "1")
+    eng = _engine(pkg, case.th_quad, case.l_max, case.covering)
+    res, st = eng.process_columns(*case.inputs())
+    assert np.array_equal(res.offsets, case.res_off) and np.array_equal(res.ids, case.res_ids)
+    eng.close()
