@@ -1286,7 +1286,7 @@ __global__ void __launch_bounds__(kJT) k_join(const Dev d) {
               const int o = (b << 5) + bit;
               if (in_rect(ox[o], oy[o], R)) D[e] |= 1u << bit;
             }
-            if (b < nbt) {
+            if (b < nbt) {  // (pairs as one 8-byte store into even-padded rows: no faster)
               orow[b] = D[e];
               cnt += __popc(D[e]);
             }

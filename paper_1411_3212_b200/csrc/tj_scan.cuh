@@ -361,6 +361,7 @@ k_radix_downsweep(KeySrc keys_in, const int32_t* vals_in, uint32_t* keys_out, in
       const bool ok = i < e;
       // invalid lanes get digit kRadixDigits (the extra bit below)
       dig[r] = ok ? ((key[r] >> shift) & (kRadixDigits - 1)) : (uint32_t)kRadixDigits;
+      // the lanes with this digit: 9 ballots (one match.any instead measured 4% slower per pass)
       uint32_t peers = 0xffffffffu;
 #pragma unroll
       for (int bit = 0; bit <= kRadixBits; ++bit) {
