@@ -761,6 +761,7 @@ int compute_tick(tj_ctx* c, int64_t n, int64_t m, const int64_t* ids, const doub
       }
       S.retries++;
       if (H.abort & (8 | 16)) return fail(c, TJ_E_CUDA, "internal capacity bound violated (leaves)");
+      if (H.abort & 64) return fail(c, TJ_E_INVALID_ARG, "tick too large: 2^32 or more bitmap words");
       if (H.abort & 32) {
         c->obj_passes = passes_for(H.L - 1);
       }

@@ -613,6 +613,7 @@ __global__ void k_check_caps(DevHdr* h, int stage, int radix_bits_obj, int radix
     if (h->S > h->cap_S) atomicOr(&h->abort, 1);
   } else if (stage == 2) {
     if (h->W > h->cap_W || h->U > h->cap_U) atomicOr(&h->abort, 2);
+    if (h->W >= (int64_t)0xffffffffll) atomicOr(&h->abort, 64);  // the decode's 32-bit word offsets
   } else if (stage == 3) {
     if (h->R > h->cap_R) atomicOr(&h->abort, 4);
   }
@@ -1439,6 +1440,7 @@ __global__ void k_close_offsets(const Dev d) {
 __device__ __forceinline__ void st_out(int64_t* p, int64_t v) { __stcs(reinterpret_cast<long long*>(p), (long long)v); }
 
 constexpr int32_t kRowEnd = 0x7fffffff;
+constexpr uint32_t kNoRow = 0xffffffffu;  // a covering slot: its run is the whole leaf block
 
 #ifndef TJ_DQ_WPL
 #define TJ_DQ_WPL 4  // decode phase A: bitmap words in flight per lane
@@ -1773,7 +1775,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
       for (int32_t c0 = slo; c0 < shi; c0 += 32) {
         const int32_t s = c0 + lane;
         int nbw = 0, obase = 0, cs = 0;
-        int64_t wof = -1;
+        uint32_t wof = kNoRow;  // the row's first word (32 bits: the tick's bitmap is < 2^32 words)
         uint32_t tail = 0;
         int2 le = make_int2(0, 0);
         if (s < shi) {  // count and slot loaded together (no dependent round trip)
@@ -1788,7 +1790,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
           obase = li.x;
           nbw = (nobj + 31) >> 5;
           tail = (nobj & 31) ? ((1u << (nobj & 31)) - 1u) : 0xffffffffu;
-          wof = row >= li.w ? -1 : d.leaf_woff[leaf] + (int64_t)row * row_words(nbw);
+          wof = row >= li.w ? kNoRow : (uint32_t)(d.leaf_woff[leaf] + (int64_t)row * row_words(nbw));
         }
         const int pos0 = (int)(d.slot_off[c0] - base);  // output offset of the chunk's first run
         const int winc = warp_incl_scan(nbw);
@@ -1811,11 +1813,11 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
             const int jx = __shfl_sync(0xffffffffu, wexc, j);
             const int jn = __shfl_sync(0xffffffffu, nbw, j);
             const int jo = __shfl_sync(0xffffffffu, obase, j);
-            const int64_t jw = __shfl_sync(0xffffffffu, wof, j);
+            const uint32_t jw = __shfl_sync(0xffffffffu, wof, j);
             const uint32_t jt = __shfl_sync(0xffffffffu, tail, j);
             const int wb = t - jx;
             w[u] = 0;
-            if (t < TW) w[u] = jw >= 0 ? __ldcs(d.bitmap + jw + wb) : (wb == jn - 1 ? jt : 0xffffffffu);  // read once: evict first
+            if (t < TW) w[u] = jw != kNoRow ? __ldcs(d.bitmap + jw + wb) : (wb == jn - 1 ? jt : 0xffffffffu);  // read once: evict first
             wo[u] = jo + (wb << 5);
           }
 #pragma unroll
