@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) k_mbr(const Dev d) {  // (capped at 64 re
   DevHdr* h = d.h;
   const int64_t n = h->n;
   unsigned long long mnx = ~0ull, mny = ~0ull, mxx = 0ull, mxy = 0ull;
-  unsigned long long imn = ~0ull, imx = 0ull;  // id range (rank mode keys)
+  unsigned long long imn = ~0ull, imx = 0ull;  // id range (keyed lists)
   int bad = 0, notid = 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   // warp-uniform trip count (the next-id shuffle below needs every lane of the warp)
