@@ -1439,6 +1439,15 @@ __global__ void k_close_offsets(const Dev d) {
 // result ids are written once and never re-read on the device: streaming stores
 __device__ __forceinline__ void st_out(int64_t* p, int64_t v) { __stcs(reinterpret_cast<long long*>(p), (long long)v); }
 
+// 4-byte asynchronous global -> shared copy (LDGSTS through L1): the load holds no register while
+// in flight, so a lane can have every lookup of its window outstanding at once
+__device__ __forceinline__ void cp_async4(int32_t* sdst, const int32_t* gsrc) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
+               "l"(gsrc)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 constexpr int32_t kRowEnd = 0x7fffffff;
 constexpr uint32_t kNoRow = 0xffffffffu;  // a covering slot: its run is the whole leaf block
 
@@ -1448,6 +1457,9 @@ constexpr uint32_t kNoRow = 0xffffffffu;  // a covering slot: its run is the who
 #ifndef TJ_DQ_RPL
 #define TJ_DQ_RPL 4  // decode phase B: row lookups in flight per lane
 #endif
+#ifndef TJ_DQ_ASYNC
+#define TJ_DQ_ASYNC 0  // decode phases A+B: each set bit's row lookup issued as a 4-byte cp.async into its slot
+#endif
 #ifndef TJ_DQ_MINB
 #define TJ_DQ_MINB 10  // resident decode CTAs per SM the register budget is cut for
 #endif
@@ -1456,7 +1468,11 @@ constexpr uint32_t kNoRow = 0xffffffffu;  // a covering slot: its run is the who
 #endif
 constexpr int kDQThreads = 128;
 constexpr int kDQWarps = kDQThreads / 32;
-constexpr int kDQStage = 1024;   // results staged per warp window
+#ifndef TJ_DQ_STAGE
+#define TJ_DQ_STAGE 896  // 1024 measured 3% slower: ten CTAs' windows then need the 196 KB shared-memory
+                         // carveout, leaving 60 KB of L1 for the leaf-position lookups instead of 92 KB
+#endif
+constexpr int kDQStage = TJ_DQ_STAGE;   // results staged per warp window
 constexpr int kLaneRuns = 4;     // lane-per-query k-way merge up to this many runs
 
 constexpr int kRankRuns = 32;  // oversized lists (> one window) of 2..32 runs: warp rank merge; more: k_merge_big
@@ -1829,7 +1845,11 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
             while (x) {
               const int bit = __ffs(x) - 1;
               x &= x - 1;
+#if TJ_DQ_ASYNC
+              cp_async4(sa + p++, sidx + wo[u] + bit);  // phase B folded in: the row lookup lands in place
+#else
               sa[p++] = wo[u] + bit;
+#endif
             }
             pos += __shfl_sync(0xffffffffu, inc, 31);
           }
@@ -1838,6 +1858,10 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         const int32_t cend = c0 + 32 < shi ? c0 + 32 : shi;
         bad |= (lane == 0) && (pos0 + pos != d.slot_off[cend] - base);  // CountMismatch (bitmap.py:131-132)
       }
+#if TJ_DQ_ASYNC
+      cp_async_wait_all();
+      __syncwarp();
+#else
       __syncwarp();
       // ---- B: leaf positions -> input rows (independent loads, 4 in flight per lane)
       for (int i0 = 0; i0 < (int)T; i0 += 32 * TJ_DQ_RPL) {
@@ -1854,6 +1878,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         }
       }
       __syncwarp();
+#endif
       // ---- C: store the window (runs concatenated; ids looked up here)
       for (int i = lane; i < (int)T; i += 32) st_out(d.out_ids + base + i, idof(sa[i]));
       __syncwarp();
