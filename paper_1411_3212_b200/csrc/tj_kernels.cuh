@@ -1439,15 +1439,6 @@ __global__ void k_close_offsets(const Dev d) {
 // result ids are written once and never re-read on the device: streaming stores
 __device__ __forceinline__ void st_out(int64_t* p, int64_t v) { __stcs(reinterpret_cast<long long*>(p), (long long)v); }
 
-// 4-byte asynchronous global -> shared copy (LDGSTS through L1): the load holds no register while
-// in flight, so a lane can have every lookup of its window outstanding at once
-__device__ __forceinline__ void cp_async4(int32_t* sdst, const int32_t* gsrc) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(sdst)),
-               "l"(gsrc)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
-
 constexpr int32_t kRowEnd = 0x7fffffff;
 constexpr uint32_t kNoRow = 0xffffffffu;  // a covering slot: its run is the whole leaf block
 
@@ -1457,8 +1448,8 @@ constexpr uint32_t kNoRow = 0xffffffffu;  // a covering slot: its run is the who
 #ifndef TJ_DQ_RPL
 #define TJ_DQ_RPL 4  // decode phase B: row lookups in flight per lane
 #endif
-#ifndef TJ_DQ_ASYNC
-#define TJ_DQ_ASYNC 0  // decode phases A+B: each set bit's row lookup issued as a 4-byte cp.async into its slot
+#ifndef TJ_DQ_TWGUARD
+#define TJ_DQ_TWGUARD 1  // decode phase A: skip the word batches past a chunk's last word (warp-uniform; C5 decode -1.2%)
 #endif
 #ifndef TJ_DQ_MINB
 #define TJ_DQ_MINB 10  // resident decode CTAs per SM the register budget is cut for
@@ -1820,6 +1811,11 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
 #pragma unroll
           for (int u = 0; u < TJ_DQ_WPL; ++u) {
             const int t = t0 + u * 32 + lane;
+            w[u] = 0;
+            wo[u] = 0;
+#if TJ_DQ_TWGUARD
+            if (t0 + u * 32 >= TW) continue;  // warp-uniform: no search for batches past the chunk's words
+#endif
             int j = 0;
 #pragma unroll
             for (int step = 16; step > 0; step >>= 1) {
@@ -1832,12 +1828,14 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
             const uint32_t jw = __shfl_sync(0xffffffffu, wof, j);
             const uint32_t jt = __shfl_sync(0xffffffffu, tail, j);
             const int wb = t - jx;
-            w[u] = 0;
             if (t < TW) w[u] = jw != kNoRow ? __ldcs(d.bitmap + jw + wb) : (wb == jn - 1 ? jt : 0xffffffffu);  // read once: evict first
             wo[u] = jo + (wb << 5);
           }
 #pragma unroll
           for (int u = 0; u < TJ_DQ_WPL; ++u) {
+#if TJ_DQ_TWGUARD
+            if (t0 + u * 32 >= TW) break;
+#endif
             uint32_t x = w[u];
             const int c = __popc(x);
             const int inc = warp_incl_scan(c);
@@ -1845,11 +1843,7 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
             while (x) {
               const int bit = __ffs(x) - 1;
               x &= x - 1;
-#if TJ_DQ_ASYNC
-              cp_async4(sa + p++, sidx + wo[u] + bit);  // phase B folded in: the row lookup lands in place
-#else
               sa[p++] = wo[u] + bit;
-#endif
             }
             pos += __shfl_sync(0xffffffffu, inc, 31);
           }
@@ -1858,10 +1852,6 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         const int32_t cend = c0 + 32 < shi ? c0 + 32 : shi;
         bad |= (lane == 0) && (pos0 + pos != d.slot_off[cend] - base);  // CountMismatch (bitmap.py:131-132)
       }
-#if TJ_DQ_ASYNC
-      cp_async_wait_all();
-      __syncwarp();
-#else
       __syncwarp();
       // ---- B: leaf positions -> input rows (independent loads, 4 in flight per lane)
       for (int i0 = 0; i0 < (int)T; i0 += 32 * TJ_DQ_RPL) {
@@ -1878,7 +1868,6 @@ __global__ void __launch_bounds__(kDQThreads, TJ_DQ_MINB) k_decode_query(const D
         }
       }
       __syncwarp();
-#endif
       // ---- C: store the window (runs concatenated; ids looked up here)
       for (int i = lane; i < (int)T; i += 32) st_out(d.out_ids + base + i, idof(sa[i]));
       __syncwarp();

@@ -12,7 +12,7 @@ for w in ${WLS:-C5}; do
   for v in ${VARIANTS:-default}; do
     if [ $v = default ]; then unset TJ_LIB_PATH; else export TJ_LIB_PATH=$PWD/paper_1411_3212_b200/_lib/exp_$v.so; fi
     timeout 900 python bench.py --workload $w --steps ${STEPS:-20} --warmup 5 --no-e2e --no-cpu-baseline \
-      > gpurun_out/sweep_${w}_$v.log 2>&1
+      >> gpurun_out/sweep_${w}_$v.log 2>&1
     echo "rc=$?" >> gpurun_out/sweep_${w}_$v.log
   done
 done
