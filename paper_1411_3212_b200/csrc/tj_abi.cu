@@ -7,6 +7,10 @@
 #include "tickjoin_b200.h"
 #include "tj_kernels.cuh"
 
+#ifndef TJ_ZMAP_GENERIC
+#define TJ_ZMAP_GENERIC 0  // 1: the zmap through the generic scan (ZFlagIn / ZOut) instead of k_zmap_count / k_zmap_rank
+#endif
+
 #include <algorithm>
 #include <cstdio>
 #include <functional>
@@ -470,7 +474,13 @@ int launch_stage(tj_ctx* c, int stage) {
         k_finalize_index<<<1, 1, 0, st>>>(h);
         k_cell_level<<<Gbig, 256, 0, st>>>(d);
       }
+#if TJ_ZMAP_GENERIC
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
+#else
+      k_zmap_count<<<sp.G, 256, 0, st>>>(d, sp.partial);
+      k_scan_partials<<<1, 1024, 0, st>>>(sp.partial, sp.G, &h->L, h);
+      k_zmap_rank<<<sp.G, 256, 0, st>>>(d, sp.partial);
+#endif
       k_check_caps<<<1, 1, 0, st>>>(h, 0, kRadixBits * c->obj_passes, 32);
       if (c->check_tiling) k_check_tiling<<<Gbig, 256, 0, st>>>(d);
       if (c->shard_n > 1) {  // leaf-range sharding: this rank's contiguous Morton range, before the scatter,

@@ -415,6 +415,98 @@ struct ZOut {
   }
 };
 
+// The zmap scan specialised (the generic scan moves 8-byte values through a
+// shared-memory tile per cell): 16 consecutive cells per thread, their levels in
+// one 16-byte load, leaf starts as a 16-bit mask, int32 block scan of the
+// masks' popcounts, the 16 zmap entries as four 16-byte stores.  Two passes
+// (starts per block, then ranks) around k_scan_partials; blocks own contiguous
+// chunks of whole 4096-cell tiles.
+constexpr int kZPer = 16, kZTile = 256 * kZPer;
+__device__ __forceinline__ void zmap_chunk(int64_t Z, int64_t* b, int64_t* e) {
+  const int64_t chunk = ((Z + gridDim.x - 1) / gridDim.x + kZTile - 1) / kZTile * kZTile;
+  *b = (int64_t)blockIdx.x * chunk;
+  *e = *b + chunk < Z ? *b + chunk : Z;
+}
+// leaf-start mask of cells c0 .. c0+15 (bit k: cell c0+k is the first deepest cell of its leaf) and their levels
+__device__ __forceinline__ uint32_t zmap_starts(const uint8_t* clev, int64_t c0, int64_t e, int ld, uint8_t lv[kZPer]) {
+  if (c0 + kZPer <= e) {
+    const uint4 q = *reinterpret_cast<const uint4*>(clev + c0);
+    const uint32_t wds[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int k = 0; k < kZPer; ++k) lv[k] = (uint8_t)(wds[k >> 2] >> (8 * (k & 3)));
+  } else {
+#pragma unroll
+    for (int k = 0; k < kZPer; ++k) lv[k] = c0 + k < e ? clev[c0 + k] : (uint8_t)ld;
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int k = 0; k < kZPer; ++k) {
+    const int64_t span_mask = (int64_t(1) << (2 * (ld - lv[k]))) - 1;
+    m |= (c0 + k < e && ((c0 + k) & span_mask) == 0) ? (1u << k) : 0u;
+  }
+  return m;
+}
+
+__global__ void __launch_bounds__(256) k_zmap_count(const Dev d, int64_t* partial) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  __shared__ int64_t sh[33];
+  int64_t b, e;
+  zmap_chunk(h->Z, &b, &e);
+  const int ld = h->l_deep;
+  int64_t cnt = 0;
+  for (int64_t base = b; base < e; base += kZTile) {
+    uint8_t lv[kZPer];
+    cnt += __popc(zmap_starts(d.clev, base + threadIdx.x * kZPer, e, ld, lv));
+  }
+  cnt = warp_sum(cnt);
+  if (lane_id() == 0) sh[threadIdx.x >> 5] = cnt;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    int64_t v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) partial[blockIdx.x] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_zmap_rank(const Dev d, const int64_t* partial) {
+  DevHdr* h = d.h;
+  if (h->abort) return;
+  __shared__ int32_t sh[33];
+  int64_t b, e;
+  zmap_chunk(h->Z, &b, &e);
+  const int ld = h->l_deep;
+  int64_t carry = partial[blockIdx.x];
+  for (int64_t base = b; base < e; base += kZTile) {
+    const int64_t c0 = base + threadIdx.x * kZPer;
+    uint8_t lv[kZPer];
+    const uint32_t m = zmap_starts(d.clev, c0, e, ld, lv);
+    int32_t tot;
+    const int64_t ex = carry + block_excl_scan((int32_t)__popc(m), sh, &tot);
+    uint32_t z[kZPer];
+#pragma unroll
+    for (int k = 0; k < kZPer; ++k) {
+      const int64_t rank = ex + __popc(m & ((2u << k) - 1u)) - 1;  // leaf starts at or before the cell, less one
+      z[k] = ((uint32_t)lv[k] << kLevelShift) | (uint32_t)rank;
+      if (((m >> k) & 1u) && rank < h->cap_L) {
+        const uint32_t zc = (uint32_t)((c0 + k) >> (2 * (ld - lv[k])));
+        d.leaf_code[rank] = ((uint32_t)lv[k] << kLevelShift) | zc;
+        d.leaf_nobj[rank] = (int32_t)node_count(d, h->F, lv[k], zc);
+      }
+    }
+    if (c0 + kZPer <= e) {
+      uint4* dst = reinterpret_cast<uint4*>(d.zmap + c0);
+#pragma unroll
+      for (int k = 0; k < kZPer / 4; ++k) dst[k] = make_uint4(z[4 * k], z[4 * k + 1], z[4 * k + 2], z[4 * k + 3]);
+    } else {
+#pragma unroll
+      for (int k = 0; k < kZPer; ++k)
+        if (c0 + k < e) d.zmap[c0 + k] = z[k];
+    }
+    carry += tot;
+  }
+}
+
 // TJ_CHECK_TILING=1: the reference's internal check of build_zmap (quadtree.py:153-157) on the
 // device — leaves in Morton order must tile the 4^l_deep deepest cells without gaps or overlaps
 // (each leaf at level l spans 4^(l_deep - l) cells starting at z * span).  Holds by construction;
