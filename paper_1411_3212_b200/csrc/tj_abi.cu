@@ -472,12 +472,15 @@ int launch_stage(tj_ctx* c, int stage) {
           for (int l = F - 1; l >= 0; --l) k_pyr_level<<<grid_for(c, int64_t(1) << (2 * l)), 256, 0, st>>>(d, l);
         }
         k_finalize_index<<<1, 1, 0, st>>>(h);
+#if TJ_ZMAP_GENERIC
         k_cell_level<<<Gbig, 256, 0, st>>>(d);
+#endif
       }
 #if TJ_ZMAP_GENERIC
       scan_launch(sp, ZFlagIn{d.clev, h}, ZOut{d}, &h->Z, h, &h->L, st);
 #else
-      k_zmap_count<<<sp.G, 256, 0, st>>>(d, sp.partial);
+      if (c->ug_sf) k_zmap_count<false><<<sp.G, 256, 0, st>>>(d, sp.partial);
+      else k_zmap_count<true><<<sp.G, 256, 0, st>>>(d, sp.partial);  // leaf levels computed here (k_cell_level fused)
       k_scan_partials<<<1, 1024, 0, st>>>(sp.partial, sp.G, &h->L, h);
       k_zmap_rank<<<sp.G, 256, 0, st>>>(d, sp.partial);
 #endif
@@ -494,7 +497,7 @@ int launch_stage(tj_ctx* c, int stage) {
                     st);
       }
       // 3 launches per scan
-      return (c->ug_sf ? 11 : 12 + (c->fused_pyr ? (F + kPyrSpan - 1) / kPyrSpan : F)) + (c->shard_n > 1 ? 4 : 0) +
+      return (c->ug_sf ? 11 : 12 - (TJ_ZMAP_GENERIC ? 0 : 1) + (c->fused_pyr ? (F + kPyrSpan - 1) / kPyrSpan : F)) + (c->shard_n > 1 ? 4 : 0) +
              (c->check_tiling ? 1 : 0);
     case kSortStage: {  // ---- K1's last part: objects into leaf order (side stream) ----
       cudaStream_t ss = c->serial_sort ? c->st : c->side;

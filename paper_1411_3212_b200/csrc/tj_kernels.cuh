@@ -447,17 +447,71 @@ __device__ __forceinline__ uint32_t zmap_starts(const uint8_t* clev, int64_t c0,
   return m;
 }
 
+// k_cell_level for an aligned group of 16 deepest cells (l_deep >= 2): they share
+// every ancestor down to level l_deep - 2, so that part of the walk is done once;
+// level l_deep - 1 has four ancestors; at l_deep the walk ends anyway.
+__device__ __forceinline__ void group_levels(const Dev& d, int64_t c0, int ld, int lmax, uint32_t th,
+                                             uint8_t lv[kZPer]) {
+  int lev = 0;
+  for (int l = 1; l <= ld - 2; ++l) {
+    const uint32_t cnt = node_count(d, 0, l, (uint32_t)(c0 >> (2 * (ld - l))));
+    if (cnt <= th || l == lmax) {
+      lev = l;
+      break;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    int lj = lev;
+    if (!lev) {
+      const uint32_t cnt = node_count(d, 0, ld - 1, (uint32_t)(c0 >> 2) + j);
+      lj = (cnt <= th || ld - 1 == lmax) ? ld - 1 : ld;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lv[4 * j + i] = (uint8_t)lj;
+  }
+}
+
+// kLevels: compute the cells' leaf levels from the pyramid and store them (the
+// quadtree; fused k_cell_level); otherwise read them (the uniform grid's).
+template <bool kLevels>
 __global__ void __launch_bounds__(256) k_zmap_count(const Dev d, int64_t* partial) {
   DevHdr* h = d.h;
   if (h->abort) return;
   __shared__ int64_t sh[33];
   int64_t b, e;
   zmap_chunk(h->Z, &b, &e);
-  const int ld = h->l_deep;
+  const int ld = h->l_deep, lmax = h->l_max;
+  const uint32_t th = (uint32_t)h->th;
   int64_t cnt = 0;
   for (int64_t base = b; base < e; base += kZTile) {
+    const int64_t c0 = base + threadIdx.x * kZPer;
+    if (kLevels && c0 < e) {
+      uint8_t lv[kZPer];
+      if (ld >= 2) {  // Z = 4^ld is a multiple of 16: whole groups
+        group_levels(d, c0, ld, lmax, th, lv);
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          w[k] = (uint32_t)lv[4 * k] | ((uint32_t)lv[4 * k + 1] << 8) | ((uint32_t)lv[4 * k + 2] << 16) |
+                 ((uint32_t)lv[4 * k + 3] << 24);
+        *reinterpret_cast<uint4*>(d.clev + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+      } else {  // a single-level tree: the per-cell walk
+        for (int64_t c = c0; c < c0 + kZPer && c < e; ++c) {
+          int lev = ld;
+          for (int l = 1; l <= ld; ++l) {
+            const uint32_t n = node_count(d, 0, l, (uint32_t)(c >> (2 * (ld - l))));
+            if (n <= th || l == lmax) {
+              lev = l;
+              break;
+            }
+          }
+          d.clev[c] = (uint8_t)lev;
+        }
+      }
+    }
     uint8_t lv[kZPer];
-    cnt += __popc(zmap_starts(d.clev, base + threadIdx.x * kZPer, e, ld, lv));
+    cnt += __popc(zmap_starts(d.clev, c0, e, ld, lv));
   }
   cnt = warp_sum(cnt);
   if (lane_id() == 0) sh[threadIdx.x >> 5] = cnt;
