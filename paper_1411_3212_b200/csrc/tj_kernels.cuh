@@ -275,25 +275,30 @@ __global__ void __launch_bounds__(256) k_pyr_fused(const Dev d, int lo, int hi) 
   __shared__ uint32_t buf[2][1024];
   const uint32_t th = (uint32_t)h->th;
   const int64_t node = blockIdx.x;  // at level lo
-  // level hi-1 from the global level hi
+  int deep = 0;  // deepest level a split of this thread's nodes creates (one atomic per warp at the end)
+  // level hi-1 from the global level hi: every child load issued before any is used
   {
+    constexpr int kIt = 4;  // level-(hi-1) nodes per thread: 4^(kPyrSpan-1) <= 4 * 256
     const int l = hi - 1;
-    const int64_t per = int64_t(1) << (2 * (l - lo));  // level-l nodes under this CTA's node
+    const int per = 1 << (2 * (l - lo));  // level-l nodes under this CTA's node
     const uint32_t* child = d.pyr + pyr_off(hi);
     uint32_t* self = d.pyr + pyr_off(l);
     const bool can_split = l >= 1 && l < h->l_max;
-    for (int64_t k0 = 0; k0 < per; k0 += blockDim.x) {
-      const int64_t k = k0 + threadIdx.x;
-      bool split = false;
+    uint4 c[kIt];
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int k = it * 256 + threadIdx.x;
+      c[it] = k < per ? *reinterpret_cast<const uint4*>(child + 4 * (node * per + k)) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int it = 0; it < kIt; ++it) {
+      const int k = it * 256 + threadIdx.x;
       if (k < per) {
-        const int64_t z = node * per + k;
-        const uint4 c = *reinterpret_cast<const uint4*>(child + 4 * z);
-        const uint32_t sum = c.x + c.y + c.z + c.w;
-        self[z] = sum;
+        const uint32_t sum = c[it].x + c[it].y + c[it].z + c[it].w;
+        self[node * per + k] = sum;
         buf[(hi - 1 - lo) & 1][k] = sum;
-        split = can_split && sum > th;
+        if (can_split && sum > th) deep = max(deep, l + 1);
       }
-      note_split(h, split, l + 1);
     }
   }
   __syncthreads();
@@ -303,19 +308,16 @@ __global__ void __launch_bounds__(256) k_pyr_fused(const Dev d, int lo, int hi) 
     uint32_t* dst = buf[(l - lo) & 1];
     uint32_t* self = d.pyr + pyr_off(l);
     const bool can_split = l >= 1 && l < h->l_max;
-    for (int64_t k0 = 0; k0 < per; k0 += blockDim.x) {
-      const int64_t k = k0 + threadIdx.x;
-      bool split = false;
-      if (k < per) {
-        const uint32_t sum = src[4 * k] + src[4 * k + 1] + src[4 * k + 2] + src[4 * k + 3];
-        self[node * per + k] = sum;
-        dst[k] = sum;
-        split = can_split && sum > th;
-      }
-      note_split(h, split, l + 1);
+    for (int64_t k = threadIdx.x; k < per; k += blockDim.x) {
+      const uint32_t sum = src[4 * k] + src[4 * k + 1] + src[4 * k + 2] + src[4 * k + 3];
+      self[node * per + k] = sum;
+      dst[k] = sum;
+      if (can_split && sum > th) deep = max(deep, l + 1);
     }
     __syncthreads();
   }
+  deep = __reduce_max_sync(0xffffffffu, deep);
+  if (lane_id() == 0 && deep > *(volatile int*)&h->l_deep) atomicMax(&h->l_deep, deep);
 }
 
 __global__ void k_finalize_index(DevHdr* h) {
