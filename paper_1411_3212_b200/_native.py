@@ -84,6 +84,25 @@ EXPORTED = (
 _lib: Optional[ctypes.CDLL] = None
 
 
+def _prefer_torch_nccl() -> None:
+    """Point the library's NCCL loader (TJ_NCCL_LIB) at the NCCL wheel torch links against, so
+    both share one libnccl.so.2 in the process whichever loads first (an older system NCCL
+    loaded first would be reused by torch and lack symbols it needs)."""
+    if os.environ.get("TJ_NCCL_LIB"):
+        return
+    import importlib.util
+
+    try:
+        spec = importlib.util.find_spec("nvidia.nccl")
+    except (ImportError, ValueError):
+        return
+    for d in (spec.submodule_search_locations or []) if spec else []:
+        cand = os.path.join(d, "lib", "libnccl.so.2")
+        if os.path.exists(cand):
+            os.environ["TJ_NCCL_LIB"] = cand
+            return
+
+
 def load_library() -> ctypes.CDLL:
     """Load the in-tree native library (raises DeviceError if it is not built)."""
     global _lib
@@ -92,6 +111,7 @@ def load_library() -> ctypes.CDLL:
     if not os.path.exists(LIB_PATH):
         raise errors.DeviceError(
             f"native library missing: {LIB_PATH} (run __graft_entry__.build()); there is no CPU fallback")
+    _prefer_torch_nccl()
     lib = ctypes.CDLL(LIB_PATH)
     i64p = POINTER(c_int64)
     lib.tj_abi_version.restype = c_int
